@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""bench.py -- Coop window-search benchmark (BASELINE.json config 4) on 1..8 B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl coop|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU, NCCL)
+
+A "step" is one pass of the batched search hot path (load the SoA
+block tables, h = c/s, span/cost prefix scans, per-start window ends, argmin, exact verify,
+output) over the rank's whole shard: 2^20 pools x 4096 blocks per GPU (weak scaling: each
+rank owns the pools [rank * 2^20, (rank + 1) * 2^20) of the global counter-based sequence
+and generates them on its own device, untimed; no data-path collective).  Inputs are
+96 GiB per GPU >> 126 MB L2, so no L2 flush is needed between steps.
+
+Rank 0 prints ONE JSON line.  `value` = pools searched per second over all ranks
+(max-over-ranks device time); `roofline` = algorithmic HBM bytes per launch / measured
+kernel time vs MEASURED_PEAKS.json; `cpu_baseline` = the CPU oracle (oracle/) timed on this
+box's host cores on a bounded sample; `e2e` = the same metric through the host-buffer C-ABI
+entry point (coop_window_search_batched_host) with H2D/D2H copies inside the timed region.
+`--impl reference` times the oracle itself (rank 0 only) on bounded samples per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_BLOCKS = 4096
+POOLS_PER_GPU = 1 << 20
+ALGO_BYTES_PER_POOL = 24 * N_BLOCKS + 8 + 32  # size_state+cost+stale, request, result
+SEED = 0
+METRIC = "window-search queries/s"
+UNIT = "queries/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="coop", choices=["coop", "reference"])
+    ap.add_argument("--pools", type=int, default=POOLS_PER_GPU, help="pools per GPU")
+    ap.add_argument("--e2e-pools", type=int, default=65536)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="CPU work budget of the oracle baseline sample")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- peaks
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the search kernel from the committed ncu --set full capture"""
+    p = os.path.join(ROOT, "profiles", "search_ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d
+    return None
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+                power.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------- oracle baseline
+def _oracle_worker(args):
+    """Runs in a worker process: generate a contiguous slice of the workload's pools on the
+    host, wait for all workers, then time the oracle on it."""
+    p0, n_pools, barrier = args
+    from gen import pools as G
+    from oracle import oracle as O
+    ss, c, s, r = G.bench_pools_host(G.MODE_BENCH, SEED, p0, n_pools, N_BLOCKS)
+    barrier.wait()
+    t = time.perf_counter()
+    O.search_many(ss, c, s, r, n_pools, N_BLOCKS, N_BLOCKS)
+    return n_pools, time.perf_counter() - t
+
+
+def cpu_baseline(cpu_seconds: float, sample_offset: int = 0):
+    cores = os.cpu_count() or 1
+    per_pool_s = 0.004  # oracle ~4 ms per 4096-block pool (one core), to size the sample
+    per_worker = max(2, int(cpu_seconds / per_pool_s / cores))
+    per_worker += per_worker % 2  # even: short and long requests alike
+    ctx = mp.get_context("fork")
+    with ctx.Manager() as m:
+        barrier = m.Barrier(cores)
+        with ctx.Pool(cores) as pool:
+            res = pool.map(_oracle_worker, [(sample_offset + w * per_worker, per_worker, barrier)
+                                            for w in range(cores)])
+    total = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return {"value": total / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{total} pools x {N_BLOCKS} blocks (global pools "
+                      f"[{sample_offset}, {sample_offset + total})), one process per core, "
+                      f"C oracle O(N*L) per pool, wall {wall:.2f} s"}
+
+
+# ------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    per_worker = 4
+    ctx = mp.get_context("fork")
+    times = []
+    total = 0
+    with ctx.Manager() as m:
+        with ctx.Pool(cores) as pool:
+            for step in range(args.warmup + args.steps):
+                barrier = m.Barrier(cores)
+                off = step * cores * per_worker
+                res = pool.map(_oracle_worker, [(off + w * per_worker, per_worker, barrier)
+                                                for w in range(cores)])
+                if step >= args.warmup:
+                    times.append(max(r[1] for r in res))
+                    total += sum(r[0] for r in res)
+    t = sum(times)
+    value = total / t
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config4-sample: batched window search, 4096-block pools "
+                                   "(bounded sample per step)",
+                       "pools_per_step": cores * per_worker, "n_blocks": N_BLOCKS},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{cores * per_worker} pools per step, one process per core"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from gen import pools as G
+    from paper_2311_00591_b200 import coop
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    P, n = args.pools, N_BLOCKS
+    p0 = rank * P
+    ss = torch.empty(P * n, dtype=torch.int64, device=dev)
+    c = torch.empty(P * n, dtype=torch.float64, device=dev)
+    s = torch.empty(P * n, dtype=torch.float64, device=dev)
+    r = torch.empty(P, dtype=torch.int64, device=dev)
+    out = torch.empty(P * 4, dtype=torch.int64, device=dev)
+    G.bench_pools_device(G.MODE_BENCH, SEED, p0, P, n, n, ss, c, s, r)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        coop.window_search_batched(ss, c, s, r, out, P, n, n, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    t_all0 = torch.cuda.Event(enable_timing=True)
+    t_all1 = torch.cuda.Event(enable_timing=True)
+    t_all0.record(stream)
+    for e0, e1 in evs:
+        e0.record(stream)
+        step()
+        e1.record(stream)
+    t_all1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+
+    elapsed_ms = t_all0.elapsed_time(t_all1)
+    kernel_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    if world > 1:
+        t = torch.tensor([elapsed_ms, statistics.mean(kernel_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, kmean = float(t[0]), float(t[1])
+    else:
+        kmean = statistics.mean(kernel_ms)
+
+    # results summary (untimed): status histogram; gather per-rank digests to rank 0
+    res = coop.windows_from_device(out)
+    digest = int(np.bitwise_xor.reduce(res.view(np.uint64)))
+    stat = {str(k): int(v) for k, v in zip(*np.unique(res["status"], return_counts=True))}
+    if world > 1:
+        # the path's only collective: gather of per-shard results (here: shard digests)
+        d = torch.tensor([digest & 0x7FFFFFFFFFFFFFFF], dtype=torch.int64, device=dev)
+        gathered = [torch.zeros_like(d) for _ in range(world)]
+        dist.all_gather(gathered, d)
+
+    # e2e through the host-buffer C-ABI entry (rank-local; pinned host copies, untimed fill)
+    e2e = None
+    Pe = min(args.e2e_pools, P)
+    if Pe > 0:
+        h_ss = torch.empty(Pe * n, dtype=torch.int64, pin_memory=True)
+        h_c = torch.empty(Pe * n, dtype=torch.float64, pin_memory=True)
+        h_s = torch.empty(Pe * n, dtype=torch.float64, pin_memory=True)
+        h_r = torch.empty(Pe, dtype=torch.int64, pin_memory=True)
+        h_ss.copy_(ss[:Pe * n]); h_c.copy_(c[:Pe * n]); h_s.copy_(s[:Pe * n]); h_r.copy_(r[:Pe])
+        h_out = np.empty(Pe, dtype=coop.WINDOW_DTYPE)
+        coop.window_search_batched_host(h_ss, h_c, h_s, h_r, Pe, n, n, out=h_out)  # warm-up
+        k_e2e = 3
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            coop.window_search_batched_host(h_ss, h_c, h_s, h_r, Pe, n, n, out=h_out)
+        te = (time.perf_counter() - t0) / k_e2e
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt[0])
+        same = h_out.tobytes() == res[:Pe].tobytes()
+        e2e = {"value": world * Pe / te, "unit": UNIT,
+               "h2d_bytes_per_step": Pe * n * 24 + Pe * 8, "d2h_bytes_per_step": Pe * 32,
+               "pools_per_gpu": Pe, "matches_device_results": same,
+               "api": "coop_window_search_batched_host (pinned host buffers, chunked "
+                      "H2D/kernel/D2H overlap on 2 streams)"}
+        del h_ss, h_c, h_s, h_r
+
+    value = world * P * args.steps / (elapsed_ms / 1e3)
+    peak, peak_src = peaks()
+    achieved = P * ALGO_BYTES_PER_POOL / (kmean / 1e3) / 1e9
+    tr = ncu_traffic()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_source": peak_src,
+            "traffic": (tr["dram_bytes_per_pool"] * P) if tr else None,
+            "algorithmic_bytes_per_launch": P * ALGO_BYTES_PER_POOL,
+            "kernel": "coop::search_kernel<8>", "kernel_ms_mean": kmean,
+            "frac_of_8TBps": achieved / 8000.0}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_seconds)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "config4: batched window search, 2^20 pools x 4096 "
+                                       "blocks per GPU (BASELINE.json configs[3])",
+                           "pools_per_gpu": P, "n_blocks": N_BLOCKS, "seed": SEED,
+                           "parallelism": f"dp{world} (pool shards, weak scaling)",
+                           "l2": "no flush: 96 GiB of inputs per step per GPU >> 126 MB L2",
+                           "generator": "gen/coop_gen.cu MODE_BENCH (counter-based, on device)"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": args.steps, "clocks": clk,
+                "results": {"status_counts": stat, "xor_digest": f"{digest:016x}"}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

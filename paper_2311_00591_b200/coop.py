@@ -1,0 +1,136 @@
+"""Thin ctypes binding of libcoop (include/coop.h): argument marshalling only.
+
+Every step of the search / replay runs in libcoop's CUDA kernels.  There is no Python or
+CPU fallback: if libcoop.so is missing or cannot load, import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcoop.so")
+
+OK = 0
+INFEASIBLE = 1
+ERR_INVALID_ARG = -1
+ERR_UNKNOWN_ID = -2
+ERR_UNSATISFIABLE = -3
+ERR_THRASHED = -4
+ERR_CUDA = -5
+ERR_NOMEM = -6
+ERR_BAD_STATE = -7
+ERR_UNIMPLEMENTED = -8
+
+FREE, EVICTABLE, PINNED = 0, 1, 2
+MAX_BLOCKS = 8192
+
+# struct coop_window (32 bytes)
+WINDOW_DTYPE = np.dtype([("first", "<i4"), ("last", "<i4"), ("span", "<u8"),
+                         ("cost", "<f8"), ("n_evict", "<i4"), ("status", "<i4")])
+assert WINDOW_DTYPE.itemsize == 32
+
+
+class CoopError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+        self.status = status
+
+
+class TablesSoA(ctypes.Structure):
+    _fields_ = [("size_state", ctypes.c_void_p), ("cost", ctypes.c_void_p),
+                ("stale", ctypes.c_void_p), ("n_pools", ctypes.c_int64),
+                ("n_blocks", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("pool_stride", ctypes.c_int64)]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libcoop.so not built at {LIB_PATH}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(LIB_PATH)
+    lib.coop_status_string.restype = ctypes.c_char_p
+    lib.coop_status_string.argtypes = [ctypes.c_int]
+    lib.coop_version.restype = ctypes.c_char_p
+    lib.coop_window_search_batched.restype = ctypes.c_int
+    lib.coop_window_search_batched.argtypes = [ctypes.POINTER(TablesSoA), ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_void_p]
+    lib.coop_window_search_batched_host.restype = ctypes.c_int
+    lib.coop_window_search_batched_host.argtypes = [ctypes.POINTER(TablesSoA), ctypes.c_void_p,
+                                                    ctypes.c_void_p, ctypes.c_int64]
+    lib.coop__fixed_round_sum_host.restype = ctypes.c_double
+    lib.coop__fixed_round_sum_host.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+    return lib
+
+
+lib = _load()
+
+
+def status_string(status: int) -> str:
+    return lib.coop_status_string(int(status)).decode()
+
+
+def version() -> str:
+    return lib.coop_version().decode()
+
+
+def _ptr(x) -> int:
+    """data pointer of a torch tensor or numpy array"""
+    if hasattr(x, "data_ptr"):
+        return int(x.data_ptr())
+    return int(x.ctypes.data)
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        import torch
+        return int(torch.cuda.current_stream().cuda_stream)
+    if hasattr(stream, "cuda_stream"):
+        return int(stream.cuda_stream)
+    return int(stream)
+
+
+def window_search_batched(size_state, cost, stale, requests, out, n_pools: int, n_blocks: int,
+                          pool_stride: int, stream=None) -> int:
+    """coop_window_search_batched on device buffers (torch CUDA tensors or raw pointers).
+
+    `out` must hold n_pools * 32 bytes (e.g. torch.empty(n_pools * 4, dtype=torch.int64)).
+    Asynchronous on `stream` (default: torch's current stream).  Raises on error status.
+    """
+    t = TablesSoA(_ptr(size_state) if not isinstance(size_state, int) else size_state,
+                  _ptr(cost) if not isinstance(cost, int) else cost,
+                  _ptr(stale) if not isinstance(stale, int) else stale,
+                  int(n_pools), int(n_blocks), 0, int(pool_stride))
+    rc = lib.coop_window_search_batched(
+        ctypes.byref(t), _ptr(requests) if not isinstance(requests, int) else requests,
+        _ptr(out) if not isinstance(out, int) else out, _stream_handle(stream))
+    if rc < 0:
+        raise CoopError(rc, "coop_window_search_batched")
+    return rc
+
+
+def window_search_batched_host(size_state, cost, stale, requests, n_pools: int, n_blocks: int,
+                               pool_stride: int, out=None, chunk_pools: int = 0) -> np.ndarray:
+    """coop_window_search_batched_host on host arrays (numpy or CPU torch, ideally pinned)."""
+    if out is None:
+        out = np.empty(n_pools, dtype=WINDOW_DTYPE)
+    t = TablesSoA(_ptr(size_state), _ptr(cost), _ptr(stale), int(n_pools), int(n_blocks), 0,
+                  int(pool_stride))
+    rc = lib.coop_window_search_batched_host(ctypes.byref(t), _ptr(requests), _ptr(out),
+                                             int(chunk_pools))
+    if rc < 0:
+        raise CoopError(rc, "coop_window_search_batched_host")
+    return out
+
+
+def windows_from_device(out_tensor) -> np.ndarray:
+    """copy a device result buffer to a numpy structured array of coop_window"""
+    raw = out_tensor.cpu().numpy().view(np.uint8)
+    return raw.view(WINDOW_DTYPE)
+
+
+def _fixed_round_sum_host(h: np.ndarray) -> float:
+    """test hook: the CUDA path's 192-bit exact-sum + RN, compiled for the host"""
+    h = np.ascontiguousarray(h, dtype=np.float64)
+    return float(lib.coop__fixed_round_sum_host(h.ctypes.data, h.size))
