@@ -51,6 +51,82 @@ int orc_window_search_many(int64_t n_pools, int32_t n, int64_t stride,
 /* Correctly rounded sum of n doubles (Shewchuk / fsum semantics); exposed for pins. */
 double orc_fsum(const double *x, int64_t n);
 
+
+/* ======================================================================= O2: replay
+ * Step-by-step replay of an allocation trace under one memory budget with the Coop
+ * allocator: Alg. 1, sliding-window eviction (Sec. 3.3), cheap tensor
+ * partitioning (Sec. 3.4), recomputable in-place (Sec. 3.5,
+ * PAPER.md:206-222).  Readings R10-R35 in DESIGN.md.  TEST INFRASTRUCTURE ONLY.
+ */
+#define ORC_PHASE_FWD 0
+#define ORC_PHASE_BWD 1
+#define ORC_PHASE_UPD 2
+
+#define ORC_F_PARTITION 1u            /* cheap tensor partitioning (Sec. 3.4)          */
+#define ORC_F_INPLACE 2u              /* recomputable in-place (Sec. 3.5); off = COW    */
+#define ORC_F_PARTITION_ALL_PHASES 4u /* partition backward/update ops too (R13)       */
+
+typedef struct {
+  int32_t n_tensors, n_ops;
+  const uint64_t *size;       /* [T] bytes, 1 <= size < 2^48                         */
+  const uint8_t *is_param;    /* [T] 1: parameter / optimizer state (unevictable)    */
+  const int32_t *producer;    /* [T] producing op, -1 for parameters                 */
+  const int64_t *cost_us;     /* [M] op compute cost (us), 0 <= cost < 2^40          */
+  const int32_t *out;         /* [M] output tensor (single output, R30)               */
+  const int32_t *inplace_src; /* [M] mutated input tensor or -1                      */
+  const uint8_t *phase;       /* [M] ORC_PHASE_*                                      */
+  const int32_t *in_ptr;      /* [M+1] CSR of op inputs                               */
+  const int32_t *in_idx;      /* [in_ptr[M]]                                          */
+} orc_trace;
+
+typedef struct {
+  uint64_t budget;
+  uint32_t flags;
+  uint32_t class_threshold; /* us per MiB, C1 iff cost*2^20 >= thr*bytes (R14); 0 -> 15 */
+  int32_t max_depth;        /* rematerialization depth bound (R23); 0 -> 512          */
+  int32_t reserved;
+} orc_cfg;
+
+typedef struct {
+  int32_t status;    /* ORC_OK, ORC_UNSATISFIABLE, ORC_THRASHED, ORC_INVALID_ARG         */
+  int32_t fail_op;   /* op index of the failure, -1 for parameter placement / none     */
+  int64_t base_us;   /* sum of op costs, each op once                                    */
+  int64_t total_us;  /* base + recompute costs                                           */
+  int64_t evictions; /* tensors evicted by window searches                               */
+  int64_t remat;     /* rematerializations (recomputes)                                  */
+  int64_t pressure;  /* allocation failures that triggered a window search               */
+  int64_t frag_fail; /* ... of which bytes_free >= size (fragmentation failures)         */
+  int64_t inplace_reuse;
+  int64_t heuristic_evals;      /* EVICTABLE items whose h was formed (R28)             */
+  uint64_t sum_free_bytes_after;/* after each pressure-event placement (R27)            */
+  int64_t sum_free_blocks_after;
+  uint64_t digest;              /* eviction sequence digest (R29)                       */
+  int32_t max_depth;            /* deepest rematerialization recursion                  */
+  int32_t max_blocks;           /* most pool blocks seen                                 */
+  uint64_t budget;
+  int64_t n_events;             /* events written (or that would have been)             */
+} orc_replay_result;
+
+/* event log record */
+#define ORC_EV_PARAM 0   /* parameter placed                    */
+#define ORC_EV_ALLOC 1   /* op output allocated                 */
+#define ORC_EV_INPLACE 2 /* output took the mutated input's block */
+#define ORC_EV_EVICT 3   /* evicted by a window                  */
+#define ORC_EV_FREE 4    /* freed at death (R20, R22)            */
+#define ORC_EV_REMAT 5   /* output of a recompute allocated      */
+#define ORC_EV_EXEC 6    /* op executed (tensor = output)        */
+#define ORC_EV_REXEC 7   /* op re-executed for a rematerialization */
+typedef struct {
+  int32_t kind, op, tensor, pad;
+  uint64_t addr;
+} orc_event;
+
+int orc_replay(const orc_trace *tr, const orc_cfg *cfg, orc_replay_result *res,
+               orc_event *log, int64_t log_cap);
+
+/* Peak of resident bytes in an unbounded, eviction-free replay (R25). */
+uint64_t orc_peak_live(const orc_trace *tr, uint32_t flags);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,3 +70,84 @@ def search_many(size_state, cost, stale, requests, n_pools: int, n: int, stride:
 def fsum(x) -> float:
     x = np.ascontiguousarray(x, np.float64)
     return float(lib().orc_fsum(x.ctypes.data, x.size))
+
+
+# ----------------------------------------------------------------------------- O2 replay
+class _OrcTrace(ctypes.Structure):
+    _fields_ = [("n_tensors", ctypes.c_int32), ("n_ops", ctypes.c_int32),
+                ("size", ctypes.c_void_p), ("is_param", ctypes.c_void_p),
+                ("producer", ctypes.c_void_p), ("cost_us", ctypes.c_void_p),
+                ("out", ctypes.c_void_p), ("inplace_src", ctypes.c_void_p),
+                ("phase", ctypes.c_void_p), ("in_ptr", ctypes.c_void_p),
+                ("in_idx", ctypes.c_void_p)]
+
+
+class _OrcCfg(ctypes.Structure):
+    _fields_ = [("budget", ctypes.c_uint64), ("flags", ctypes.c_uint32),
+                ("class_threshold", ctypes.c_uint32), ("max_depth", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+F_PARTITION, F_INPLACE, F_PARTITION_ALL_PHASES = 1, 2, 4
+UNSATISFIABLE, THRASHED = -3, -4
+EV_PARAM, EV_ALLOC, EV_INPLACE, EV_EVICT, EV_FREE, EV_REMAT, EV_EXEC, EV_REXEC = range(8)
+
+ORC_RESULT = np.dtype([("status", "<i4"), ("fail_op", "<i4"), ("base_us", "<i8"),
+                       ("total_us", "<i8"), ("evictions", "<i8"), ("remat", "<i8"),
+                       ("pressure", "<i8"), ("frag_fail", "<i8"), ("inplace_reuse", "<i8"),
+                       ("heuristic_evals", "<i8"), ("sum_free_bytes_after", "<u8"),
+                       ("sum_free_blocks_after", "<i8"), ("digest", "<u8"),
+                       ("max_depth", "<i4"), ("max_blocks", "<i4"), ("budget", "<u8"),
+                       ("n_events", "<i8")])
+ORC_EVENT = np.dtype([("kind", "<i4"), ("op", "<i4"), ("tensor", "<i4"), ("pad", "<i4"),
+                      ("addr", "<u8")])
+
+
+def _trace_struct(tr):
+    arrs = dict(size=np.ascontiguousarray(tr.size, np.uint64),
+                is_param=np.ascontiguousarray(tr.is_param, np.uint8),
+                producer=np.ascontiguousarray(tr.producer, np.int32),
+                cost_us=np.ascontiguousarray(tr.cost_us, np.int64),
+                out=np.ascontiguousarray(tr.out, np.int32),
+                inplace_src=np.ascontiguousarray(tr.inplace_src, np.int32),
+                phase=np.ascontiguousarray(tr.phase, np.uint8),
+                in_ptr=np.ascontiguousarray(tr.in_ptr, np.int32),
+                in_idx=np.ascontiguousarray(tr.in_idx if len(tr.in_idx) else np.zeros(1, np.int32), np.int32))
+    st = _OrcTrace(len(arrs["size"]), len(arrs["out"]), *[arrs[k].ctypes.data for k in
+                   ("size", "is_param", "producer", "cost_us", "out", "inplace_src", "phase",
+                    "in_ptr", "in_idx")])
+    return st, arrs
+
+
+def _replay_lib():
+    L = lib()
+    if not getattr(L, "_replay_ready", False):
+        L.orc_replay.argtypes = [ctypes.POINTER(_OrcTrace), ctypes.POINTER(_OrcCfg),
+                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+        L.orc_replay.restype = ctypes.c_int
+        L.orc_peak_live.argtypes = [ctypes.POINTER(_OrcTrace), ctypes.c_uint32]
+        L.orc_peak_live.restype = ctypes.c_uint64
+        L._replay_ready = True
+    return L
+
+
+def replay(tr, budget: int, flags: int = F_PARTITION | F_INPLACE, class_threshold: int = 15,
+           max_depth: int = 512, log_cap: int = 0):
+    """O2 -> (result record, event log array or None)"""
+    L = _replay_lib()
+    st, keep = _trace_struct(tr)
+    cfg = _OrcCfg(int(budget), int(flags), int(class_threshold), int(max_depth), 0)
+    res = np.zeros(1, ORC_RESULT)
+    log = np.zeros(max(log_cap, 1), ORC_EVENT) if log_cap else None
+    L.orc_replay(ctypes.byref(st), ctypes.byref(cfg), res.ctypes.data,
+                 log.ctypes.data if log is not None else None, int(log_cap))
+    r = res[0]
+    if log is not None:
+        log = log[:min(int(r["n_events"]), log_cap)]
+    return r, log
+
+
+def peak_live(tr, flags: int = F_PARTITION | F_INPLACE) -> int:
+    L = _replay_lib()
+    st, keep = _trace_struct(tr)
+    return int(L.orc_peak_live(ctypes.byref(st), int(flags)))

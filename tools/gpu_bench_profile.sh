@@ -1,0 +1,9 @@
+set -x
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -3 gpurun_out/bench.err
+cat gpurun_out/bench.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 1 --no-cpu-baseline --e2e-pools 0 > gpurun_out/ncu_list.out 2>&1
+tail -3 gpurun_out/ncu_list.out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:search_kernel -s 1 -c 1 -o gpurun_out/search_full python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-pools 0 > gpurun_out/ncu_full.out 2>&1
+tail -5 gpurun_out/ncu_full.out
+ls -la gpurun_out
