@@ -122,6 +122,89 @@ int coop_window_search_batched_host(const coop_tables_soa *host_tables,
                                     const uint64_t *host_requests, coop_window *host_out,
                                     int64_t chunk_pools);
 
+
+/* ------------------------------------------------------------------ traces & replay
+ * A trace is the execution-ordered op list of one or more training iterations (SoA):
+ * tensors have a size, a parameter flag (parameters / optimizer states are unevictable
+ * and placed before the first op) and a producing op; every op has a cost
+ * (us), ONE output tensor (R30), an optional mutated input (in-place op, Sec. 3.5
+ * PAPER.md:206-222), a phase and an input list (CSR).  Validation (R19, R30):
+ * producer[out[k]] == k; inputs are parameters or outputs of earlier ops; an in-place
+ * op's mutated input is one of its inputs, has the output's size and is never read
+ * again; 1 <= size < 2^48; 0 <= cost < 2^40.
+ */
+#define COOP_PHASE_FWD 0
+#define COOP_PHASE_BWD 1
+#define COOP_PHASE_UPD 2
+
+typedef struct {
+  int32_t n_tensors;          /* T >= 1                                           */
+  int32_t n_ops;              /* M >= 0                                           */
+  const uint64_t *size;       /* [T] bytes                                        */
+  const uint8_t *is_param;    /* [T] 1 = parameter / optimizer state              */
+  const int32_t *producer;    /* [T] producing op, -1 for parameters              */
+  const int64_t *cost_us;     /* [M]                                              */
+  const int32_t *out;         /* [M] output tensor                                */
+  const int32_t *inplace_src; /* [M] mutated input, -1 if none                    */
+  const uint8_t *phase;       /* [M] COOP_PHASE_*                                 */
+  const int32_t *in_ptr;      /* [M+1] input CSR offsets                          */
+  const int32_t *in_idx;      /* [in_ptr[M]] input tensors                        */
+} coop_trace_desc;            /* all HOST pointers; deep-copied by coop_trace_create */
+
+typedef struct coop_trace_s *coop_trace_t;
+
+/* Validate, preprocess (last uses, deaths, consumers, R36 lock lists) and upload a trace
+ * to the current device.  Returns COOP_ERR_INVALID_ARG on a malformed trace. */
+int coop_trace_create(const coop_trace_desc *desc, coop_trace_t *out);
+int coop_trace_destroy(coop_trace_t trace);
+
+/* Peak resident bytes of an unbounded, eviction-free replay (R25), host-side. */
+int coop_trace_peak_live(coop_trace_t trace, uint32_t flags, uint64_t *out);
+
+/* replay flags */
+#define COOP_F_PARTITION 1u            /* cheap tensor partitioning, Sec. 3.4 */
+#define COOP_F_INPLACE 2u              /* recomputable in-place, Sec. 3.5; off = copy-on-write */
+#define COOP_F_PARTITION_ALL_PHASES 4u /* partition backward/update ops too (R13)          */
+
+typedef struct {
+  int32_t status;              /* COOP_OK, COOP_ERR_UNSATISFIABLE, COOP_ERR_THRASHED,
+                                  COOP_ERR_NOMEM (pool exceeded the kernel's block table)  */
+  int32_t fail_op;             /* op index of the failure, -1 = parameter placement / none */
+  int64_t base_us, total_us;   /* compute without / with recomputation (overhead metric)  */
+  int64_t evictions, remat, pressure, frag_fail, inplace_reuse, heuristic_evals;
+  uint64_t sum_free_bytes_after; /* fragmentation samples after pressure events (R27)    */
+  int64_t sum_free_blocks_after;
+  uint64_t digest;             /* eviction sequence digest (R29)                         */
+  int32_t max_depth, max_blocks;
+  uint64_t budget;
+  int64_t n_events;            /* events produced (log entries written = min(cap, this)) */
+  int64_t search_ns_total;     /* %globaltimer ns spent in window searches (R28)         */
+  int64_t search_ns_max;
+} coop_replay_result;          /* 136 bytes */
+
+typedef struct {
+  int32_t kind;   /* 0 param placed, 1 output allocated, 2 in-place reuse, 3 evicted,
+                     4 freed at death, 5 recompute output allocated, 6 op executed,
+                     7 op re-executed for a recompute                                 */
+  int32_t op;     /* op index (trace op for 0..4 and 6; producer op for 5 and 7)     */
+  int32_t tensor;
+  int32_t pad;
+  uint64_t addr;
+} coop_event;     /* 24 bytes */
+
+/*
+ * coop_replay_trace -- replay `trace` once per budget, one CTA per budget (Alg. 1,
+ * PAPER.md:117-138, with Sec. 3.3-3.5), on `stream`.  budgets: HOST array [n_budgets];
+ * out: DEVICE array [n_budgets]; log: DEVICE array [n_budgets * log_cap_per_budget] or
+ * NULL.  class_threshold: us per MiB separating C1/C2 (0 -> 15, R14); max_depth:
+ * rematerialization bound (0 -> 512, R23).  The trace's device workspace grows on demand
+ * (first call with a larger n_budgets allocates).  Asynchronous.
+ */
+int coop_replay_trace(coop_trace_t trace, const uint64_t *budgets, int32_t n_budgets,
+                      uint32_t flags, uint32_t class_threshold, int32_t max_depth,
+                      coop_replay_result *out, coop_event *log, int64_t log_cap_per_budget,
+                      coop_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -338,11 +338,9 @@ static int materialize(R *r, int32_t t, int depth) {
   log_ev(r, ORC_EV_REXEC, op, t, r->addr[t]);
   for (int k = 0; k < ni; ++k) r->last_access[in_at(tr, op, k)] = r->clock;
   r->last_access[t] = r->clock;
-  for (int k = 0; k < ni; ++k) {
-    int32_t u = in_at(tr, op, k);
-    r->pins[u]--;
-    if (r->dead[u] && r->resident[u] && r->pins[u] == 0 && !r->unevict[u]) free_tensor(r, u);
-  }
+  for (int k = 0; k < ni; ++k) r->pins[in_at(tr, op, k)]--;
+  /* a dead input materialized for this recompute stays resident (evictable) until the
+   * end of the current trace op (R22) */
   return 0;
 }
 
@@ -593,14 +591,12 @@ int orc_replay(const orc_trace *tr, const orc_cfg *cfg_in, orc_replay_result *re
     for (int j = 0; j < ni; ++j) r.last_access[in_at(tr, k, j)] = r.clock;
     r.last_access[o] = r.clock;
     for (int j = 0; j < ni; ++j) r.pins[in_at(tr, k, j)]--;
-    /* deaths after op k, ascending tensor id (R20); the mutated input always dies here */
+    /* deaths after op k, ascending tensor id (R20; the mutated input always dies here),
+     * together with dead tensors rematerialized transiently during this op (R22) */
     int32_t src = tr->inplace_src[k];
-    for (int j = 0; j < ni; ++j) (void)j;
     for (int t = 0; t < T; ++t) {
-      if (r.last_use[t] != k) continue;
-      if (r.unevict[t] && t != src) continue; /* parameters / optimizer states live on */
-      r.dead[t] = 1;
-      if (r.resident[t]) free_tensor(&r, t);
+      if (r.last_use[t] == k && (!r.unevict[t] || t == src)) r.dead[t] = 1;
+      if (r.dead[t] && r.resident[t] && (!r.unevict[t] || t == src)) free_tensor(&r, t);
     }
   }
   res->status = r.status;

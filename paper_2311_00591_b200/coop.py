@@ -134,3 +134,106 @@ def _fixed_round_sum_host(h: np.ndarray) -> float:
     """test hook: the CUDA path's 192-bit exact-sum + RN, compiled for the host"""
     h = np.ascontiguousarray(h, dtype=np.float64)
     return float(lib.coop__fixed_round_sum_host(h.ctypes.data, h.size))
+
+
+# ----------------------------------------------------------------------------- replay
+class TraceDesc(ctypes.Structure):
+    _fields_ = [("n_tensors", ctypes.c_int32), ("n_ops", ctypes.c_int32),
+                ("size", ctypes.c_void_p), ("is_param", ctypes.c_void_p),
+                ("producer", ctypes.c_void_p), ("cost_us", ctypes.c_void_p),
+                ("out", ctypes.c_void_p), ("inplace_src", ctypes.c_void_p),
+                ("phase", ctypes.c_void_p), ("in_ptr", ctypes.c_void_p),
+                ("in_idx", ctypes.c_void_p)]
+
+
+F_PARTITION, F_INPLACE, F_PARTITION_ALL_PHASES = 1, 2, 4
+
+REPLAY_RESULT_DTYPE = np.dtype([
+    ("status", "<i4"), ("fail_op", "<i4"), ("base_us", "<i8"), ("total_us", "<i8"),
+    ("evictions", "<i8"), ("remat", "<i8"), ("pressure", "<i8"), ("frag_fail", "<i8"),
+    ("inplace_reuse", "<i8"), ("heuristic_evals", "<i8"), ("sum_free_bytes_after", "<u8"),
+    ("sum_free_blocks_after", "<i8"), ("digest", "<u8"), ("max_depth", "<i4"),
+    ("max_blocks", "<i4"), ("budget", "<u8"), ("n_events", "<i8"),
+    ("search_ns_total", "<i8"), ("search_ns_max", "<i8")])
+assert REPLAY_RESULT_DTYPE.itemsize == 136
+EVENT_DTYPE = np.dtype([("kind", "<i4"), ("op", "<i4"), ("tensor", "<i4"), ("pad", "<i4"),
+                        ("addr", "<u8")])
+
+lib.coop_trace_create.argtypes = [ctypes.POINTER(TraceDesc), ctypes.POINTER(ctypes.c_void_p)]
+lib.coop_trace_create.restype = ctypes.c_int
+lib.coop_trace_destroy.argtypes = [ctypes.c_void_p]
+lib.coop_trace_destroy.restype = ctypes.c_int
+lib.coop_trace_peak_live.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64)]
+lib.coop_trace_peak_live.restype = ctypes.c_int
+lib.coop_replay_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32,
+                                  ctypes.c_uint32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_int64, ctypes.c_void_p]
+lib.coop_replay_trace.restype = ctypes.c_int
+
+
+class Trace:
+    """A trace uploaded to the device (coop_trace_create); `tr` has the SoA fields of
+    gen.traces.Trace."""
+
+    def __init__(self, tr):
+        arrs = dict(size=np.ascontiguousarray(tr.size, np.uint64),
+                    is_param=np.ascontiguousarray(tr.is_param, np.uint8),
+                    producer=np.ascontiguousarray(tr.producer, np.int32),
+                    cost_us=np.ascontiguousarray(tr.cost_us, np.int64),
+                    out=np.ascontiguousarray(tr.out, np.int32),
+                    inplace_src=np.ascontiguousarray(tr.inplace_src, np.int32),
+                    phase=np.ascontiguousarray(tr.phase, np.uint8),
+                    in_ptr=np.ascontiguousarray(tr.in_ptr, np.int32),
+                    in_idx=np.ascontiguousarray(tr.in_idx if len(tr.in_idx) else np.zeros(1, np.int32), np.int32))
+        d = TraceDesc(len(arrs["size"]), len(arrs["out"]), *[arrs[k].ctypes.data for k in
+                      ("size", "is_param", "producer", "cost_us", "out", "inplace_src", "phase",
+                       "in_ptr", "in_idx")])
+        h = ctypes.c_void_p()
+        rc = lib.coop_trace_create(ctypes.byref(d), ctypes.byref(h))
+        if rc != OK:
+            raise CoopError(rc, "coop_trace_create")
+        self.handle = h
+        self.n_tensors = len(arrs["size"])
+        self.n_ops = len(arrs["out"])
+
+    def close(self):
+        if self.handle:
+            lib.coop_trace_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def peak_live(self, flags: int) -> int:
+        v = ctypes.c_uint64()
+        rc = lib.coop_trace_peak_live(self.handle, int(flags), ctypes.byref(v))
+        if rc != OK:
+            raise CoopError(rc, "coop_trace_peak_live")
+        return int(v.value)
+
+    def replay_device(self, budgets, flags, out, log=None, log_cap: int = 0, class_threshold: int = 0,
+                      max_depth: int = 0, stream=None) -> None:
+        """coop_replay_trace into device buffers (torch tensors); asynchronous."""
+        b = np.ascontiguousarray(budgets, np.uint64)
+        rc = lib.coop_replay_trace(self.handle, b.ctypes.data, len(b), int(flags),
+                                   int(class_threshold), int(max_depth), _ptr(out),
+                                   _ptr(log) if log is not None else None, int(log_cap),
+                                   _stream_handle(stream))
+        if rc != OK:
+            raise CoopError(rc, "coop_replay_trace")
+
+    def replay(self, budgets, flags, log_cap: int = 0, class_threshold: int = 0, max_depth: int = 0):
+        """Synchronous convenience wrapper -> (results [n], events [n, log_cap] or None)."""
+        import torch
+        n = len(budgets)
+        out = torch.empty(n * REPLAY_RESULT_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+        log = (torch.empty(max(1, n * log_cap) * EVENT_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+               if log_cap else None)
+        self.replay_device(budgets, flags, out, log, log_cap, class_threshold, max_depth)
+        torch.cuda.synchronize()
+        res = out.cpu().numpy().view(REPLAY_RESULT_DTYPE)
+        ev = log.cpu().numpy().view(EVENT_DTYPE).reshape(n, log_cap) if log is not None else None
+        return res, ev

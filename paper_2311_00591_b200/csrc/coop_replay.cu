@@ -1,0 +1,1165 @@
+// coop_replay.cu -- trace replay under memory budgets: one CTA per (trace, budget) cell.
+//
+// Replays Alg. 1 Allocate(op, size) with the sliding-window eviction of
+// Sec. 3.3, cheap tensor partitioning (Sec. 3.4),
+// recomputable in-place (Sec. 3.5) and on-demand rematerialization
+// (PAPER.md:22, 219-220), with the readings R10-R36 of DESIGN.md.  Bit-exact with the oracle
+// O2 (same events, counters and eviction digest).
+//
+// Layout:
+//   * the pool's address-ordered block table (addr, size, owner) lives in SHARED memory,
+//     double-buffered so an insert / erase is one parallel copy + one barrier;
+//   * per-tensor state (residency flags, pins, last access, address) and the scratch of
+//     the window search live in a per-cell GLOBAL workspace (L2-resident);
+//   * control flow is CTA-uniform: every thread walks the same op loop and the same
+//     explicit rematerialization stack; scalar state changes are made by thread 0 and
+//     published by __syncthreads; the parallel steps are the free-block scans, the shifts,
+//     and on every pressure event the item view with projected costs (one DFS per thread
+//     per candidate), the exact 192-bit span/cost scans, the per-start window ends and
+//     the lexicographic argmin.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <new>
+#include <vector>
+
+#include "coop.h"
+#include "coop_internal.h"
+#include "fixed192.cuh"
+
+namespace coop {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kCap = 2048;       // blocks per pool held by the kernel (COOP_ERR_NOMEM beyond)
+constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
+constexpr int kDfsCap = 512;     // per-thread DFS stack (projected-cost closures)
+constexpr int kFree = -1;
+
+enum : uint8_t { TF_RES = 1, TF_BORN = 2, TF_DEAD = 4, TF_LOCK = 8 };
+
+struct TraceDev {
+  int32_t T, M, n_params;
+  const uint64_t *size;
+  const int32_t *producer;
+  const uint8_t *unevict;
+  const int64_t *cost;
+  const int32_t *out;
+  const int32_t *src;
+  const uint8_t *phase;
+  const int32_t *in_ptr, *in_idx;
+  const int32_t *cons_ptr, *cons_idx;
+  const int32_t *lock_ptr, *lock_idx;
+  const int32_t *die_ptr, *die_idx;
+  const int32_t *params;
+};
+
+struct WsLayout {  // byte offsets inside one cell's workspace
+  size_t tflags, pins, last_access, taddr, epochs, marks, isz, ih, ist, S, H, B, trans, victims;
+  size_t bytes;
+};
+
+struct CellPtrs {
+  uint8_t *tflags;
+  int32_t *pins;
+  int64_t *last_access;
+  uint64_t *taddr;
+  uint32_t *epochs, *marks;
+  uint64_t *isz;
+  double *ih;
+  uint8_t *ist;
+  uint64_t *S;
+  U192 *H;
+  int32_t *B;
+  int32_t *trans, *victims;
+};
+
+struct KArgs {
+  TraceDev tr;
+  const uint64_t *budgets;
+  uint32_t flags, thr;
+  int32_t max_depth;
+  int32_t n_cells;
+  coop_replay_result *out;
+  coop_event *log;
+  int64_t log_cap;
+  unsigned char *ws;
+  WsLayout lay;
+};
+
+struct Shared {
+  uint64_t addr[2][kCap];
+  uint64_t size[2][kCap];
+  int32_t owner[2][kCap];
+  int32_t cur, nb;
+  // CTA-uniform scalars (written by thread 0, published by a barrier)
+  uint64_t bytes_free;
+  int64_t clock;
+  int32_t status, fail_op, cur_op;
+  int32_t sp;
+  int32_t ntrans;
+  int32_t bcast_i;
+  uint64_t bcast_u;
+  // counters (thread 0 only)
+  coop_replay_result res;
+  // rematerialization stack
+  int32_t st_t[kStackCap], st_stage[kStackCap], st_idx[kStackCap], st_depth[kStackCap];
+  // reductions
+  uint64_t red64[2][kWarps];
+  int32_t red32[2][kWarps];
+  U192 red192[kWarps];
+  int32_t redpar;
+};
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ------------------------------------------------------------------ CTA reductions
+// Each returns the reduced value to every thread (two barriers-worth of ordering via a
+// parity-double-buffered scratch: one __syncthreads per call).
+__device__ __forceinline__ int32_t cta_min_i32(Shared &sh, int32_t v) {
+  for (int d = 16; d > 0; d >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, d));
+  const int par = sh.redpar;
+  if ((threadIdx.x & 31) == 0) sh.red32[par][threadIdx.x >> 5] = v;
+  __syncthreads();
+  int32_t r = sh.red32[par][0];
+  for (int w = 1; w < kWarps; ++w) r = min(r, sh.red32[par][w]);
+  if (threadIdx.x == 0) sh.redpar = par ^ 1;  // next call uses the other buffer
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ int32_t cta_max_i32(Shared &sh, int32_t v) { return -cta_min_i32(sh, -v); }
+__device__ __forceinline__ int32_t cta_sum_i32(Shared &sh, int32_t v) {
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  const int par = sh.redpar;
+  if ((threadIdx.x & 31) == 0) sh.red32[par][threadIdx.x >> 5] = v;
+  __syncthreads();
+  int32_t r = 0;
+  for (int w = 0; w < kWarps; ++w) r += sh.red32[par][w];
+  if (threadIdx.x == 0) sh.redpar = par ^ 1;
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ uint64_t cta_min_u64(Shared &sh, uint64_t v) {
+  for (int d = 16; d > 0; d >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, v, d);
+    v = o < v ? o : v;
+  }
+  const int par = sh.redpar;
+  if ((threadIdx.x & 31) == 0) sh.red64[par][threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint64_t r = sh.red64[par][0];
+  for (int w = 1; w < kWarps; ++w) r = sh.red64[par][w] < r ? sh.red64[par][w] : r;
+  if (threadIdx.x == 0) sh.redpar = par ^ 1;
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------ the replay cell
+struct Cell {
+  const KArgs &a;
+  const TraceDev &tr;
+  Shared &sh;
+  CellPtrs w;
+  int cell;
+  uint32_t epoch;  // per-thread DFS epoch
+  coop_event *log;
+
+  __device__ Cell(const KArgs &a_, Shared &sh_, int cell_) : a(a_), tr(a_.tr), sh(sh_), cell(cell_) {
+    unsigned char *base = a.ws + (size_t)blockIdx.x * a.lay.bytes;  // this CTA's slot
+    w.tflags = (uint8_t *)(base + a.lay.tflags);
+    w.pins = (int32_t *)(base + a.lay.pins);
+    w.last_access = (int64_t *)(base + a.lay.last_access);
+    w.taddr = (uint64_t *)(base + a.lay.taddr);
+    w.epochs = (uint32_t *)(base + a.lay.epochs);
+    w.marks = (uint32_t *)(base + a.lay.marks);
+    w.isz = (uint64_t *)(base + a.lay.isz);
+    w.ih = (double *)(base + a.lay.ih);
+    w.ist = (uint8_t *)(base + a.lay.ist);
+    w.S = (uint64_t *)(base + a.lay.S);
+    w.H = (U192 *)(base + a.lay.H);
+    w.B = (int32_t *)(base + a.lay.B);
+    w.trans = (int32_t *)(base + a.lay.trans);
+    w.victims = (int32_t *)(base + a.lay.victims);
+    log = a.log ? a.log + (size_t)cell * a.log_cap : nullptr;
+  }
+
+  __device__ __forceinline__ bool ok() const { return sh.status == COOP_OK; }
+  __device__ __forceinline__ int nin(int op) const { return tr.in_ptr[op + 1] - tr.in_ptr[op]; }
+  __device__ __forceinline__ int in_at(int op, int j) const { return tr.in_idx[tr.in_ptr[op] + j]; }
+  __device__ __forceinline__ uint64_t *A() { return sh.addr[sh.cur]; }
+  __device__ __forceinline__ uint64_t *Z() { return sh.size[sh.cur]; }
+  __device__ __forceinline__ int32_t *O() { return sh.owner[sh.cur]; }
+
+  __device__ void log_ev(int kind, int op, int t, uint64_t addr) {  // thread 0 only
+    const int64_t i = sh.res.n_events++;
+    if (log && i < a.log_cap) {
+      coop_event e;
+      e.kind = kind;
+      e.op = op;
+      e.tensor = t;
+      e.pad = 0;
+      e.addr = addr;
+      log[i] = e;
+    }
+  }
+
+  // ---------------------------------------------------------------- block table ops
+  // lowest (right = false) / highest (right = true) free block with size >= need, or -1
+  __device__ int find_fit(uint64_t need, bool right) {
+    const int nb = sh.nb;
+    int best = right ? -1 : 0x7fffffff;
+    for (int b = threadIdx.x; b < nb; b += kThreads)
+      if (O()[b] == kFree && Z()[b] >= need) best = right ? max(best, b) : min(best, b);
+    if (right) return cta_max_i32(sh, best);
+    const int r = cta_min_i32(sh, best);
+    return r == 0x7fffffff ? -1 : r;
+  }
+
+  // replace blocks [lo, hi] (hi >= lo - 1; hi = lo - 1 means pure insertion at lo) by the
+  // m new blocks nb_[0..m) -- one parallel copy into the other buffer
+  __device__ void splice(int lo, int hi, int m, const uint64_t *na, const uint64_t *nz, const int32_t *no) {
+    const int nb = sh.nb, cur = sh.cur, nxt = cur ^ 1;
+    const int removed = hi - lo + 1;
+    const int nnb = nb - removed + m;
+    for (int j = threadIdx.x; j < nnb; j += kThreads) {
+      uint64_t ad, sz;
+      int32_t ow;
+      if (j < lo) {
+        ad = sh.addr[cur][j]; sz = sh.size[cur][j]; ow = sh.owner[cur][j];
+      } else if (j < lo + m) {
+        ad = na[j - lo]; sz = nz[j - lo]; ow = no[j - lo];
+      } else {
+        const int s = j - m + removed;
+        ad = sh.addr[cur][s]; sz = sh.size[cur][s]; ow = sh.owner[cur][s];
+      }
+      sh.addr[nxt][j] = ad;
+      sh.size[nxt][j] = sz;
+      sh.owner[nxt][j] = ow;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sh.cur = nxt;
+      sh.nb = nnb;
+      if (nnb > sh.res.max_blocks) sh.res.max_blocks = nnb;
+    }
+    __syncthreads();
+  }
+
+  // place `need` bytes of tensor t into free block i (left end, or right end - need)
+  __device__ uint64_t place(int i, uint64_t need, bool right, int t) {
+    const uint64_t fa = A()[i], fz = Z()[i];
+    uint64_t at;
+    if (fz == need) {
+      __syncthreads();
+      if (threadIdx.x == 0) O()[i] = t;
+      at = fa;
+      __syncthreads();
+    } else if (sh.nb + 1 > kCap) {
+      if (threadIdx.x == 0) sh.status = COOP_ERR_NOMEM;
+      __syncthreads();
+      return 0;
+    } else if (!right) {
+      const uint64_t na[2] = {fa, fa + need}, nz[2] = {need, fz - need};
+      const int32_t no[2] = {t, kFree};
+      splice(i, i, 2, na, nz, no);
+      at = fa;
+    } else {
+      const uint64_t na[2] = {fa, fa + fz - need}, nz[2] = {fz - need, need};
+      const int32_t no[2] = {kFree, t};
+      splice(i, i, 2, na, nz, no);
+      at = fa + fz - need;
+    }
+    if (threadIdx.x == 0) sh.bytes_free -= need;
+    return at;
+  }
+
+  __device__ int block_of_addr(uint64_t ad) {  // binary search (uniform)
+    int lo = 0, hi = sh.nb - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (A()[mid] <= ad) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  }
+
+  // free block i and merge with free neighbours
+  __device__ void release(int i) {
+    const int nb = sh.nb;
+    int lo = i, hi = i;
+    if (i > 0 && O()[i - 1] == kFree) lo = i - 1;
+    if (i + 1 < nb && O()[i + 1] == kFree) hi = i + 1;
+    const uint64_t na = A()[lo], nz = A()[hi] + Z()[hi] - A()[lo];
+    const int32_t no = kFree;
+    if (threadIdx.x == 0) sh.bytes_free += Z()[i];
+    splice(lo, hi, 1, &na, &nz, &no);
+  }
+
+  __device__ void free_tensor(int t) {  // resident tensor -> freed (R20, R22)
+    const uint64_t ad = w.taddr[t];
+    const int b = block_of_addr(ad);
+    release(b);
+    if (threadIdx.x == 0) {
+      w.tflags[t] &= (uint8_t)~TF_RES;
+      log_ev(4, sh.cur_op, t, ad);
+    }
+    __syncthreads();
+  }
+
+  // ---------------------------------------------------------------- heuristics
+  __device__ bool is_c1(int op) const {  // R14: C1 iff cost * 2^20 >= thr * out bytes
+    return (uint64_t)tr.cost[op] * 1048576ull >= (uint64_t)a.thr * tr.size[tr.out[op]];
+  }
+  __device__ bool goes_right(int op) const {  // PAPER.md:173; R12-R13
+    if (!(a.flags & COOP_F_PARTITION)) return false;
+    if (tr.phase[op] != COOP_PHASE_FWD && !(a.flags & COOP_F_PARTITION_ALL_PHASES)) return false;
+    return !is_c1(op);
+  }
+
+  // c(t) = producer cost + the SET of non-resident ancestors reachable through
+  // non-resident tensors + the SET of evicted descendants reachable through evicted
+  // tensors (R18).  One thread; visited marks = per-thread epochs.
+  __device__ int64_t projected_cost(int t, bool &overflow) {
+    uint32_t *mk = w.marks + (size_t)threadIdx.x * tr.T;
+    const uint32_t ep = ++epoch;
+    int stk[kDfsCap];
+    int sp = 0;
+    const int op = tr.producer[t];
+    int64_t c = tr.cost[op];
+    mk[t] = ep;
+    for (int j = tr.in_ptr[op]; j < tr.in_ptr[op + 1]; ++j) {
+      if (sp == kDfsCap) { overflow = true; return c; }
+      stk[sp++] = tr.in_idx[j];
+    }
+    while (sp > 0) {
+      const int u = stk[--sp];
+      if (mk[u] == ep) continue;
+      mk[u] = ep;
+      if ((w.tflags[u] & TF_RES) || tr.producer[u] < 0) continue;
+      const int pu = tr.producer[u];
+      c += tr.cost[pu];
+      for (int j = tr.in_ptr[pu]; j < tr.in_ptr[pu + 1]; ++j) {
+        if (sp == kDfsCap) { overflow = true; return c; }
+        stk[sp++] = tr.in_idx[j];
+      }
+    }
+    for (int j = tr.cons_ptr[t]; j < tr.cons_ptr[t + 1]; ++j) {
+      if (sp == kDfsCap) { overflow = true; return c; }
+      stk[sp++] = tr.out[tr.cons_idx[j]];
+    }
+    while (sp > 0) {
+      const int d = stk[--sp];
+      if (mk[d] == ep) continue;
+      mk[d] = ep;
+      const uint8_t f = w.tflags[d];
+      if (!(f & TF_BORN) || (f & TF_RES) || (f & TF_DEAD)) continue;
+      c += tr.cost[tr.producer[d]];
+      for (int j = tr.cons_ptr[d]; j < tr.cons_ptr[d + 1]; ++j) {
+        if (sp == kDfsCap) { overflow = true; return c; }
+        stk[sp++] = tr.out[tr.cons_idx[j]];
+      }
+    }
+    return c;
+  }
+
+  // ---------------------------------------------------------------- Sec. 3.3 search
+  // Sliding-window search over the address-ordered item view and eviction of the window;
+  // returns false when no window exists (R24).
+  __device__ bool evict_window(uint64_t need) {
+    const uint64_t t0 = gtimer();
+    const int nb = sh.nb;
+    // item view: FREE -> h = 0; unevictable / pinned / locked -> barrier; else h = c/s
+    int nev = 0;
+    bool overflow = false;
+    for (int b = threadIdx.x; b < nb; b += kThreads) {
+      const int o = O()[b];
+      uint8_t st;
+      double h = 0.0;
+      if (o == kFree) {
+        st = COOP_FREE;
+      } else if (tr.unevict[o] || w.pins[o] > 0 || (w.tflags[o] & TF_LOCK)) {
+        st = COOP_PINNED;
+      } else {
+        st = COOP_EVICTABLE;
+        int64_t s = sh.clock - w.last_access[o];  // staleness (R17)
+        if (s < 1) s = 1;
+        h = __ddiv_rn((double)projected_cost(o, overflow), (double)s);
+        ++nev;
+      }
+      w.isz[b] = Z()[b];
+      w.ih[b] = h;
+      w.ist[b] = st;
+    }
+    nev = cta_sum_i32(sh, nev);
+    if (cta_max_i32(sh, overflow ? 1 : 0)) {
+      if (threadIdx.x == 0) sh.status = COOP_ERR_NOMEM;
+      __syncthreads();
+      return false;
+    }
+    // exclusive prefixes over items: span S (u64), exact heuristic H (192-bit fixed
+    // point, LSB 2^-116), barrier count B -- chunked per thread + serial carry by thread 0
+    const int chunk = (nb + kThreads - 1) / kThreads;
+    const int b0 = min(nb, (int)threadIdx.x * chunk), b1 = min(nb, b0 + chunk);
+    uint64_t ls = 0;
+    U192 lh = u192_zero();
+    int lb = 0;
+    for (int b = b0; b < b1; ++b) {
+      ls += w.isz[b];
+      lh = u192_add(lh, u192_from_double(w.ih[b]));
+      lb += (w.ist[b] == COOP_PINNED);
+    }
+    // thread totals -> exclusive carries (serial over kThreads in thread 0; small)
+    U192 *totH = w.H + (kCap + 1);  // workspace has room for kThreads extra entries
+    uint64_t *totS = w.S + (kCap + 1);
+    int32_t *totB = w.B + (kCap + 1);
+    totS[threadIdx.x] = ls;
+    totH[threadIdx.x] = lh;
+    totB[threadIdx.x] = lb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t cs = 0;
+      U192 ch = u192_zero();
+      int cb = 0;
+      for (int t = 0; t < kThreads; ++t) {
+        const uint64_t s2 = totS[t];
+        const U192 h2 = totH[t];
+        const int b2 = totB[t];
+        totS[t] = cs;
+        totH[t] = ch;
+        totB[t] = cb;
+        cs += s2;
+        ch = u192_add(ch, h2);
+        cb += b2;
+      }
+      w.S[nb] = cs;
+      w.H[nb] = ch;
+      w.B[nb] = cb;
+    }
+    __syncthreads();
+    {
+      uint64_t cs = totS[threadIdx.x];
+      U192 ch = totH[threadIdx.x];
+      int cb = totB[threadIdx.x];
+      for (int b = b0; b < b1; ++b) {
+        w.S[b] = cs;
+        w.H[b] = ch;
+        w.B[b] = cb;
+        cs += w.isz[b];
+        ch = u192_add(ch, u192_from_double(w.ih[b]));
+        cb += (w.ist[b] == COOP_PINNED);
+      }
+    }
+    __syncthreads();
+    // per start: minimal end by bisection, barrier check, exact cost RN(H[e] - H[i]);
+    // argmin over (cost bits, start) (R3, R4)
+    const uint64_t Stot = w.S[nb];
+    uint64_t bestc = ~0ull;
+    int besti = 0x7fffffff;
+    for (int i = threadIdx.x; i < nb; i += kThreads) {
+      if (w.ist[i] == COOP_PINNED) continue;
+      const uint64_t target = w.S[i] + need;
+      if (target > Stot) continue;
+      int lo = i + 1, hi = nb;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (w.S[mid] >= target) hi = mid;
+        else lo = mid + 1;
+      }
+      const int e = lo;
+      if (w.B[e] != w.B[i]) continue;
+      const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(u192_sub(w.H[e], w.H[i])));
+      if (cb < bestc || (cb == bestc && i < besti)) {
+        bestc = cb;
+        besti = i;
+      }
+    }
+    const uint64_t cmin = cta_min_u64(sh, bestc);
+    const int first = cta_min_i32(sh, bestc == cmin ? besti : 0x7fffffff);
+    if (threadIdx.x == 0) {
+      sh.res.heuristic_evals += nev;
+      const int64_t dt = (int64_t)(gtimer() - t0);
+      sh.res.search_ns_total += dt;
+      if (dt > sh.res.search_ns_max) sh.res.search_ns_max = dt;
+    }
+    if (cmin == ~0ull) {
+      __syncthreads();
+      return false;
+    }
+    // window end of the winner; evict its tensors in ascending address order (R10)
+    int last;
+    {
+      const uint64_t target = w.S[first] + need;
+      int lo = first + 1, hi = nb;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (w.S[mid] >= target) hi = mid;
+        else lo = mid + 1;
+      }
+      last = lo - 1;
+    }
+    if (threadIdx.x == 0) {
+      uint64_t d = sh.res.digest;
+      for (int b = first; b <= last; ++b) {
+        const int o = O()[b];
+        if (o == kFree) continue;
+        const uint64_t ad = A()[b];
+        w.tflags[o] &= (uint8_t)~TF_RES;
+        sh.res.evictions++;
+        log_ev(3, sh.cur_op, o, ad);
+        d = splitmix64(d ^ (((uint64_t)(uint32_t)sh.cur_op << 32) | (uint32_t)o));  // R29
+        d = splitmix64(d ^ ad);
+        sh.bytes_free += Z()[b];
+      }
+      sh.res.digest = d;
+    }
+    __syncthreads();
+    // the window and its free neighbours coalesce into one free block
+    int lo = first, hi = last;
+    if (lo > 0 && O()[lo - 1] == kFree) --lo;
+    if (hi + 1 < nb && O()[hi + 1] == kFree) ++hi;
+    // (window FREE items were already counted in bytes_free; only tensors were added)
+    const uint64_t na = A()[lo], nz = A()[hi] + Z()[hi] - A()[lo];
+    const int32_t no = kFree;
+    splice(lo, hi, 1, &na, &nz, &no);
+    return true;
+  }
+
+  // ---------------------------------------------------------------- Alg. 1
+  __device__ void allocate(int op, int t, bool allow_inplace, int kind) {
+    const uint64_t need = tr.size[t];
+    const int src = tr.src[op];
+    if (allow_inplace && src >= 0 && (a.flags & COOP_F_INPLACE)) {  // addr <- input.addr
+      const uint64_t ad = w.taddr[src];
+      const int b = block_of_addr(ad);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        O()[b] = t;
+        w.taddr[t] = ad;
+        w.tflags[src] &= (uint8_t)~TF_RES;
+        w.tflags[t] |= TF_RES;
+        sh.res.inplace_reuse++;
+        log_ev(2, op, t, ad);
+      }
+      __syncthreads();
+      return;
+    }
+    const bool right = goes_right(op);
+    int i = find_fit(need, right);
+    uint64_t at;
+    if (i < 0) {
+      if (threadIdx.x == 0) {
+        sh.res.pressure++;
+        if (sh.bytes_free >= need) sh.res.frag_fail++;
+      }
+      if (!evict_window(need)) {
+        if (threadIdx.x == 0) {
+          if (sh.status == COOP_OK) sh.status = COOP_ERR_UNSATISFIABLE;
+          sh.res.fail_op = sh.cur_op;
+        }
+        __syncthreads();
+        return;
+      }
+      i = find_fit(need, right);  // the unique coalesced block >= need
+      at = place(i, need, right, t);
+      if (!ok()) return;
+      int nfree = 0;
+      for (int b = threadIdx.x; b < sh.nb; b += kThreads) nfree += (O()[b] == kFree);
+      nfree = cta_sum_i32(sh, nfree);
+      if (threadIdx.x == 0) {
+        sh.res.sum_free_bytes_after += sh.bytes_free;  // R27
+        sh.res.sum_free_blocks_after += nfree;
+      }
+    } else {
+      at = place(i, need, right, t);
+      if (!ok()) return;
+    }
+    if (threadIdx.x == 0) {
+      w.taddr[t] = at;
+      w.tflags[t] |= TF_RES;
+      log_ev(kind, op, t, at);
+    }
+    __syncthreads();
+  }
+
+  // ---------------------------------------------------------------- rematerialization
+  // M(t): explicit stack (R21-R23); a dead tensor recomputed here stays resident until
+  // the end of the current trace op (R22).
+  __device__ void materialize(int t0) {
+    if (threadIdx.x == 0) {
+      sh.sp = 1;
+      sh.st_t[0] = t0;
+      sh.st_stage[0] = 0;
+      sh.st_idx[0] = 0;
+      sh.st_depth[0] = 0;
+    }
+    __syncthreads();
+    while (sh.sp > 0 && ok()) {
+      const int f = sh.sp - 1;
+      const int t = sh.st_t[f], depth = sh.st_depth[f];
+      const int op = tr.producer[t];
+      if (sh.st_stage[f] == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          if (depth > a.max_depth) {
+            sh.status = COOP_ERR_THRASHED;  // R23
+            sh.res.fail_op = sh.cur_op;
+          } else if (op < 0) {
+            sh.status = COOP_ERR_UNSATISFIABLE;
+            sh.res.fail_op = sh.cur_op;
+          } else {
+            if (depth > sh.res.max_depth) sh.res.max_depth = depth;
+            sh.st_stage[f] = 1;
+          }
+        }
+        __syncthreads();
+        if (!ok()) return;
+        for (int j = threadIdx.x; j < nin(op); j += kThreads) atomicAdd(&w.pins[in_at(op, j)], 1);
+        __syncthreads();
+        continue;
+      }
+      if (sh.st_stage[f] == 1) {
+        int j = sh.st_idx[f];
+        const int n = nin(op);
+        while (j < n && (w.tflags[in_at(op, j)] & TF_RES)) ++j;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          if (j < n) {
+            sh.st_idx[f] = j + 1;
+            if (sh.sp >= kStackCap) {
+              sh.status = COOP_ERR_THRASHED;
+              sh.res.fail_op = sh.cur_op;
+            } else {
+              const int g = sh.sp++;
+              sh.st_t[g] = in_at(op, j);
+              sh.st_stage[g] = 0;
+              sh.st_idx[g] = 0;
+              sh.st_depth[g] = depth + 1;
+            }
+          } else {
+            sh.st_stage[f] = 2;
+          }
+        }
+        __syncthreads();
+        continue;
+      }
+      // stage 2: recompute t out-of-place (R21)
+      allocate(op, t, false, 5);
+      if (!ok()) return;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        sh.clock += tr.cost[op];
+        sh.res.total_us += tr.cost[op];
+        sh.res.remat++;
+        log_ev(7, op, t, w.taddr[t]);
+        if (w.tflags[t] & TF_DEAD) {
+          if (sh.ntrans < 4 * tr.T) w.trans[sh.ntrans++] = t;
+          else sh.status = COOP_ERR_NOMEM;
+        }
+        sh.sp--;
+      }
+      __syncthreads();
+      const int64_t clk = sh.clock;
+      for (int j = threadIdx.x; j < nin(op); j += kThreads) {
+        const int u = in_at(op, j);
+        w.last_access[u] = clk;
+        atomicSub(&w.pins[u], 1);
+      }
+      if (threadIdx.x == 0) w.last_access[t] = clk;
+      __syncthreads();
+    }
+  }
+
+  // ---------------------------------------------------------------- the op loop
+  __device__ void run(uint64_t budget) {
+    const int T = tr.T, M = tr.M;
+    for (int t = threadIdx.x; t < T; t += kThreads) {
+      w.tflags[t] = 0;
+      w.pins[t] = 0;
+      w.last_access[t] = 0;
+      w.taddr[t] = 0;
+    }
+    if (threadIdx.x == 0) {
+      sh.cur = 0;
+      sh.nb = 1;
+      sh.addr[0][0] = 0;
+      sh.size[0][0] = budget;
+      sh.owner[0][0] = kFree;
+      sh.bytes_free = budget;
+      sh.clock = 0;
+      sh.status = COOP_OK;
+      sh.cur_op = -1;
+      sh.redpar = 0;
+      memset(&sh.res, 0, sizeof(sh.res));
+      sh.res.fail_op = -1;
+      sh.res.digest = 0x9E3779B97F4A7C15ull;
+      sh.res.budget = budget;
+      sh.res.max_blocks = 1;
+    }
+    epoch = w.epochs[threadIdx.x];
+    __syncthreads();
+    // parameters to the two ends (R15)
+    {
+      uint64_t lb = 0, rb = 0;
+      for (int j = 0; j < tr.n_params && ok(); ++j) {
+        const int t = tr.params[j];
+        const bool right = (a.flags & COOP_F_INPLACE) ? (rb < lb) : false;
+        const int i = find_fit(tr.size[t], right);
+        if (i < 0) {
+          if (threadIdx.x == 0) sh.status = COOP_ERR_UNSATISFIABLE;
+          __syncthreads();
+          break;
+        }
+        const uint64_t at = place(i, tr.size[t], right, t);
+        if (!ok()) break;
+        if (right) rb += tr.size[t];
+        else lb += tr.size[t];
+        if (threadIdx.x == 0) {
+          w.taddr[t] = at;
+          w.tflags[t] = TF_RES | TF_BORN;
+          log_ev(0, -1, t, at);
+        }
+        __syncthreads();
+      }
+    }
+    for (int k = 0; k < M && ok(); ++k) {
+      const int n = nin(k), o = tr.out[k], src = tr.src[k];
+      if (threadIdx.x == 0) {
+        sh.cur_op = k;
+        sh.ntrans = 0;
+      }
+      for (int j = threadIdx.x; j < n; j += kThreads) atomicAdd(&w.pins[in_at(k, j)], 1);
+      for (int j = tr.lock_ptr[k] + threadIdx.x; j < tr.lock_ptr[k + 1]; j += kThreads)
+        w.tflags[tr.lock_idx[j]] |= TF_LOCK;  // R36
+      __syncthreads();
+      for (int j = 0; j < n && ok(); ++j) {
+        const int u = in_at(k, j);
+        const bool res = w.tflags[u] & TF_RES;
+        __syncthreads();
+        if (!res) materialize(u);
+      }
+      for (int j = tr.lock_ptr[k]; j < tr.lock_ptr[k + 1] && ok(); ++j) {
+        const int u = tr.lock_idx[j];
+        const bool res = w.tflags[u] & TF_RES;
+        __syncthreads();
+        if (!res) materialize(u);
+      }
+      if (!ok()) break;
+      allocate(k, o, true, 1);
+      if (!ok()) break;
+      if (threadIdx.x == 0) {
+        w.tflags[o] |= TF_BORN;
+        sh.clock += tr.cost[k];
+        sh.res.base_us += tr.cost[k];
+        sh.res.total_us += tr.cost[k];
+        log_ev(6, k, o, w.taddr[o]);
+      }
+      __syncthreads();
+      const int64_t clk = sh.clock;
+      for (int j = threadIdx.x; j < n; j += kThreads) {
+        const int u = in_at(k, j);
+        w.last_access[u] = clk;
+        atomicSub(&w.pins[u], 1);
+      }
+      if (threadIdx.x == 0) w.last_access[o] = clk;
+      __syncthreads();
+      // deaths after op k (R20) merged with transient dead recomputes (R22), ascending id
+      if (threadIdx.x == 0) {
+        for (int j = tr.die_ptr[k]; j < tr.die_ptr[k + 1]; ++j) w.tflags[tr.die_idx[j]] |= TF_DEAD;
+        // insertion-sort the transient list (small) and merge with the (sorted) die list
+        int *tl = w.trans;
+        const int nt = sh.ntrans;
+        for (int x = 1; x < nt; ++x) {
+          const int v = tl[x];
+          int y = x - 1;
+          while (y >= 0 && tl[y] > v) { tl[y + 1] = tl[y]; --y; }
+          tl[y + 1] = v;
+        }
+      }
+      __syncthreads();
+      {
+        int pd = tr.die_ptr[k];
+        const int pe = tr.die_ptr[k + 1];
+        int pt = 0;
+        const int nt = sh.ntrans;
+        int last = -1;
+        while (pd < pe || pt < nt) {
+          int t;
+          if (pt >= nt || (pd < pe && tr.die_idx[pd] <= w.trans[pt])) t = tr.die_idx[pd++];
+          else t = w.trans[pt++];
+          if (t == last) continue;
+          last = t;
+          const uint8_t f = w.tflags[t];
+          const bool keep = tr.unevict[t] && t != src;
+          __syncthreads();
+          if ((f & TF_DEAD) && (f & TF_RES) && !keep) free_tensor(t);
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      sh.res.status = sh.status;
+      if (sh.status != COOP_OK && sh.res.fail_op < 0 && sh.cur_op >= 0) sh.res.fail_op = sh.cur_op;
+    }
+    w.epochs[threadIdx.x] = epoch;
+    __syncthreads();
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) replay_kernel(const KArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Shared &sh = *reinterpret_cast<Shared *>(smem);
+  for (int cell = blockIdx.x; cell < a.n_cells; cell += gridDim.x) {
+    Cell c(a, sh, cell);
+    c.run(a.budgets[cell]);
+    if (threadIdx.x == 0) a.out[cell] = sh.res;
+    __syncthreads();
+  }
+}
+
+}  // namespace
+}  // namespace coop
+
+// =============================================================================== host
+using namespace coop;
+
+struct coop_trace_s {
+  int32_t T = 0, M = 0, n_params = 0;
+  std::vector<uint64_t> size;
+  std::vector<uint8_t> is_param, unevict;
+  std::vector<int32_t> producer, out, src, in_ptr, in_idx, last_use, params;
+  std::vector<int64_t> cost;
+  std::vector<uint8_t> phase;
+  std::vector<int32_t> cons_ptr, cons_idx, lock_ptr, lock_idx, die_ptr, die_idx;
+  void *dev = nullptr;
+  TraceDev td{};
+  unsigned char *ws = nullptr;
+  size_t ws_cells = 0;
+  WsLayout lay{};
+  uint64_t *d_budgets = nullptr;
+  size_t budgets_cap = 0;
+  int device = 0;
+};
+
+namespace {
+
+// independent validation (R19, R30) -- not shared with the oracle
+int validate_and_prepare(coop_trace_s &t) {
+  const int T = t.T, M = t.M;
+  if (T < 1 || M < 0 || t.in_ptr[0] != 0) return COOP_ERR_INVALID_ARG;
+  t.last_use.assign(T, -1);
+  for (int i = 0; i < T; ++i) {
+    if (t.size[i] < 1 || t.size[i] >= (1ull << 48)) return COOP_ERR_INVALID_ARG;
+    if (t.is_param[i]) {
+      if (t.producer[i] != -1) return COOP_ERR_INVALID_ARG;
+    } else if (t.producer[i] < 0 || t.producer[i] >= M || t.out[t.producer[i]] != i) {
+      return COOP_ERR_INVALID_ARG;
+    }
+  }
+  for (int k = 0; k < M; ++k) {
+    if (t.cost[k] < 0 || t.cost[k] >= (1ll << 40) || t.phase[k] > COOP_PHASE_UPD) return COOP_ERR_INVALID_ARG;
+    const int o = t.out[k];
+    if (o < 0 || o >= T || t.producer[o] != k || t.in_ptr[k + 1] < t.in_ptr[k]) return COOP_ERR_INVALID_ARG;
+    bool seen = false;
+    for (int j = t.in_ptr[k]; j < t.in_ptr[k + 1]; ++j) {
+      const int u = t.in_idx[j];
+      if (u < 0 || u >= T) return COOP_ERR_INVALID_ARG;
+      if (!t.is_param[u] && t.producer[u] >= k) return COOP_ERR_INVALID_ARG;
+      if (u == t.src[k]) seen = true;
+      t.last_use[u] = k;
+    }
+    if (t.src[k] >= 0 && (t.src[k] >= T || !seen || t.size[t.src[k]] != t.size[o])) return COOP_ERR_INVALID_ARG;
+  }
+  for (int k = 0; k < M; ++k)
+    if (t.src[k] >= 0 && t.last_use[t.src[k]] != k) return COOP_ERR_INVALID_ARG;
+  for (int i = 0; i < T; ++i)
+    if (t.last_use[i] < 0 && !t.is_param[i]) t.last_use[i] = t.producer[i];
+  // unevictable: parameters and in-place results of unevictable inputs (R19)
+  t.unevict.assign(T, 0);
+  for (int i = 0; i < T; ++i) t.unevict[i] = t.is_param[i] ? 1 : 0;
+  for (int k = 0; k < M; ++k)
+    if (t.src[k] >= 0 && t.unevict[t.src[k]]) t.unevict[t.out[k]] = 1;
+  t.params.clear();
+  for (int i = 0; i < T; ++i)
+    if (t.is_param[i]) t.params.push_back(i);
+  t.n_params = (int32_t)t.params.size();
+  // consumers (ops reading each tensor, in op order)
+  t.cons_ptr.assign(T + 1, 0);
+  for (int32_t u : t.in_idx) t.cons_ptr[u + 1]++;
+  for (int i = 0; i < T; ++i) t.cons_ptr[i + 1] += t.cons_ptr[i];
+  t.cons_idx.assign(t.in_idx.size(), 0);
+  {
+    std::vector<int32_t> fill(T, 0);
+    for (int k = 0; k < M; ++k)
+      for (int j = t.in_ptr[k]; j < t.in_ptr[k + 1]; ++j) {
+        const int u = t.in_idx[j];
+        t.cons_idx[t.cons_ptr[u] + fill[u]++] = k;
+      }
+  }
+  // deaths per op, ascending tensor id (R20): last use here, unless unevictable (except
+  // the op's mutated input)
+  t.die_ptr.assign(M + 1, 0);
+  {
+    std::vector<std::vector<int32_t>> d(M);
+    for (int i = 0; i < T; ++i) {
+      const int k = t.last_use[i];
+      if (k < 0) continue;
+      if (t.unevict[i] && t.src[k] != i) continue;
+      d[k].push_back(i);
+    }
+    t.die_idx.clear();
+    for (int k = 0; k < M; ++k) {
+      t.die_idx.insert(t.die_idx.end(), d[k].begin(), d[k].end());
+      t.die_ptr[k + 1] = (int32_t)t.die_idx.size();
+    }
+  }
+  // R36 lock lists: need(t) = unevictable tensors read by t's recompute closure
+  {
+    std::vector<int32_t> uid(T, -1);
+    int nu = 0;
+    for (int i = 0; i < T; ++i)
+      if (t.unevict[i]) uid[i] = nu++;
+    const int words = std::max(1, (nu + 63) / 64);
+    std::vector<uint64_t> need((size_t)T * words, 0);
+    for (int k = 0; k < M; ++k) {
+      uint64_t *no = &need[(size_t)t.out[k] * words];
+      for (int j = t.in_ptr[k]; j < t.in_ptr[k + 1]; ++j) {
+        const int u = t.in_idx[j];
+        if (t.unevict[u]) no[uid[u] >> 6] |= 1ull << (uid[u] & 63);
+        else {
+          const uint64_t *nu_ = &need[(size_t)u * words];
+          for (int x = 0; x < words; ++x) no[x] |= nu_[x];
+        }
+      }
+    }
+    t.lock_ptr.assign(M + 1, 0);
+    t.lock_idx.clear();
+    for (int k = 0; k < M; ++k) {
+      const int s = t.src[k];
+      if (s >= 0 && t.unevict[s]) {
+        for (int i = 0; i < T; ++i) {
+          if (t.unevict[i] || t.is_param[i] || t.producer[i] >= k || t.last_use[i] <= k) continue;
+          if ((need[(size_t)i * words + (uid[s] >> 6)] >> (uid[s] & 63)) & 1ull) t.lock_idx.push_back(i);
+        }
+      }
+      t.lock_ptr[k + 1] = (int32_t)t.lock_idx.size();
+    }
+  }
+  return COOP_OK;
+}
+
+template <class V>
+size_t put(std::vector<unsigned char> &blob, const V &v) {
+  size_t off = (blob.size() + 15) / 16 * 16;
+  const size_t bytes = v.size() * sizeof(typename V::value_type);
+  blob.resize(off + bytes + 16);
+  if (bytes) memcpy(blob.data() + off, v.data(), bytes);
+  return off;
+}
+
+WsLayout make_layout(int T) {
+  WsLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = (o + bytes + 255) / 256 * 256;
+    return r;
+  };
+  L.tflags = take((size_t)T);
+  L.pins = take((size_t)T * 4);
+  L.last_access = take((size_t)T * 8);
+  L.taddr = take((size_t)T * 8);
+  L.epochs = take((size_t)kThreads * 4);
+  L.marks = take((size_t)kThreads * T * 4);
+  L.isz = take((size_t)(kCap + 1) * 8);
+  L.ih = take((size_t)(kCap + 1) * 8);
+  L.ist = take((size_t)(kCap + 1));
+  L.S = take((size_t)(kCap + 1 + kThreads) * 8);
+  L.H = take((size_t)(kCap + 1 + kThreads) * sizeof(U192));
+  L.B = take((size_t)(kCap + 1 + kThreads) * 4);
+  L.trans = take((size_t)T * 4 * 4);
+  L.victims = take((size_t)kCap * 4);
+  L.bytes = o;
+  return L;
+}
+
+}  // namespace
+
+
+// Device mirror of the preprocessed trace, uploaded on first use (so creation, validation
+// and peak computation work without a GPU).
+static int upload_trace(coop_trace_s *t) {
+  if (t->dev) return COOP_OK;
+  const int T = t->T, M = t->M;
+  std::vector<unsigned char> blob;
+  const size_t o_size = put(blob, t->size), o_prod = put(blob, t->producer), o_unev = put(blob, t->unevict),
+               o_cost = put(blob, t->cost), o_out = put(blob, t->out), o_src = put(blob, t->src),
+               o_phase = put(blob, t->phase), o_inp = put(blob, t->in_ptr), o_ini = put(blob, t->in_idx),
+               o_cp = put(blob, t->cons_ptr), o_ci = put(blob, t->cons_idx), o_lp = put(blob, t->lock_ptr),
+               o_li = put(blob, t->lock_idx), o_dp = put(blob, t->die_ptr), o_di = put(blob, t->die_idx),
+               o_par = put(blob, t->params);
+  cudaGetDevice(&t->device);
+  if (cudaMalloc(&t->dev, blob.size()) != cudaSuccess) {
+    t->dev = nullptr;
+    return COOP_ERR_NOMEM;
+  }
+  if (cudaMemcpy(t->dev, blob.data(), blob.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(t->dev);
+    t->dev = nullptr;
+    return COOP_ERR_CUDA;
+  }
+  unsigned char *b = (unsigned char *)t->dev;
+  TraceDev &td = t->td;
+  td.T = T;
+  td.M = M;
+  td.n_params = t->n_params;
+  td.size = (const uint64_t *)(b + o_size);
+  td.producer = (const int32_t *)(b + o_prod);
+  td.unevict = (const uint8_t *)(b + o_unev);
+  td.cost = (const int64_t *)(b + o_cost);
+  td.out = (const int32_t *)(b + o_out);
+  td.src = (const int32_t *)(b + o_src);
+  td.phase = (const uint8_t *)(b + o_phase);
+  td.in_ptr = (const int32_t *)(b + o_inp);
+  td.in_idx = (const int32_t *)(b + o_ini);
+  td.cons_ptr = (const int32_t *)(b + o_cp);
+  td.cons_idx = (const int32_t *)(b + o_ci);
+  td.lock_ptr = (const int32_t *)(b + o_lp);
+  td.lock_idx = (const int32_t *)(b + o_li);
+  td.die_ptr = (const int32_t *)(b + o_dp);
+  td.die_idx = (const int32_t *)(b + o_di);
+  td.params = (const int32_t *)(b + o_par);
+  return COOP_OK;
+}
+
+extern "C" int coop_trace_create(const coop_trace_desc *d, coop_trace_t *out) {
+  if (!d || !out || d->n_tensors < 1 || d->n_ops < 0 || !d->size || !d->is_param || !d->producer ||
+      (d->n_ops > 0 && (!d->cost_us || !d->out || !d->inplace_src || !d->phase || !d->in_ptr)))
+    return COOP_ERR_INVALID_ARG;
+  coop_trace_s *t = new (std::nothrow) coop_trace_s();
+  if (!t) return COOP_ERR_NOMEM;
+  const int T = d->n_tensors, M = d->n_ops;
+  t->T = T;
+  t->M = M;
+  t->size.assign(d->size, d->size + T);
+  t->is_param.assign(d->is_param, d->is_param + T);
+  t->producer.assign(d->producer, d->producer + T);
+  t->cost.assign(d->cost_us, d->cost_us + M);
+  t->out.assign(d->out, d->out + M);
+  t->src.assign(d->inplace_src, d->inplace_src + M);
+  t->phase.assign(d->phase, d->phase + M);
+  t->in_ptr.assign(d->in_ptr, d->in_ptr + M + 1);
+  if (M == 0) t->in_ptr.assign(1, 0);
+  const int nnz = t->in_ptr[M];
+  if (nnz < 0 || (nnz > 0 && !d->in_idx)) {
+    delete t;
+    return COOP_ERR_INVALID_ARG;
+  }
+  t->in_idx.assign(d->in_idx, d->in_idx + nnz);
+  int rc = validate_and_prepare(*t);
+  if (rc != COOP_OK) {
+    delete t;
+    return rc;
+  }
+  t->lay = make_layout(T);
+  *out = t;
+  return COOP_OK;
+}
+
+extern "C" int coop_trace_destroy(coop_trace_t t) {
+  if (!t) return COOP_ERR_INVALID_ARG;
+  if (t->dev) cudaFree(t->dev);
+  if (t->ws) cudaFree(t->ws);
+  if (t->d_budgets) cudaFree(t->d_budgets);
+  delete t;
+  return COOP_OK;
+}
+
+// Peak resident bytes without eviction (R25): host-side sweep of the liveness intervals.
+extern "C" int coop_trace_peak_live(coop_trace_t t, uint32_t flags, uint64_t *out) {
+  if (!t || !out) return COOP_ERR_INVALID_ARG;
+  uint64_t live = 0, peak = 0;
+  for (int i = 0; i < t->T; ++i)
+    if (t->is_param[i]) live += t->size[i];
+  peak = live;
+  for (int k = 0; k < t->M; ++k) {
+    const int s = t->src[k];
+    const bool inplace = s >= 0 && (flags & COOP_F_INPLACE);
+    if (!inplace) live += t->size[t->out[k]];
+    peak = std::max(peak, live);
+    for (int j = t->die_ptr[k]; j < t->die_ptr[k + 1]; ++j) {
+      const int i = t->die_idx[j];
+      if (inplace && i == s) continue;  // its bytes now belong to the output
+      live -= t->size[i];
+    }
+  }
+  *out = peak;
+  return COOP_OK;
+}
+
+extern "C" int coop_replay_trace(coop_trace_t t, const uint64_t *budgets, int32_t n_budgets,
+                                 uint32_t flags, uint32_t class_threshold, int32_t max_depth,
+                                 coop_replay_result *out, coop_event *log, int64_t log_cap,
+                                 coop_stream_t stream) {
+  if (!t || n_budgets < 0 || (n_budgets > 0 && (!budgets || !out)) || log_cap < 0 ||
+      (flags & ~7u) || max_depth > 1024)
+    return COOP_ERR_INVALID_ARG;
+  if (n_budgets == 0) return COOP_OK;
+  for (int i = 0; i < n_budgets; ++i)
+    if (budgets[i] < 1) return COOP_ERR_INVALID_ARG;
+  if (!is_device_ptr(out) || (log && !is_device_ptr(log))) return COOP_ERR_INVALID_ARG;
+  const int up = upload_trace(t);
+  if (up != COOP_OK) return up;
+  cudaStream_t st = (cudaStream_t)stream;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
+  const size_t smem = sizeof(Shared);
+  if (cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return COOP_ERR_CUDA;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, replay_kernel, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  // concurrent cells = min(n_budgets, resident CTAs); the workspace holds that many
+  const size_t cells = (size_t)std::min<int64_t>(n_budgets, (int64_t)sms * per_sm);
+  if (cells > t->ws_cells) {
+    if (t->ws) cudaFree(t->ws);
+    t->ws = nullptr;
+    t->ws_cells = 0;
+    if (cudaMalloc(&t->ws, cells * t->lay.bytes) != cudaSuccess) return COOP_ERR_NOMEM;
+    cudaMemset(t->ws, 0, cells * t->lay.bytes);  // DFS epochs start at 0
+    t->ws_cells = cells;
+  }
+  if ((size_t)n_budgets > t->budgets_cap) {
+    if (t->d_budgets) cudaFree(t->d_budgets);
+    if (cudaMalloc(&t->d_budgets, (size_t)n_budgets * 8) != cudaSuccess) return COOP_ERR_NOMEM;
+    t->budgets_cap = (size_t)n_budgets;
+  }
+  cudaMemcpyAsync(t->d_budgets, budgets, (size_t)n_budgets * 8, cudaMemcpyHostToDevice, st);
+  KArgs a{};
+  a.tr = t->td;
+  a.budgets = t->d_budgets;
+  a.flags = flags;
+  a.thr = class_threshold ? class_threshold : 15;
+  a.max_depth = max_depth > 0 ? max_depth : 512;
+  a.n_cells = n_budgets;
+  a.out = out;
+  a.log = log;
+  a.log_cap = log ? log_cap : 0;
+  a.ws = t->ws;
+  a.lay = t->lay;
+  // each CTA owns a workspace slot: cells are assigned cyclically, CTA b takes cells
+  // b, b + grid, ... and always uses slot b
+  replay_kernel<<<(unsigned)cells, kThreads, smem, st>>>(a);
+  return cudaGetLastError() == cudaSuccess ? COOP_OK : COOP_ERR_CUDA;
+}

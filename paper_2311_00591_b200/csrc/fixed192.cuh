@@ -43,6 +43,28 @@ COOP_HD U192 u192_add(U192 a, U192 b) {
 #endif
 }
 
+COOP_HD U192 u192_sub(U192 a, U192 b) {  // a - b, requires a >= b
+#ifdef __CUDA_ARCH__
+  U192 r;
+  asm("sub.cc.u64 %0, %3, %6;\n\t"
+      "subc.cc.u64 %1, %4, %7;\n\t"
+      "subc.u64 %2, %5, %8;"
+      : "=l"(r.w0), "=l"(r.w1), "=l"(r.w2)
+      : "l"(a.w0), "l"(a.w1), "l"(a.w2), "l"(b.w0), "l"(b.w1), "l"(b.w2));
+  return r;
+#else
+  U192 r;
+  r.w0 = a.w0 - b.w0;
+  uint64_t br0 = a.w0 < b.w0;
+  uint64_t t1 = a.w1 - b.w1;
+  uint64_t br1 = a.w1 < b.w1;
+  r.w1 = t1 - br0;
+  br1 |= (t1 < br0);
+  r.w2 = a.w2 - b.w2 - br1;
+  return r;
+#endif
+}
+
 // h (an admissible binary64: +-0 or in [2^-64, 2^60)) -> exact fixed point.
 // The sign bit is ignored (the search encodes FREE items as -0.0).
 COOP_HD U192 u192_from_double(double h) {

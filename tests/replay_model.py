@@ -244,9 +244,6 @@ class Model:
         self.last_access[t] = self.clock
         for u in self.ins[op]:
             self.pins[u] -= 1
-            if self.dead[u] and self.resident[u] and self.pins[u] == 0 and not self.unev[u]:
-                a = self.clear(u)
-                self.events.append((4, self.cur_op, u, a))
 
     def run(self):
         tr = self.tr
@@ -293,10 +290,10 @@ class Model:
                     self.pins[u] -= 1
                 src = int(tr.inplace_src[k])
                 for t in range(tr.n_tensors):
-                    if self.last_use[t] != k or (self.unev[t] and t != src):
-                        continue
-                    self.dead[t] = True
-                    if self.resident[t]:
+                    keep = self.unev[t] and t != src
+                    if self.last_use[t] == k and not keep:
+                        self.dead[t] = True
+                    if self.dead[t] and self.resident[t] and not keep:
                         a = self.clear(t)
                         self.events.append((4, k, t, a))
         except Unsat:

@@ -1,0 +1,91 @@
+"""GPU parity: coop_replay_trace (one CTA per budget, through the C ABI) vs the O2 oracle.
+Bit-exact on every integer counter, the eviction digest, and the full event log."""
+import numpy as np
+import pytest
+
+from gen import dnn
+from gen import traces as TR
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+from paper_2311_00591_b200 import coop  # noqa: E402
+
+FIELDS = ["status", "fail_op", "base_us", "total_us", "evictions", "remat", "pressure",
+          "frag_fail", "inplace_reuse", "heuristic_evals", "sum_free_bytes_after",
+          "sum_free_blocks_after", "digest", "max_depth", "max_blocks", "budget", "n_events"]
+ALL_FLAGS = [0, 1, 2, 3, 7]
+
+
+def check(tr, budgets, flags, log_cap=0, ctx=""):
+    t = coop.Trace(tr)
+    res, ev = t.replay(budgets, flags, log_cap=log_cap)
+    for j, b in enumerate(budgets):
+        r, log = O.replay(tr, int(b), flags, log_cap=log_cap)
+        got = {f: int(res[j][f]) for f in FIELDS}
+        want = {f: int(r[f]) for f in FIELDS}
+        assert got == want, f"{ctx} budget {b} flags {flags}: gpu {got} oracle {want}"
+        if log_cap:
+            m = min(int(r["n_events"]), log_cap)
+            g = ev[j][:m]
+            for k in ("kind", "op", "tensor", "addr"):
+                assert np.array_equal(g[k], log[:m][k]), f"{ctx} budget {b}: event field {k}"
+    return res
+
+
+def test_fig2_gpu():
+    tr = TR.fig2_trace()
+    for flags in ALL_FLAGS:
+        check(tr, [250 << 20, 200 << 20, 300 << 20], flags, log_cap=200, ctx="fig2")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_traces_gpu(seed):
+    rng = np.random.default_rng(500 + seed)
+    for _ in range(15):
+        tr = TR.random_trace(rng, n_params=int(rng.integers(0, 4)), n_fwd=int(rng.integers(2, 12)),
+                             iters=int(rng.integers(1, 3)), inplace_p=0.25)
+        flags = int(rng.choice(ALL_FLAGS))
+        peak = O.peak_live(tr, flags)
+        budgets = [max(1, int(peak * f)) for f in (0.35, 0.5, 0.65, 0.8, 1.0, 1.4)]
+        check(tr, budgets, flags, log_cap=4000, ctx=f"seed {seed}")
+
+
+@pytest.mark.parametrize("name", list(dnn.DNNS))
+def test_dnn_traces_gpu(name):
+    tr = dnn.dnn(name)
+    flags = coop.F_PARTITION | coop.F_INPLACE
+    peak = O.peak_live(tr, flags)
+    budgets = [int(peak * f) for f in (0.3, 0.45, 0.6, 0.75, 0.9, 1.0)]
+    check(tr, budgets, flags, log_cap=20000, ctx=name)
+
+
+def test_config2_resnet50_half_budget():
+    """BASELINE config 2: ResNet-50 replay at 50 % of peak, partitioning + in-place."""
+    tr = dnn.resnet50()
+    flags = coop.F_PARTITION | coop.F_INPLACE
+    res = check(tr, [O.peak_live(tr, flags) // 2], flags, log_cap=50000, ctx="config2")
+    assert int(res[0]["status"]) == 0 and int(res[0]["evictions"]) > 0
+
+
+def test_config3_gpt3_64_budgets():
+    """BASELINE config 3: GPT-3-style 2.7B, 64 budgets from 25 % to 100 % of peak."""
+    tr = dnn.gpt3_2p7b()
+    flags = coop.F_PARTITION | coop.F_INPLACE
+    peak = O.peak_live(tr, flags)
+    budgets = [peak * (1575 + 75 * k) // 6300 for k in range(64)]
+    res = check(tr, budgets, flags, ctx="config3")
+    st = res["status"]
+    assert (st == 0).sum() > 10 and (st == coop.ERR_UNSATISFIABLE).sum() > 0
+
+
+def test_ablation_flags_dnn():
+    """The same traces without partitioning / with copy-on-write (App. B ablations)."""
+    for name in ("unet", "bert_large"):
+        tr = dnn.dnn(name)
+        for flags in (0, coop.F_INPLACE, coop.F_PARTITION, 7):
+            peak = O.peak_live(tr, flags)
+            check(tr, [int(peak * 0.6), int(peak * 0.85)], flags, ctx=f"{name} flags {flags}")
