@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--pools", type=int, default=POOLS_PER_GPU, help="pools per GPU")
     ap.add_argument("--e2e-pools", type=int, default=65536)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-replay", action="store_true", help="skip the replay sweeps")
+    ap.add_argument("--replay-steps", type=int, default=2)
+    ap.add_argument("--replay-config5", action="store_true",
+                    help="also run config 5 (8 DNN shapes x 256 budgets; slow)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="CPU work budget of the oracle baseline sample")
     return ap.parse_args()
@@ -188,6 +192,108 @@ def run_reference(args):
     return 0
 
 
+# ----------------------------------------------------------------------- replay sweeps
+def replay_bench(world: int, rank: int, steps: int, with_config5: bool):
+    """BASELINE configs 3 and 5 on this rank's cells (config 5 cells cyclic over ranks):
+    trace ops/s = trace ops (not counting recomputes) replayed per second, summed over
+    cells; device time per sweep with CUDA events; one stream per trace."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from gen import dnn
+    from paper_2311_00591_b200 import coop
+    from paper_2311_00591_b200 import dist as D
+
+    flags = coop.F_PARTITION | coop.F_INPLACE
+    out = {}
+    traces = {name: dnn.dnn(name) for name in dnn.DNNS}
+    handles = {name: coop.Trace(tr) for name, tr in traces.items()}
+    peaks = {name: handles[name].peak_live(flags) for name in traces}
+    sweeps = {
+        # config 2: ResNet-50 at 50 % of peak, one cell
+        "config2": [("resnet50", [peaks["resnet50"] // 2])],
+        # config 3: GPT-3-style 2.7B, 64 budgets 25 %..100 % of peak, one CTA per budget
+        "config3": [("gpt3_2.7b", [peaks["gpt3_2.7b"] * (1575 + 75 * k) // 6300 for k in range(64)])],
+        # config 5: eight DNN shapes x 256 budgets 20 %..100 % of peak
+        "config5": [(name, [peaks[name] * (20 * 255 + 80 * k) // (100 * 255) for k in range(256)])
+                    for name in dnn.DNNS],
+    }
+    if not with_config5:
+        del sweeps["config5"]
+    streams = {name: torch.cuda.Stream() for name in traces}
+    main_s = torch.cuda.current_stream()
+    for key, sweep in sweeps.items():
+        # shard: global cell index over the sweep, cyclic over ranks (config 3 too)
+        cells = [(name, j, b) for name, bs in sweep for j, b in enumerate(bs)]
+        mine = [cells[c] for c in D.cyclic_cells(len(cells), rank, world)]
+        per = {}
+        for name, j, b in mine:
+            per.setdefault(name, []).append(b)
+        bufs = {name: torch.empty(len(bs) * coop.REPLAY_RESULT_DTYPE.itemsize, dtype=torch.uint8,
+                                  device="cuda") for name, bs in per.items()}
+        ops = sum(traces[name].n_ops * len(bs) for name, bs in per.items())
+
+        def sweep_once():
+            ev0 = torch.cuda.Event()
+            ev0.record(main_s)
+            for name, bs in per.items():
+                st = streams[name]
+                st.wait_event(ev0)
+                handles[name].replay_device(bs, flags, bufs[name], stream=st)
+            for name in per:
+                e = torch.cuda.Event()
+                e.record(streams[name])
+                main_s.wait_event(e)
+
+        sweep_once()  # warm-up (allocates the per-trace workspaces)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(main_s)
+        for _ in range(steps):
+            sweep_once()
+        t1.record(main_s)
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / steps
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t[0])
+            tops = torch.tensor([ops], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tops)
+            ops_all = float(tops[0])
+        else:
+            ops_all = float(ops)
+        res = np.concatenate([bufs[n].cpu().numpy().view(coop.REPLAY_RESULT_DTYPE) for n in per]) \
+            if per else np.zeros(0, coop.REPLAY_RESULT_DTYPE)
+        ok = res["status"] == 0
+        frag = (res["sum_free_bytes_after"][ok] / np.maximum(1, res["pressure"][ok]) /
+                res["budget"][ok].astype(np.float64))
+        ovh = (res["total_us"][ok] - res["base_us"][ok]) / np.maximum(1, res["base_us"][ok])
+        lat = res["search_ns_total"][ok] / np.maximum(1, res["pressure"][ok])
+        out[key] = {
+            "workload": {"config2": "ResNet-50 at 50 % of peak, 1 budget",
+                         "config3": "GPT-3-style 2.7B x 64 budgets (25-100 % of peak)",
+                         "config5": "8 DNN shapes x 256 budgets (20-100 % of peak)"}[key],
+            "flags": "partition+recomputable-inplace", "cells": len(cells),
+            "cells_this_rank": len(mine), "ms_per_sweep": ms,
+            "trace_ops_per_s": ops_all / (ms / 1e3),
+            "events_per_s_incl_recompute": (ops_all + float(res["remat"].sum()) * world) / (ms / 1e3),
+            "completed_cells_rank0": int(ok.sum()),
+            "mean_frag_rate_rank0": float(frag.mean()) if ok.any() else None,
+            "mean_overhead_rank0": float(ovh.mean()) if ok.any() else None,
+            "search_latency_us_mean_rank0": float(lat.mean() / 1e3) if ok.any() else None,
+            "search_latency_us_max_rank0": float(res["search_ns_max"][ok].max() / 1e3) if ok.any() else None,
+            "gpu_launches_per_sweep": len(per),
+        }
+    for h in handles.values():
+        h.close()
+    return out
+
+
 # ---------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -309,6 +415,9 @@ def main():
             "algorithmic_bytes_per_launch": P * ALGO_BYTES_PER_POOL,
             "kernel": "coop::search_kernel<8>", "kernel_ms_mean": kmean,
             "frac_of_8TBps": achieved / 8000.0}
+    replay = None
+    if not args.no_replay:
+        replay = replay_bench(world, rank, args.replay_steps, args.replay_config5)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_seconds)
@@ -325,7 +434,7 @@ def main():
                            "l2": "no flush: 96 GiB of inputs per step per GPU >> 126 MB L2",
                            "generator": "gen/coop_gen.cu MODE_BENCH (counter-based, on device)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": args.steps, "clocks": clk,
+                "gpu_launches": args.steps, "clocks": clk, "replay": replay,
                 "results": {"status_counts": stat, "xor_digest": f"{digest:016x}"}}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "coop.h"
 #include "coop_internal.h"
@@ -52,6 +53,7 @@ struct Scratch {
   int32_t bend[kMaxWarps];
   int32_t bnev[kMaxWarps];
   int32_t ncand;
+  int32_t xend, xnev;  // end / evictions of the best exactly-costed window
   uint32_t cand[kCandCap];
   unsigned long long mbar[2];
 };
@@ -71,6 +73,7 @@ struct Args {
   uint32_t stage_bytes;
   int32_t stages;
   int32_t use_tma;
+  int32_t dbg;  // profiling hook (COOP_SEARCH_DBG): 1 = load only, 2 = + phase A/scan, 3 = + zero pass
   double gerr;  // filter error coefficient: |C^ - C| <= gerr * (H^[e] + H^[i])
 };
 
@@ -179,136 +182,140 @@ __device__ __forceinline__ bool better(uint64_t cb, int i, uint64_t bb, int bi) 
   return cb < bb || (cb == bb && i < bi);
 }
 
-// Per-pool context.  Thread t owns items [k0, k0 + K).  After phase A the stage holds
-//   region 0: S[k]  (exclusive span prefix, k in [0, n]; S[n] = total span)
-//   region 1: H^[k] (fp64 prefix of h, k in [0, n])
-//   region 2: h[k]  (binary64; FREE items stored as -0.0)
-template <int K>
-struct PoolCtx {
+// Per-pool view after phase A (all in shared memory):
+//   region 0: S[k]   exclusive span prefix, k in [0, n]; S[n] = total span, S[n+1] = ~0
+//   region 1: H^[k]  fp64 prefix of h, k in [0, n]
+//   region 2: v[k]   h as binary64; FREE items stored as -0.0, PINNED items as NaN
+//   E[a]             (u16, scratch) window end of start a from the merge path
+struct PoolView {
   smem_t *sr, *hr, *vr;
-  int32_t n, k0;
-  uint64_t R, S_car, S_total;
-  double H_car, gerr;
-  uint32_t barmask, nzmask;
-  int32_t nb_right, nz_right;
-  uint64_t spre[K];
-  double hpre[K];
+  uint16_t *E;
+  int32_t n;
+  uint64_t R, S_total;
+  double gerr;
 
   __device__ __forceinline__ uint64_t S_at(int x) const { return sm<uint64_t>(sr, swz((uint32_t)x)); }
   __device__ __forceinline__ double H_at(int x) const { return sm<double>(hr, swz((uint32_t)x)); }
-  __device__ __forceinline__ double h_at(int x) const { return sm<double>(vr, swz((uint32_t)x)); }
-  __device__ __forceinline__ int32_t next_barrier(int q) const {  // first PINNED index >= k0+q
-    const uint32_t m = barmask >> q;
-    return m ? k0 + q + __ffs(m) - 1 : nb_right;
-  }
-  __device__ __forceinline__ int32_t next_nonzero(int q) const {  // first h != 0 index >= k0+q
-    const uint32_t m = nzmask >> q;
-    return m ? k0 + q + __ffs(m) - 1 : nz_right;
-  }
+  __device__ __forceinline__ double v_at(int x) const { return sm<double>(vr, swz((uint32_t)x)); }
 
-  // Walk this thread's starts from q_from: binary search for the first start's window end,
-  // then a galloping two-pointer (cost ~2 log2 of each advance).  Called only when no
-  // zero-cost window exists, so every feasible window holds a nonzero h.
-  // MODE 0: fp64 filter bounds (U_t, L_t).
-  // MODE 1: append starts whose lower bound <= thresh to the candidate list; returns
-  //         the q at which the list overflowed (resume point) or K when done.
-  template <int MODE>
-  __device__ __forceinline__ int walk(int q_from, double thresh, Scratch &sc, double &U_t,
-                                      double &L_t, uint64_t &xb, int &xi, int &xe) const {
-    int e = 0;
-#pragma unroll
-    for (int q = 0; q < K; ++q) {
-      if (q < q_from) continue;
-      const int i = k0 + q;
-      if (i >= n) break;
-      if ((barmask >> q) & 1u) continue;
-      const uint64_t target = S_car + spre[q] + R;  // R clamped: no overflow
-      if (target > S_total) break;                  // this and every later start: infeasible
-      if (e <= i) {  // first start: bisect (i, n]; S[n] >= target
-        int lo = i + 1, hi = n;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (S_at(mid) >= target) hi = mid;
-          else lo = mid + 1;
-        }
-        e = lo;
-      } else if (S_at(e) < target) {  // gallop to a bracket, then bisect
-        int lo = e + 1, step = 1, hi = e + 1;
-        while (hi < n && S_at(hi) < target) {
-          lo = hi + 1;
-          step <<= 1;
-          hi = e + step;
-        }
-        if (hi > n) hi = n;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (S_at(mid) >= target) hi = mid;
-          else lo = mid + 1;
-        }
-        e = lo;
-      }
-      if (next_barrier(q) < e) continue;  // a PINNED item inside [i, e-1]
-      const int len = e - i;
-      double C, err;
-      bool exact = false;
-      if (len <= 2) {  // one IEEE add is correctly rounded: the exact window cost
-        const double h0 = fabs(h_at(i));
-        C = (len == 1) ? h0 : __dadd_rn(h0, fabs(h_at(i + 1)));
-        err = 0.0;
-        exact = true;
-      } else if (len <= 8) {  // direct sum of nonnegative terms: relative error < 7u
-        double acc = 0.0;
-        for (int k = i; k < e; ++k) acc = __dadd_rn(acc, fabs(h_at(k)));
-        C = acc;
-        err = 0x1p-50 * acc;
-      } else {  // prefix difference: error bounded by the prefix magnitudes
-        const double He = H_at(e);
-        const double Hi = __dadd_rn(H_car, hpre[q]);
-        C = He - Hi;
-        err = gerr * (He + Hi);
-      }
-      const double Lb = C - err;
-      if (MODE == 0) {
-        if (exact) {
-          const uint64_t cb = (uint64_t)__double_as_longlong(C);
-          if (cb < xb) {  // starts ascend within a thread: ties keep the lower start
-            xb = cb;
-            xi = i;
-            xe = e;
-          }
-        } else {
-          U_t = fmin(U_t, C + err);
-          L_t = fmin(L_t, Lb);
-        }
-      } else if (!exact && Lb <= thresh) {
-        const int slot = atomicAdd(&sc.ncand, 1);
-        if (slot >= kCandCap) return q;
-        sc.cand[slot] = ((uint32_t)i << 16) | (uint32_t)(e - i);  // n <= 8192
-      }
+  // Window ends of all starts by a merge path of A[a] = S[a] + R (a < n) with B[b] = S[b]
+  // (b <= n): e(a) = #{b : S[b] < A[a]} = min{e : S[e] - S[a] >= R}, or n + 1 when no end
+  // exists.  The 2n + 1 steps are split evenly over the T threads (balanced whatever the
+  // item-size distribution); the sentinels S[n + 1] = ~0 and A[n] = S[n] + R > S[n] make
+  // every step branch-free.
+  __device__ __forceinline__ void merge_path(int t, int T) const {
+    const int L = 2 * n + 1;
+    const int D = (L + T - 1) / T;
+    const int d0 = min(t * D, L), d1 = min(d0 + D, L);
+    if (d0 >= d1) return;
+    int lo = max(0, d0 - (n + 1)), hi = min(d0, n);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (S_at(mid) + R <= S_at(d0 - mid - 1)) lo = mid + 1;
+      else hi = mid;
     }
-    return K;
-  }
-
-  // Lowest start of a zero-cost window in this thread's chunk (kInfIdx if none): a run of
-  // consecutive h = 0 items (FREE, or EVICTABLE with c = 0) is a zero-cost window iff its
-  // span covers R; the run's first item is then the lowest such start.
-  __device__ __forceinline__ int zero_start() const {
-    const int cnt = n - k0;
-    const uint32_t valid = cnt >= K ? (K == 32 ? ~0u : ((1u << K) - 1u)) : (cnt > 0 ? (1u << cnt) - 1u : 0u);
-    const uint32_t zm = valid & ~barmask & ~nzmask;
-    const uint32_t heads = zm & ~(zm << 1);  // first item of each zero run inside the chunk
-#pragma unroll
-    for (int q = 0; q < K; ++q) {  // static indices: spre stays in registers
-      if (!((heads >> q) & 1u)) continue;
-      const int stop = min(min(next_nonzero(q), next_barrier(q)), n);
-      if (S_at(stop) - (S_car + spre[q]) >= R) return k0 + q;
+    int ai = lo, bi = d0 - lo;
+    uint64_t Av = S_at(ai) + R, Bv = S_at(bi);
+    for (int d = d0; d < d1; ++d) {
+      const bool takeA = Av <= Bv;  // start ai is complete: its window is [ai, bi - 1]
+      if (takeA) E[ai] = (uint16_t)bi;
+      const int x = takeA ? ++ai : ++bi;
+      const uint64_t sx = S_at(x);
+      Av = takeA ? sx + R : Av;
+      Bv = takeA ? Bv : sx;
     }
-    return kInfIdx;
   }
 };
 
-template <int K>
-__global__ void __launch_bounds__(512, 1)
+// Per-thread running state of the filter.
+struct LaneBest {
+  double U, L, L2;   // inexact windows: min upper bound, min / second-min lower bound
+  int li, le;        // the inexact start with the minimal lower bound and its end
+  uint64_t xb;       // exactly known windows (zero-cost, or <= 2 items): min cost bits
+  int xi, xe;        //   ... its start (lowest among equal cost) and end
+};
+
+// The owner thread's filter over its K starts, ends from E[].  MODE 0 fills LaneBest;
+// MODE 1 appends the inexact starts in [w_lo, w_hi) whose lower bound is <= thresh.
+template <int K, int MODE>
+__device__ __forceinline__ void filter_starts(const PoolView &v, int k0, uint32_t barmask,
+                                              uint32_t nzmask, int nb_right, int nz_right,
+                                              const double (&hpre)[K], double H_car, double thresh,
+                                              int w_lo, int w_hi, Scratch &sc, LaneBest &b) {
+  const int n = v.n;
+  uint16_t E[K];
+#pragma unroll
+  for (int q = 0; q < K; q += 8) {
+    const uint4 w = *reinterpret_cast<const uint4 *>(v.E + k0 + q);
+    E[q + 0] = (uint16_t)(w.x & 0xffffu); E[q + 1] = (uint16_t)(w.x >> 16);
+    E[q + 2] = (uint16_t)(w.y & 0xffffu); E[q + 3] = (uint16_t)(w.y >> 16);
+    E[q + 4] = (uint16_t)(w.z & 0xffffu); E[q + 5] = (uint16_t)(w.z >> 16);
+    E[q + 6] = (uint16_t)(w.w & 0xffffu); E[q + 7] = (uint16_t)(w.w >> 16);
+  }
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const int i = k0 + q;
+    if (i >= n) break;
+    if ((barmask >> q) & 1u) continue;
+    const int e = E[q];
+    if (e > n) break;  // this and every later start: no window covers R
+    const uint32_t mb = barmask >> q, mz = nzmask >> q;
+    const int nb = mb ? i + __ffs(mb) - 1 : nb_right;
+    if (nb < e) continue;  // a PINNED item inside [i, e-1]
+    const int nz = mz ? i + __ffs(mz) - 1 : nz_right;
+    const int len = e - i;
+    double C, err;
+    bool exact;
+    if (nz >= e) {  // only h = 0 items: exact cost 0
+      C = 0.0;
+      err = 0.0;
+      exact = true;
+    } else if (len <= 2) {  // one IEEE add is correctly rounded
+      const double h0 = fabs(v.v_at(i));
+      C = (len == 1) ? h0 : __dadd_rn(h0, fabs(v.v_at(i + 1)));
+      err = 0.0;
+      exact = true;
+    } else if (len <= 8) {  // direct sum of nonnegative terms: relative error < 7u
+      double acc = 0.0;
+      for (int k = i; k < e; ++k) acc = __dadd_rn(acc, fabs(v.v_at(k)));
+      C = acc;
+      err = 0x1p-50 * acc;
+      exact = false;
+    } else {  // prefix difference: error bounded by the prefix magnitudes
+      const double He = v.H_at(e), Hi = __dadd_rn(H_car, hpre[q]);
+      C = He - Hi;
+      err = v.gerr * (He + Hi);
+      exact = false;
+    }
+    const double Lb = C - err;
+    if (MODE == 0) {
+      if (exact) {
+        const uint64_t cb = (uint64_t)__double_as_longlong(C);
+        if (cb < b.xb) {  // starts ascend: ties keep the lower start
+          b.xb = cb;
+          b.xi = i;
+          b.xe = e;
+        }
+      } else {
+        b.U = fmin(b.U, C + err);
+        if (Lb < b.L) {
+          b.L2 = b.L;
+          b.L = Lb;
+          b.li = i;
+          b.le = e;
+        } else {
+          b.L2 = fmin(b.L2, Lb);
+        }
+      }
+    } else if (!exact && Lb <= thresh && i >= w_lo && i < w_hi) {
+      const int slot = atomicAdd(&sc.ncand, 1);
+      if (slot < kCandCap) sc.cand[slot] = ((uint32_t)i << 16) | (uint32_t)(e - i);  // n <= 8192
+    }
+  }
+}
+
+template <int K, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
     search_kernel(const __grid_constant__ CUtensorMap m_ss, const __grid_constant__ CUtensorMap m_c,
                   const __grid_constant__ CUtensorMap m_s, const Args a) {
   extern __shared__ unsigned char smem_raw[];
@@ -316,6 +323,8 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t base = (raw + 1023u) & ~1023u;
   smem_t *base_ptr = smem_raw + (base - raw);
   Scratch &sc = *reinterpret_cast<Scratch *>(base_ptr + (size_t)a.stages * a.stage_bytes);
+  uint16_t *Ebuf = reinterpret_cast<uint16_t *>(base_ptr + (size_t)a.stages * a.stage_bytes +
+                                                 (sizeof(Scratch) + 15) / 16 * 16);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = blockDim.x, W = T >> 5;
@@ -347,323 +356,331 @@ __global__ void __launch_bounds__(512, 1)
       stage_plain(a, stage, p);
       __syncthreads();
     }
+    PoolView v;
+    v.sr = stage;
+    v.hr = stage + a.region_bytes;
+    v.vr = stage + 2u * a.region_bytes;
+    v.E = Ebuf;
+    v.n = n;
+    v.R = Rraw < kRClamp ? Rraw : kRClamp;
+    v.gerr = a.gerr;
+    const int k0 = tid * K;
 
-    PoolCtx<K> cx;
-    cx.sr = stage;
-    cx.hr = stage + a.region_bytes;
-    cx.vr = stage + 2u * a.region_bytes;
-    cx.n = n;
-    cx.k0 = tid * K;
-    cx.gerr = a.gerr;
-    cx.R = Rraw < kRClamp ? Rraw : kRClamp;
-
-    // ---------------- phase A: decode, validate, h = c/s, local prefixes -------------
-    bool bad = (Rraw == 0);
-    uint32_t barmask = 0, nzmask = 0;
-    uint64_t sacc = 0;
-    double hacc = 0.0;
-#pragma unroll
-    for (int q = 0; q < K; q += 2) {
-      const int k = cx.k0 + q;
-      uint64_t sv[2] = {0, 0};
-      double cv[2] = {0.0, 0.0}, tv[2] = {1.0, 1.0};
-      const uint32_t o = swz((uint32_t)k);
-      if (k < n) {
-        const ulonglong2 vs = sm<ulonglong2>(cx.sr, o);
-        const double2 vc = sm<double2>(cx.hr, o);
-        const double2 vt = sm<double2>(cx.vr, o);
-        sv[0] = vs.x; sv[1] = vs.y; cv[0] = vc.x; cv[1] = vc.y; tv[0] = vt.x; tv[1] = vt.y;
-      }
-      double hs[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int kk = k + r;
-        uint64_t size = 0;
-        double h = 0.0, hslot = 0.0;
-        if (kk < n) {
-          const uint32_t state = (uint32_t)(sv[r] >> 62);
-          const bool ev = (state == COOP_EVICTABLE);
-          size = sv[r] & kSizeMask;
-          const double c = ev ? cv[r] : 0.0, st = ev ? tv[r] : 1.0;
-          h = __ddiv_rn(c, st);  // h(t) = c(t)/s(t), IEEE RN (R1); 0 if not EVICTABLE
-          bad |= (size == 0) | (size >= kSizeLimit) | (state > 2u) |
-                 (ev & (!(c >= 0.0 && c <= 1.7976931348623157e308) |
-                        !(st >= 1.0 && st <= 1.7976931348623157e308) |
-                        ((h != 0.0) & ((h < 0x1p-64) | (h >= 0x1p60)))));
-          nzmask |= (uint32_t)(h != 0.0) << (q + r);
-          barmask |= (uint32_t)(state == COOP_PINNED) << (q + r);
-          hslot = (state == COOP_FREE) ? -0.0 : h;  // FREE: h = 0, sign = not an eviction
-        }
-        cx.spre[q + r] = sacc;
-        cx.hpre[q + r] = hacc;
-        sacc += size;
-        hacc = __dadd_rn(hacc, h);
-        hs[r] = hslot;
-      }
-      if (k < n) sm<double2>(cx.vr, o) = make_double2(hs[0], hs[1]);
+    if (a.dbg == 1) {
+      if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK);
+      goto pool_done;
     }
-    cx.barmask = barmask;
-    cx.nzmask = nzmask;
-
-    // ---------------- block scan: S (u64), H^ (fp64), next PINNED / next nonzero-h ------
-    uint64_t sinc = sacc;
-    double hinc = hacc;
-    int32_t fb = barmask ? cx.k0 + __ffs(barmask) - 1 : kInfIdx;
-    int32_t fz = nzmask ? cx.k0 + __ffs(nzmask) - 1 : kInfIdx;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t so = __shfl_up_sync(0xffffffffu, sinc, d);
-      const double ho = __shfl_up_sync(0xffffffffu, hinc, d);
-      const int32_t bo = __shfl_down_sync(0xffffffffu, fb, d);
-      const int32_t zo = __shfl_down_sync(0xffffffffu, fz, d);
-      if (lane >= d) {
-        sinc += so;
-        hinc = __dadd_rn(ho, hinc);
-      }
-      if (lane + d < 32) {
-        fb = min(fb, bo);
-        fz = min(fz, zo);
-      }
-    }
-    uint64_t sexc = __shfl_up_sync(0xffffffffu, sinc, 1);
-    double hexc = __shfl_up_sync(0xffffffffu, hinc, 1);
-    int32_t bexc = __shfl_down_sync(0xffffffffu, fb, 1);
-    int32_t zexc = __shfl_down_sync(0xffffffffu, fz, 1);
-    if (lane == 0) {
-      sexc = 0;
-      hexc = 0.0;
-    }
-    if (lane == 31) {
-      bexc = kInfIdx;
-      zexc = kInfIdx;
-      sc.wS[warp] = sinc;
-      sc.wH[warp] = hinc;
-    }
-    if (lane == 0) {
-      sc.wF[warp] = fb;
-      sc.wZ[warp] = fz;
-    }
-    const int bad_any = __syncthreads_or(bad);
     {
-      // cross-warp: lane l < W holds warp l's totals; shuffle scan over the (<= 16) warps
-      uint64_t ws = lane < W ? sc.wS[lane] : 0ull;
-      double wh = lane < W ? sc.wH[lane] : 0.0;
-      int32_t wb = lane < W ? sc.wF[lane] : kInfIdx;
-      int32_t wz = lane < W ? sc.wZ[lane] : kInfIdx;
-#pragma unroll
-      for (int d = 1; d < kMaxWarps; d <<= 1) {
-        const uint64_t so = __shfl_up_sync(0xffffffffu, ws, d);
-        const double ho = __shfl_up_sync(0xffffffffu, wh, d);
-        const int32_t bo = __shfl_down_sync(0xffffffffu, wb, d);
-        const int32_t zo = __shfl_down_sync(0xffffffffu, wz, d);
-        if (lane >= d) {
-          ws += so;
-          wh = __dadd_rn(ho, wh);
-        }
-        if (lane + d < 32) {
-          wb = min(wb, bo);
-          wz = min(wz, zo);
-        }
-      }
-      const uint64_t sprev = __shfl_sync(0xffffffffu, ws, warp ? warp - 1 : 0);
-      const double hprev = __shfl_sync(0xffffffffu, wh, warp ? warp - 1 : 0);
-      const int32_t bnext = __shfl_sync(0xffffffffu, wb, min(warp + 1, 31));
-      const int32_t znext = __shfl_sync(0xffffffffu, wz, min(warp + 1, 31));
-      cx.S_car = (warp ? sprev : 0ull) + sexc;
-      cx.H_car = __dadd_rn(warp ? hprev : 0.0, hexc);
-      cx.nb_right = min(bexc, warp + 1 < W ? bnext : kInfIdx);
-      cx.nz_right = min(zexc, warp + 1 < W ? znext : kInfIdx);
-      cx.S_total = __shfl_sync(0xffffffffu, ws, W - 1);
-    }
-    if (!bad_any) {
+      // ---------------- phase A: decode, validate, h = c/s, local prefixes -------------
+      bool bad = (Rraw == 0);
+      uint32_t barmask = 0, nzmask = 0;
+      uint64_t spre[K];
+      double hpre[K];
+      uint64_t sacc = 0;
+      double hacc = 0.0;
 #pragma unroll
       for (int q = 0; q < K; q += 2) {
-        const int k = cx.k0 + q;
+        const int k = k0 + q;
+        uint64_t sv[2] = {0, 0};
+        double cv[2] = {0.0, 0.0}, tv[2] = {1.0, 1.0};
+        const uint32_t o = swz((uint32_t)k);
         if (k < n) {
-          const uint32_t o = swz((uint32_t)k);
-          sm<ulonglong2>(cx.sr, o) = make_ulonglong2(cx.S_car + cx.spre[q], cx.S_car + cx.spre[q + 1]);
-          sm<double2>(cx.hr, o) = make_double2(__dadd_rn(cx.H_car, cx.hpre[q]),
-                                               __dadd_rn(cx.H_car, cx.hpre[q + 1]));
+          const ulonglong2 vs = sm<ulonglong2>(v.sr, o);
+          const double2 vc = sm<double2>(v.hr, o);
+          const double2 vt = sm<double2>(v.vr, o);
+          sv[0] = vs.x; sv[1] = vs.y; cv[0] = vc.x; cv[1] = vc.y; tv[0] = vt.x; tv[1] = vt.y;
+        }
+        double hs[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int kk = k + r;
+          uint64_t size = 0;
+          double h = 0.0, hslot = 0.0;
+          if (kk < n) {
+            const uint32_t state = (uint32_t)(sv[r] >> 62);
+            const bool ev = (state == COOP_EVICTABLE);
+            size = sv[r] & kSizeMask;
+            const double c = ev ? cv[r] : 1.0, st = ev ? tv[r] : 1.0;  // 1/1: no slow path
+            h = ev ? __ddiv_rn(c, st) : 0.0;  // h(t) = c(t)/s(t), IEEE RN (R1)
+            bad |= (size == 0) | (size >= kSizeLimit) | (state > 2u) |
+                   (ev & (!(c >= 0.0 && c <= 1.7976931348623157e308) |
+                          !(st >= 1.0 && st <= 1.7976931348623157e308) |
+                          ((h != 0.0) & ((h < 0x1p-64) | (h >= 0x1p60)))));
+            nzmask |= (uint32_t)(h != 0.0) << (q + r);
+            barmask |= (uint32_t)(state == COOP_PINNED) << (q + r);
+            // FREE: h = 0, sign = not an eviction; PINNED: NaN (never summed)
+            hslot = (state == COOP_FREE) ? -0.0 : (state == COOP_PINNED ? __longlong_as_double(0x7ff8000000000000ll) : h);
+          }
+          spre[q + r] = sacc;
+          hpre[q + r] = hacc;
+          sacc += size;
+          hacc = __dadd_rn(hacc, h);
+          hs[r] = hslot;
+        }
+        if (k < n) sm<double2>(v.vr, o) = make_double2(hs[0], hs[1]);
+      }
+
+      // ---------------- block scan: S (u64), H^ (fp64), next PINNED / next nonzero-h ------
+      uint64_t sinc = sacc;
+      double hinc = hacc;
+      int32_t fb = barmask ? k0 + __ffs(barmask) - 1 : kInfIdx;
+      int32_t fz = nzmask ? k0 + __ffs(nzmask) - 1 : kInfIdx;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t so = __shfl_up_sync(0xffffffffu, sinc, d);
+        const double ho = __shfl_up_sync(0xffffffffu, hinc, d);
+        const int32_t bo = __shfl_down_sync(0xffffffffu, fb, d);
+        const int32_t zo = __shfl_down_sync(0xffffffffu, fz, d);
+        if (lane >= d) {
+          sinc += so;
+          hinc = __dadd_rn(ho, hinc);
+        }
+        if (lane + d < 32) {
+          fb = min(fb, bo);
+          fz = min(fz, zo);
         }
       }
-      if (cx.k0 <= n - 1 && n - 1 < cx.k0 + K) {  // sentinels at slot n
-        sm<uint64_t>(cx.sr, swz((uint32_t)n)) = cx.S_total;
-        sm<double>(cx.hr, swz((uint32_t)n)) = __dadd_rn(cx.H_car, hacc);
+      uint64_t sexc = __shfl_up_sync(0xffffffffu, sinc, 1);
+      double hexc = __shfl_up_sync(0xffffffffu, hinc, 1);
+      int32_t bexc = __shfl_down_sync(0xffffffffu, fb, 1);
+      int32_t zexc = __shfl_down_sync(0xffffffffu, fz, 1);
+      if (lane == 0) {
+        sexc = 0;
+        hexc = 0.0;
       }
-    }
-    __syncthreads();
-
-    if (bad_any) {
-      if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_ERR_INVALID_ARG);
-    } else {
-      // ---------------- phase B1: zero-cost windows (h = 0 runs covering R) -------------
-      const int zw = warp_allreduce(cx.zero_start(), [](int x, int y) { return min(x, y); });
-      if (lane == 0) sc.wZ[warp] = zw;
+      if (lane == 31) {
+        bexc = kInfIdx;
+        zexc = kInfIdx;
+        sc.wS[warp] = sinc;
+        sc.wH[warp] = hinc;
+      }
+      if (lane == 0) {
+        sc.wF[warp] = fb;
+        sc.wZ[warp] = fz;
+      }
+      const int bad_any = __syncthreads_or(bad);
+      uint64_t S_car, S_total;
+      double H_car;
+      int32_t nb_right, nz_right;
+      {
+        // cross-warp: lane l < W holds warp l's totals; shuffle scan over the (<= 16) warps
+        uint64_t ws = lane < W ? sc.wS[lane] : 0ull;
+        double wh = lane < W ? sc.wH[lane] : 0.0;
+        int32_t wb = lane < W ? sc.wF[lane] : kInfIdx;
+        int32_t wz = lane < W ? sc.wZ[lane] : kInfIdx;
+#pragma unroll
+        for (int d = 1; d < kMaxWarps; d <<= 1) {
+          const uint64_t so = __shfl_up_sync(0xffffffffu, ws, d);
+          const double ho = __shfl_up_sync(0xffffffffu, wh, d);
+          const int32_t bo = __shfl_down_sync(0xffffffffu, wb, d);
+          const int32_t zo = __shfl_down_sync(0xffffffffu, wz, d);
+          if (lane >= d) {
+            ws += so;
+            wh = __dadd_rn(ho, wh);
+          }
+          if (lane + d < 32) {
+            wb = min(wb, bo);
+            wz = min(wz, zo);
+          }
+        }
+        const uint64_t sprev = __shfl_sync(0xffffffffu, ws, warp ? warp - 1 : 0);
+        const double hprev = __shfl_sync(0xffffffffu, wh, warp ? warp - 1 : 0);
+        const int32_t bnext = __shfl_sync(0xffffffffu, wb, min(warp + 1, 31));
+        const int32_t znext = __shfl_sync(0xffffffffu, wz, min(warp + 1, 31));
+        S_car = (warp ? sprev : 0ull) + sexc;
+        H_car = __dadd_rn(warp ? hprev : 0.0, hexc);
+        nb_right = min(bexc, warp + 1 < W ? bnext : kInfIdx);
+        nz_right = min(zexc, warp + 1 < W ? znext : kInfIdx);
+        S_total = __shfl_sync(0xffffffffu, ws, W - 1);
+      }
+      v.S_total = S_total;
+      if (!bad_any) {
+#pragma unroll
+        for (int q = 0; q < K; q += 2) {
+          const int k = k0 + q;
+          if (k < n) {
+            const uint32_t o = swz((uint32_t)k);
+            sm<ulonglong2>(v.sr, o) = make_ulonglong2(S_car + spre[q], S_car + spre[q + 1]);
+            sm<double2>(v.hr, o) = make_double2(__dadd_rn(H_car, hpre[q]), __dadd_rn(H_car, hpre[q + 1]));
+          }
+        }
+        if (k0 <= n - 1 && n - 1 < k0 + K) {  // sentinels at slots n, n + 1
+          sm<uint64_t>(v.sr, swz((uint32_t)n)) = S_total;
+          sm<uint64_t>(v.sr, swz((uint32_t)n + 1u)) = ~0ull;
+          sm<double>(v.hr, swz((uint32_t)n)) = __dadd_rn(H_car, hacc);
+        }
+      }
       __syncthreads();
-      const int zmin = warp_allreduce(lane < W ? sc.wZ[lane] : kInfIdx,
-                                      [](int x, int y) { return min(x, y); });
-      double Umin = kInf, L_t = kInf;
-      uint64_t xbest = ~0ull;  // best exactly-costed window (length <= 2): bits, start, end
-      int xfirst = kInfIdx, xend = -1;
-      if (zmin == kInfIdx) {
-        // ---------------- phase B2: window ends + fp64 filter ----------------------------
-        double U_t = kInf;
-        uint64_t xb = ~0ull;
-        int xi = kInfIdx, xe = -1;
-        cx.template walk<0>(0, 0.0, sc, U_t, L_t, xb, xi, xe);
-        const double Uw = warp_allreduce(U_t, [](double x, double y) { return fmin(x, y); });
-        const uint64_t xw = warp_allreduce(xb, [](uint64_t x, uint64_t y) { return x < y ? x : y; });
+
+      if (bad_any || a.dbg == 2) {
+        if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_ERR_INVALID_ARG);
+      } else {
+        // ---------------- phase B: window ends (merge path), then the fp64 filter ----------
+        v.merge_path(tid, T);
+        __syncthreads();
+        LaneBest bl;
+        bl.U = kInf; bl.L = kInf; bl.L2 = kInf; bl.li = -1; bl.le = -1;
+        bl.xb = ~0ull; bl.xi = kInfIdx; bl.xe = -1;
+        filter_starts<K, 0>(v, k0, barmask, nzmask, nb_right, nz_right, hpre, H_car, 0.0, 0, 0, sc, bl);
+        const double Uw = warp_allreduce(bl.U, [](double x, double y) { return fmin(x, y); });
+        const uint64_t xw = warp_allreduce(bl.xb, [](uint64_t x, uint64_t y) { return x < y ? x : y; });
         if (lane == 0) {
           sc.wU[warp] = Uw;
           sc.bcost[warp] = xw;
         }
+        if (tid == 0) sc.ncand = 0;
         __syncthreads();
-        Umin = warp_allreduce(lane < W ? sc.wU[lane] : kInf,
-                              [](double x, double y) { return fmin(x, y); });
-        xbest = warp_allreduce(lane < W ? sc.bcost[lane] : ~0ull,
-                               [](uint64_t x, uint64_t y) { return x < y ? x : y; });
-        if (xbest != ~0ull) {  // lowest start among the exact windows with that cost
-          const int xiw = warp_allreduce(xb == xbest ? xi : kInfIdx, [](int x, int y) { return min(x, y); });
-          if (lane == 0) sc.bfirst[warp] = xiw;
-          __syncthreads();
-          xfirst = warp_allreduce(lane < W ? sc.bfirst[lane] : kInfIdx, [](int x, int y) { return min(x, y); });
-          if (xi == xfirst) sc.ncand = xe;  // unique owner publishes the end
-          __syncthreads();
-          xend = sc.ncand;
+        const double Umin = warp_allreduce(lane < W ? sc.wU[lane] : kInf,
+                                           [](double x, double y) { return fmin(x, y); });
+        const uint64_t xbest = warp_allreduce(lane < W ? sc.bcost[lane] : ~0ull,
+                                              [](uint64_t x, uint64_t y) { return x < y ? x : y; });
+        const double thresh = fmin(Umin, __longlong_as_double((long long)xbest)) * (1.0 + 0x1p-45);
+        // a lane with exactly one start under the threshold appends it; two or more re-walk
+        const bool multi = (bl.L2 <= thresh);
+        if (bl.L <= thresh && !multi) {
+          const int slot = atomicAdd(&sc.ncand, 1);
+          if (slot < kCandCap) sc.cand[slot] = ((uint32_t)bl.li << 16) | (uint32_t)(bl.le - bl.li);
         }
-      }
-      if (zmin != kInfIdx) {
-        // exact cost 0 is the minimum; the lowest start wins, with its minimal end
-        if (warp == 0) {
-          const int i = zmin;
-          const uint64_t target = cx.S_at(i) + cx.R;
-          int lo = i + 1, hi = n;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (cx.S_at(mid) >= target) hi = mid;
-            else lo = mid + 1;
-          }
-          const int e = lo;
-          int nev = 0;
-          for (int k = i + lane; k < e; k += 32)
-            nev += (__double_as_longlong(cx.h_at(k)) >= 0);  // sign clear: EVICTABLE
-          nev = warp_allreduce(nev, [](int x, int y) { return x + y; });
-          if (lane == 0) write_result(a.out + p, i, e - 1, cx.S_at(e) - cx.S_at(i), 0.0, nev, COOP_OK);
+        const int xiw = warp_allreduce(bl.xb == xbest ? bl.xi : kInfIdx, [](int x, int y) { return min(x, y); });
+        const int mw = __any_sync(0xffffffffu, multi) ? 1 : 0;
+        if (lane == 0) {
+          sc.bfirst[warp] = xiw;
+          sc.bnev[warp] = mw;
         }
-      } else if (Umin == kInf && xbest == ~0ull) {
-        if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_INFEASIBLE);
-      } else {
-        // ------------- candidates: exact 192-bit re-summation, RN, (cost, first) min --
-        const double xval = __longlong_as_double((long long)xbest);
-        const double thresh = fmin(Umin, xval) * (1.0 + 0x1p-45);
-        int resume = (L_t <= thresh) ? 0 : K;
-        uint64_t best = xbest;  // meaningful in thread 0
-        int bfirst = xfirst, bend = xend, bnev = 0;
-        if (tid == 0 && xbest != ~0ull)
-          for (int k = xfirst; k < xend; ++k) bnev += (__double_as_longlong(cx.h_at(k)) >= 0);
-        const int any_cand = __syncthreads_or(resume < K);
-        while (any_cand) {
-          if (tid == 0) sc.ncand = 0;
-          __syncthreads();
-          if (resume < K) {
-            double du = 0, dl = 0;
-            uint64_t dxb = 0;
-            int dxi = 0, dxe = 0;
-            resume = cx.template walk<1>(resume, thresh, sc, du, dl, dxb, dxi, dxe);
+        __syncthreads();
+        const int xfirst = warp_allreduce(lane < W ? sc.bfirst[lane] : kInfIdx, [](int x, int y) { return min(x, y); });
+        const int any_multi = warp_allreduce(lane < W ? sc.bnev[lane] : 0, [](int x, int y) { return x | y; });
+        const int nc0 = sc.ncand;
+        const bool x_owner = (xbest != ~0ull) && bl.xi == xfirst && bl.xb == xbest;
+        if (Umin == kInf && xbest == ~0ull) {
+          if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_INFEASIBLE);
+        } else if (nc0 == 0 && !any_multi) {
+          // no window of inexactly known cost can reach the exact best: the owner writes
+          if (x_owner) {
+            int nev = 0;
+            for (int k = bl.xi; k < bl.xe; ++k) nev += (__double_as_longlong(v.v_at(k)) >= 0);
+            write_result(a.out + p, bl.xi, bl.xe - 1, v.S_at(bl.xe) - v.S_at(bl.xi),
+                         __longlong_as_double((long long)xbest), nev, COOP_OK);
           }
-          const int pending = __syncthreads_or(resume < K);
-          const int nc = min(sc.ncand, kCandCap);
-          if (nc <= W) {
-            // few candidates: the whole CTA sums each window (short latency chain)
-            for (int c = 0; c < nc; ++c) {
-              const uint32_t cd = sc.cand[c];
-              const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
-              U192 acc = u192_zero();
-              int nev = 0;
-              if (i + warp * 32 < e) {  // warp-uniform: warps without items skip the shuffles
-                for (int k = i + tid; k < e; k += T) {
-                  const double hv = cx.h_at(k);
+        } else {
+          // ------------- candidates: exact 192-bit re-summation, RN, (cost, first) min ----
+          if (x_owner) {
+            int nev = 0;
+            for (int k = bl.xi; k < bl.xe; ++k) nev += (__double_as_longlong(v.v_at(k)) >= 0);
+            sc.xend = bl.xe;
+            sc.xnev = nev;
+          }
+          __syncthreads();
+          uint64_t best = xbest;  // meaningful in thread 0
+          int bfirst = xfirst, bend = xbest != ~0ull ? sc.xend : -1, bnev = xbest != ~0ull ? sc.xnev : 0;
+          const bool wmulti = __any_sync(0xffffffffu, bl.L <= thresh);  // this warp holds candidates
+          // rounds: the prebuilt list (no multi), or re-walks restricted to windows of
+          // kCandCap consecutive starts (cannot overflow the list)
+          const int rounds = any_multi ? (n + kCandCap - 1) / kCandCap : 1;
+          for (int rd = 0; rd < rounds; ++rd) {
+            if (any_multi) {
+              __syncthreads();
+              if (tid == 0) sc.ncand = 0;
+              __syncthreads();
+              const int w_lo = rd * kCandCap, w_hi = w_lo + kCandCap;
+              if (wmulti && k0 < w_hi && k0 + K > w_lo) {
+                LaneBest dummy = bl;
+                filter_starts<K, 1>(v, k0, barmask, nzmask, nb_right, nz_right, hpre, H_car, thresh, w_lo, w_hi, sc, dummy);
+              }
+              __syncthreads();
+            }
+            const int nc = min(sc.ncand, kCandCap);
+            if (nc <= W) {
+              // few candidates: the whole CTA sums each window (short latency chain)
+              for (int c = 0; c < nc; ++c) {
+                const uint32_t cd = sc.cand[c];
+                const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
+                U192 acc = u192_zero();
+                int nev = 0;
+                if (i + warp * 32 < e) {  // warp-uniform: warps without items skip
+                  for (int k = i + tid; k < e; k += T) {
+                    const double hv = v.v_at(k);
+                    nev += (__double_as_longlong(hv) >= 0);
+                    acc = u192_add(acc, u192_from_double(hv));
+                  }
+                  acc = warp_sum192(acc, nev);
+                }
+                const int par = c & 1;
+                if (lane == 0) {
+                  sc.part[par][warp][0] = acc.w0;
+                  sc.part[par][warp][1] = acc.w1;
+                  sc.part[par][warp][2] = acc.w2;
+                  sc.partn[par][warp] = nev;
+                }
+                __syncthreads();
+                if (warp == 0) {
+                  U192 t = u192_zero();
+                  int tn = 0;
+                  if (lane < W) {
+                    t.w0 = sc.part[par][lane][0];
+                    t.w1 = sc.part[par][lane][1];
+                    t.w2 = sc.part[par][lane][2];
+                    tn = sc.partn[par][lane];
+                  }
+                  t = warp_sum192(t, tn);
+                  const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(t));
+                  if (lane == 0 && better(cb, i, best, bfirst)) {
+                    best = cb;
+                    bfirst = i;
+                    bend = e;
+                    bnev = tn;
+                  }
+                }
+              }
+            } else {
+              // many candidates: one warp per candidate window
+              uint64_t wbest = ~0ull;
+              int32_t wfirst = kInfIdx, wend = -1, wnev = 0;
+              for (int c = warp; c < nc; c += W) {
+                const uint32_t cd = sc.cand[c];
+                const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
+                U192 acc = u192_zero();
+                int nev = 0;
+                for (int k = i + lane; k < e; k += 32) {
+                  const double hv = v.v_at(k);
                   nev += (__double_as_longlong(hv) >= 0);
                   acc = u192_add(acc, u192_from_double(hv));
                 }
                 acc = warp_sum192(acc, nev);
+                const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(acc));
+                if (better(cb, i, wbest, wfirst)) {
+                  wbest = cb;
+                  wfirst = i;
+                  wend = e;
+                  wnev = nev;
+                }
               }
-              const int par = c & 1;
               if (lane == 0) {
-                sc.part[par][warp][0] = acc.w0;
-                sc.part[par][warp][1] = acc.w1;
-                sc.part[par][warp][2] = acc.w2;
-                sc.partn[par][warp] = nev;
+                sc.bcost[warp] = wbest;
+                sc.bfirst[warp] = wfirst;
+                sc.bend[warp] = wend;
+                sc.bnev[warp] = wnev;
               }
               __syncthreads();
-              if (warp == 0) {
-                U192 t = u192_zero();
-                int tn = 0;
-                if (lane < W) {
-                  t.w0 = sc.part[par][lane][0];
-                  t.w1 = sc.part[par][lane][1];
-                  t.w2 = sc.part[par][lane][2];
-                  tn = sc.partn[par][lane];
-                }
-                t = warp_sum192(t, tn);
-                const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(t));
-                if (lane == 0 && better(cb, i, best, bfirst)) {
-                  best = cb;
-                  bfirst = i;
-                  bend = e;
-                  bnev = tn;
-                }
-              }
-            }
-          } else {
-            // many candidates: one warp per candidate window
-            uint64_t wbest = ~0ull;
-            int32_t wfirst = kInfIdx, wend = -1, wnev = 0;
-            for (int c = warp; c < nc; c += W) {
-              const uint32_t cd = sc.cand[c];
-              const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
-              U192 acc = u192_zero();
-              int nev = 0;
-              for (int k = i + lane; k < e; k += 32) {
-                const double hv = cx.h_at(k);
-                nev += (__double_as_longlong(hv) >= 0);
-                acc = u192_add(acc, u192_from_double(hv));
-              }
-              acc = warp_sum192(acc, nev);
-              const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(acc));
-              if (better(cb, i, wbest, wfirst)) {
-                wbest = cb;
-                wfirst = i;
-                wend = e;
-                wnev = nev;
-              }
-            }
-            if (lane == 0) {
-              sc.bcost[warp] = wbest;
-              sc.bfirst[warp] = wfirst;
-              sc.bend[warp] = wend;
-              sc.bnev[warp] = wnev;
-            }
-            __syncthreads();
-            if (tid == 0) {
-              for (int w = 0; w < W; ++w) {
-                if (sc.bend[w] >= 0 && better(sc.bcost[w], sc.bfirst[w], best, bfirst)) {
-                  best = sc.bcost[w];
-                  bfirst = sc.bfirst[w];
-                  bend = sc.bend[w];
-                  bnev = sc.bnev[w];
+              if (tid == 0) {
+                for (int w = 0; w < W; ++w) {
+                  if (sc.bend[w] >= 0 && better(sc.bcost[w], sc.bfirst[w], best, bfirst)) {
+                    best = sc.bcost[w];
+                    bfirst = sc.bfirst[w];
+                    bend = sc.bend[w];
+                    bnev = sc.bnev[w];
+                  }
                 }
               }
             }
           }
-          if (!pending) break;
-          __syncthreads();  // the candidate list is rewritten next round
+          if (tid == 0)
+            write_result(a.out + p, bfirst, bend - 1, v.S_at(bend) - v.S_at(bfirst),
+                         __longlong_as_double((long long)best), bnev, COOP_OK);
         }
-        if (tid == 0)
-          write_result(a.out + p, bfirst, bend - 1, cx.S_at(bend) - cx.S_at(bfirst),
-                       __longlong_as_double((long long)best), bnev, COOP_OK);
       }
     }
+  pool_done:
     __syncthreads();  // stage s fully consumed
     if (a.use_tma && tid == 0) {
       const int64_t pn = p + (int64_t)a.stages * gridDim.x;
@@ -703,7 +720,7 @@ bool make_map(CUtensorMap *m, const void *ptr, int64_t stride, int64_t n_pools, 
   return r == CUDA_SUCCESS;
 }
 
-template <int K>
+template <int K, int MAXT, int MINB>
 int launch_k(const Args &a0, cudaStream_t st) {
   Args a = a0;
   const int rows = (a.n + 15) / 16;
@@ -725,8 +742,17 @@ int launch_k(const Args &a0, cudaStream_t st) {
   int max_smem = 0, sms = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t fixed = sizeof(Scratch) + 1024;
-  a.stages = (2 * (size_t)a.stage_bytes + fixed <= (size_t)max_smem) ? 2 : 1;
+  const size_t fixed = (sizeof(Scratch) + 15) / 16 * 16 + ((size_t)threads * K + 16) * 2 + 1024;  // + E[]
+  // MINB CTAs per SM share the SM's shared memory (228 KiB less 1 KiB per CTA reserved);
+  // each CTA double-buffers only if that still fits
+  size_t per_cta = (size_t)max_smem;
+  if (MINB > 1) {
+    int sm_total = 0;
+    cudaDeviceGetAttribute(&sm_total, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    per_cta = (size_t)sm_total / MINB - 1024;
+    if (per_cta > (size_t)max_smem) per_cta = (size_t)max_smem;
+  }
+  a.stages = (2 * (size_t)a.stage_bytes + fixed <= per_cta) ? 2 : 1;
   const size_t smem = (size_t)a.stages * a.stage_bytes + fixed;
   if (smem > (size_t)max_smem) return COOP_ERR_INVALID_ARG;
 
@@ -735,6 +761,10 @@ int launch_k(const Args &a0, cudaStream_t st) {
   memset(&m_c, 0, sizeof(m_c));
   memset(&m_s, 0, sizeof(m_s));
   a.use_tma = 0;
+  {
+    const char *d = getenv("COOP_SEARCH_DBG");
+    a.dbg = d ? atoi(d) : 0;
+  }
   const bool aligned = ((uintptr_t)a.ss % 16 == 0) && ((uintptr_t)a.cost % 16 == 0) &&
                        ((uintptr_t)a.stale % 16 == 0) && (a.stride % 16 == 0) &&
                        (a.n_pools < (1ll << 31)) && !coop_force_plain_staging();
@@ -743,7 +773,8 @@ int launch_k(const Args &a0, cudaStream_t st) {
       make_map(&m_s, a.stale, a.stride, a.n_pools, a.box_rows))
     a.use_tma = 1;
 
-  auto kern = search_kernel<K>;
+  if (threads > MAXT) return COOP_ERR_INVALID_ARG;
+  auto kern = search_kernel<K, MAXT, MINB>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return COOP_ERR_CUDA;
@@ -771,8 +802,11 @@ int launch_window_search(const coop_tables_soa *t, const uint64_t *requests, coo
   a.stride = t->pool_stride;
   a.n = t->n_blocks;
   if (a.n_pools == 0) return COOP_OK;
-  if (a.n <= 4096) return launch_k<8>(a, st);
-  return launch_k<16>(a, st);
+  const char *two = getenv("COOP_SEARCH_TWO_CTA");  // profiling hook: 2 CTAs/SM, 1 stage
+  if (two && two[0] == '1' && a.n <= 4096) return launch_k<16, 256, 2>(a, st);
+  if (a.n <= 2048) return launch_k<8, 256, 2>(a, st);  // 2 CTAs per SM
+  if (a.n <= 4096) return launch_k<8, 512, 1>(a, st);  // 1 CTA per SM, 2 stages
+  return launch_k<16, 512, 1>(a, st);
 }
 
 }  // namespace coop
