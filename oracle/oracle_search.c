@@ -77,7 +77,8 @@ double orc_fsum(const double *x, int64_t n) {
       if (yy == yr) hi = xx;
     }
   }
-  return hi;
+  /* the exact real sum 0 is represented as +0.0 (as math.fsum does for -0.0 inputs) */
+  return hi == 0.0 ? 0.0 : hi;
 }
 
 static void set_empty(orc_window *o, int status) {

@@ -37,6 +37,8 @@ constexpr int kCap = 2048;       // blocks per pool held by the kernel (COOP_ERR
 constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
 constexpr int kDfsCap = 512;     // per-thread DFS stack (projected-cost closures)
 constexpr int kFree = -1;
+constexpr int kMaxT = 16384;     // tensors per trace whose flags live in shared memory
+constexpr int kVisCap = 64;      // per-thread DFS visited set in shared memory (power of 2)
 
 enum : uint8_t { TF_RES = 1, TF_BORN = 2, TF_DEAD = 4, TF_LOCK = 8 };
 
@@ -90,9 +92,14 @@ struct KArgs {
 };
 
 struct Shared {
-  uint64_t addr[2][kCap];
-  uint64_t size[2][kCap];
-  int32_t owner[2][kCap];
+  uint64_t addr[2][kCap + 2];  // the inactive buffer doubles as search scratch (S, B, state)
+  uint64_t size[2][kCap + 2];
+  int32_t owner[2][kCap + 2];
+  uint8_t tfl[kMaxT];          // per-tensor flags TF_*
+  uint32_t vis[kThreads][kVisCap];  // per-thread open-addressing set of visited tensors (DFS)
+  uint64_t wS[kWarps];
+  U192 wH[kWarps];
+  int32_t wB[kWarps];
   int32_t cur, nb;
   // CTA-uniform scalars (written by thread 0, published by a barrier)
   uint64_t bytes_free;
@@ -313,7 +320,7 @@ struct Cell {
     const int b = block_of_addr(ad);
     release(b);
     if (threadIdx.x == 0) {
-      w.tflags[t] &= (uint8_t)~TF_RES;
+      sh.tfl[t] &= (uint8_t)~TF_RES;
       log_ev(4, sh.cur_op, t, ad);
     }
     __syncthreads();
@@ -333,64 +340,121 @@ struct Cell {
   // non-resident tensors + the SET of evicted descendants reachable through evicted
   // tensors (R18).  One thread; visited marks = per-thread epochs.
   __device__ int64_t projected_cost(int t, bool &overflow) {
+    const int op = __ldg(&tr.producer[t]);
+    int64_t c = __ldg(&tr.cost[op]);
+    // quick path: no non-resident input and no evicted consumer output -> c = own cost
+    bool simple = true;
+    for (int j = __ldg(&tr.in_ptr[op]); j < __ldg(&tr.in_ptr[op + 1]) && simple; ++j) {
+      const int u = __ldg(&tr.in_idx[j]);
+      if (!(sh.tfl[u] & TF_RES) && __ldg(&tr.producer[u]) >= 0) simple = false;
+    }
+    for (int j = __ldg(&tr.cons_ptr[t]); j < __ldg(&tr.cons_ptr[t + 1]) && simple; ++j) {
+      const uint8_t f = sh.tfl[__ldg(&tr.out[__ldg(&tr.cons_idx[j])])];
+      if ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD)) simple = false;
+    }
+    if (simple) return c;
+    // Only non-resident tensors contribute and expand, so only they need the visited set
+    // (a resident tensor reached twice is skipped twice).  The set lives in this thread's
+    // shared-memory slots (open addressing, key = tensor + 1); on overflow the closure is
+    // redone with the per-thread global marks.
+    uint32_t *vs = sh.vis[threadIdx.x];
+    for (int k = 0; k < kVisCap; ++k) vs[k] = 0u;
+    int nvis = 0;
+    bool use_marks = false;
     uint32_t *mk = w.marks + (size_t)threadIdx.x * tr.T;
-    const uint32_t ep = ++epoch;
-    int stk[kDfsCap];
-    int sp = 0;
-    const int op = tr.producer[t];
-    int64_t c = tr.cost[op];
-    mk[t] = ep;
-    for (int j = tr.in_ptr[op]; j < tr.in_ptr[op + 1]; ++j) {
-      if (sp == kDfsCap) { overflow = true; return c; }
-      stk[sp++] = tr.in_idx[j];
-    }
-    while (sp > 0) {
-      const int u = stk[--sp];
-      if (mk[u] == ep) continue;
-      mk[u] = ep;
-      if ((w.tflags[u] & TF_RES) || tr.producer[u] < 0) continue;
-      const int pu = tr.producer[u];
-      c += tr.cost[pu];
-      for (int j = tr.in_ptr[pu]; j < tr.in_ptr[pu + 1]; ++j) {
-        if (sp == kDfsCap) { overflow = true; return c; }
-        stk[sp++] = tr.in_idx[j];
+    uint32_t ep = 0;
+    auto seen = [&](int x) -> bool {  // test-and-insert
+      if (use_marks) {
+        if (mk[x] == ep) return true;
+        mk[x] = ep;
+        return false;
       }
-    }
-    for (int j = tr.cons_ptr[t]; j < tr.cons_ptr[t + 1]; ++j) {
-      if (sp == kDfsCap) { overflow = true; return c; }
-      stk[sp++] = tr.out[tr.cons_idx[j]];
-    }
-    while (sp > 0) {
-      const int d = stk[--sp];
-      if (mk[d] == ep) continue;
-      mk[d] = ep;
-      const uint8_t f = w.tflags[d];
-      if (!(f & TF_BORN) || (f & TF_RES) || (f & TF_DEAD)) continue;
-      c += tr.cost[tr.producer[d]];
-      for (int j = tr.cons_ptr[d]; j < tr.cons_ptr[d + 1]; ++j) {
-        if (sp == kDfsCap) { overflow = true; return c; }
-        stk[sp++] = tr.out[tr.cons_idx[j]];
+      uint32_t hsh = ((uint32_t)x * 2654435761u) & (kVisCap - 1);
+      while (true) {
+        const uint32_t k = vs[hsh];
+        if (k == (uint32_t)x + 1u) return true;
+        if (k == 0u) break;
+        hsh = (hsh + 1) & (kVisCap - 1);
       }
+      vs[hsh] = (uint32_t)x + 1u;
+      ++nvis;
+      return false;
+    };
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (attempt == 1) {
+        use_marks = true;
+        ep = ++epoch;
+        c = __ldg(&tr.cost[op]);
+      }
+      bool full = false;
+      int stk[kDfsCap];
+      int sp = 0;
+      for (int j = __ldg(&tr.in_ptr[op]); j < __ldg(&tr.in_ptr[op + 1]); ++j) {
+        if (sp == kDfsCap) { overflow = true; return c; }
+        stk[sp++] = __ldg(&tr.in_idx[j]);
+      }
+      while (sp > 0 && !full) {
+        const int u = stk[--sp];
+        if ((sh.tfl[u] & TF_RES) || __ldg(&tr.producer[u]) < 0) continue;
+        if (!use_marks && nvis >= kVisCap / 2) { full = true; break; }
+        if (seen(u)) continue;
+        const int pu = __ldg(&tr.producer[u]);
+        c += __ldg(&tr.cost[pu]);
+        for (int j = __ldg(&tr.in_ptr[pu]); j < __ldg(&tr.in_ptr[pu + 1]); ++j) {
+          if (sp == kDfsCap) { overflow = true; return c; }
+          stk[sp++] = __ldg(&tr.in_idx[j]);
+        }
+      }
+      if (full) continue;
+      for (int j = __ldg(&tr.cons_ptr[t]); j < __ldg(&tr.cons_ptr[t + 1]); ++j) {
+        if (sp == kDfsCap) { overflow = true; return c; }
+        stk[sp++] = __ldg(&tr.out[__ldg(&tr.cons_idx[j])]);
+      }
+      while (sp > 0 && !full) {
+        const int d = stk[--sp];
+        const uint8_t f = sh.tfl[d];
+        if (!(f & TF_BORN) || (f & TF_RES) || (f & TF_DEAD)) continue;
+        if (!use_marks && nvis >= kVisCap / 2) { full = true; break; }
+        if (seen(d)) continue;
+        c += __ldg(&tr.cost[__ldg(&tr.producer[d])]);
+        for (int j = __ldg(&tr.cons_ptr[d]); j < __ldg(&tr.cons_ptr[d + 1]); ++j) {
+          if (sp == kDfsCap) { overflow = true; return c; }
+          stk[sp++] = __ldg(&tr.out[__ldg(&tr.cons_idx[j])]);
+        }
+      }
+      if (!full) return c;
     }
     return c;
   }
 
   // ---------------------------------------------------------------- Sec. 3.3 search
   // Sliding-window search over the address-ordered item view and eviction of the window;
-  // returns false when no window exists (R24).
+  // returns false when no window exists (R24).  Scratch: the inactive block buffer holds
+  // S (span prefix, u64) in its addr[], B (barrier count prefix) in its size[] and the
+  // item states in its owner[]; the exact 192-bit prefix H and h live in global memory.
   __device__ bool evict_window(uint64_t need) {
     const uint64_t t0 = gtimer();
-    const int nb = sh.nb;
-    // item view: FREE -> h = 0; unevictable / pinned / locked -> barrier; else h = c/s
+    const int nb = sh.nb, nx = sh.cur ^ 1;
+    uint64_t *S = sh.addr[nx];
+    int32_t *Bc = reinterpret_cast<int32_t *>(sh.size[nx]);
+    int32_t *St = sh.owner[nx];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // item view (contiguous chunk per thread): FREE -> h = 0; unevictable / pinned /
+    // locked -> barrier; else h = c/s with the projected cost and the staleness
+    const int chunk = (nb + kThreads - 1) / kThreads;
+    const int b0 = min(nb, (int)threadIdx.x * chunk), b1 = min(nb, b0 + chunk);
     int nev = 0;
     bool overflow = false;
-    for (int b = threadIdx.x; b < nb; b += kThreads) {
+    uint64_t ls = 0;
+    U192 lh = u192_zero();
+    int lb = 0;
+    for (int b = b0; b < b1; ++b) {
       const int o = O()[b];
-      uint8_t st;
+      int st;
       double h = 0.0;
       if (o == kFree) {
         st = COOP_FREE;
-      } else if (tr.unevict[o] || w.pins[o] > 0 || (w.tflags[o] & TF_LOCK)) {
+      } else if (__ldg(&tr.unevict[o]) || w.pins[o] > 0 || (sh.tfl[o] & TF_LOCK)) {
         st = COOP_PINNED;
       } else {
         st = COOP_EVICTABLE;
@@ -399,90 +463,87 @@ struct Cell {
         h = __ddiv_rn((double)projected_cost(o, overflow), (double)s);
         ++nev;
       }
-      w.isz[b] = Z()[b];
       w.ih[b] = h;
-      w.ist[b] = st;
+      St[b] = st;
+      ls += Z()[b];
+      lh = u192_add(lh, u192_from_double(h));
+      lb += (st == COOP_PINNED);
     }
-    nev = cta_sum_i32(sh, nev);
+    // exclusive scans of the thread totals: warp shuffles, then the <= 8 warp totals
+    uint64_t is = ls;
+    U192 ih = lh;
+    int ib = lb;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t so = __shfl_up_sync(0xffffffffu, is, d);
+      U192 ho;
+      ho.w0 = __shfl_up_sync(0xffffffffu, ih.w0, d);
+      ho.w1 = __shfl_up_sync(0xffffffffu, ih.w1, d);
+      ho.w2 = __shfl_up_sync(0xffffffffu, ih.w2, d);
+      const int bo = __shfl_up_sync(0xffffffffu, ib, d);
+      if (lane >= d) {
+        is += so;
+        ih = u192_add(ih, ho);
+        ib += bo;
+      }
+    }
+    if (lane == 31) {
+      sh.wS[warp] = is;
+      sh.wH[warp] = ih;
+      sh.wB[warp] = ib;
+    }
+    nev = cta_sum_i32(sh, nev);  // (its barrier also publishes the warp totals)
     if (cta_max_i32(sh, overflow ? 1 : 0)) {
       if (threadIdx.x == 0) sh.status = COOP_ERR_NOMEM;
       __syncthreads();
       return false;
     }
-    // exclusive prefixes over items: span S (u64), exact heuristic H (192-bit fixed
-    // point, LSB 2^-116), barrier count B -- chunked per thread + serial carry by thread 0
-    const int chunk = (nb + kThreads - 1) / kThreads;
-    const int b0 = min(nb, (int)threadIdx.x * chunk), b1 = min(nb, b0 + chunk);
-    uint64_t ls = 0;
-    U192 lh = u192_zero();
-    int lb = 0;
+    uint64_t cs = is - ls;  // exclusive within the warp
+    U192 ch = u192_sub(ih, lh);
+    int cb = ib - lb;
+    for (int w2 = 0; w2 < warp; ++w2) {
+      cs += sh.wS[w2];
+      ch = u192_add(ch, sh.wH[w2]);
+      cb += sh.wB[w2];
+    }
     for (int b = b0; b < b1; ++b) {
-      ls += w.isz[b];
-      lh = u192_add(lh, u192_from_double(w.ih[b]));
-      lb += (w.ist[b] == COOP_PINNED);
+      S[b] = cs;
+      w.H[b] = ch;
+      Bc[b] = cb;
+      cs += Z()[b];
+      ch = u192_add(ch, u192_from_double(w.ih[b]));
+      cb += (St[b] == COOP_PINNED);
     }
-    // thread totals -> exclusive carries (serial over kThreads in thread 0; small)
-    U192 *totH = w.H + (kCap + 1);  // workspace has room for kThreads extra entries
-    uint64_t *totS = w.S + (kCap + 1);
-    int32_t *totB = w.B + (kCap + 1);
-    totS[threadIdx.x] = ls;
-    totH[threadIdx.x] = lh;
-    totB[threadIdx.x] = lb;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint64_t cs = 0;
-      U192 ch = u192_zero();
-      int cb = 0;
-      for (int t = 0; t < kThreads; ++t) {
-        const uint64_t s2 = totS[t];
-        const U192 h2 = totH[t];
-        const int b2 = totB[t];
-        totS[t] = cs;
-        totH[t] = ch;
-        totB[t] = cb;
-        cs += s2;
-        ch = u192_add(ch, h2);
-        cb += b2;
-      }
-      w.S[nb] = cs;
+    if (b1 == nb && b0 < b1) {
+      S[nb] = cs;
       w.H[nb] = ch;
-      w.B[nb] = cb;
+      Bc[nb] = cb;
+    }
+    if (nb == 0 && threadIdx.x == 0) {
+      S[0] = 0;
+      Bc[0] = 0;
     }
     __syncthreads();
-    {
-      uint64_t cs = totS[threadIdx.x];
-      U192 ch = totH[threadIdx.x];
-      int cb = totB[threadIdx.x];
-      for (int b = b0; b < b1; ++b) {
-        w.S[b] = cs;
-        w.H[b] = ch;
-        w.B[b] = cb;
-        cs += w.isz[b];
-        ch = u192_add(ch, u192_from_double(w.ih[b]));
-        cb += (w.ist[b] == COOP_PINNED);
-      }
-    }
-    __syncthreads();
-    // per start: minimal end by bisection, barrier check, exact cost RN(H[e] - H[i]);
+    // per start: minimal end by bisection on S, barrier check, exact cost RN(H[e] - H[i]);
     // argmin over (cost bits, start) (R3, R4)
-    const uint64_t Stot = w.S[nb];
+    const uint64_t Stot = S[nb];
     uint64_t bestc = ~0ull;
     int besti = 0x7fffffff;
     for (int i = threadIdx.x; i < nb; i += kThreads) {
-      if (w.ist[i] == COOP_PINNED) continue;
-      const uint64_t target = w.S[i] + need;
+      if (St[i] == COOP_PINNED) continue;
+      const uint64_t target = S[i] + need;
       if (target > Stot) continue;
       int lo = i + 1, hi = nb;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (w.S[mid] >= target) hi = mid;
+        if (S[mid] >= target) hi = mid;
         else lo = mid + 1;
       }
       const int e = lo;
-      if (w.B[e] != w.B[i]) continue;
-      const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(u192_sub(w.H[e], w.H[i])));
-      if (cb < bestc || (cb == bestc && i < besti)) {
-        bestc = cb;
+      if (Bc[e] != Bc[i]) continue;
+      const uint64_t cb2 = (uint64_t)__double_as_longlong(u192_round_to_double(u192_sub(w.H[e], w.H[i])));
+      if (cb2 < bestc || (cb2 == bestc && i < besti)) {
+        bestc = cb2;
         besti = i;
       }
     }
@@ -501,11 +562,11 @@ struct Cell {
     // window end of the winner; evict its tensors in ascending address order (R10)
     int last;
     {
-      const uint64_t target = w.S[first] + need;
+      const uint64_t target = S[first] + need;
       int lo = first + 1, hi = nb;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (w.S[mid] >= target) hi = mid;
+        if (S[mid] >= target) hi = mid;
         else lo = mid + 1;
       }
       last = lo - 1;
@@ -516,7 +577,7 @@ struct Cell {
         const int o = O()[b];
         if (o == kFree) continue;
         const uint64_t ad = A()[b];
-        w.tflags[o] &= (uint8_t)~TF_RES;
+        sh.tfl[o] &= (uint8_t)~TF_RES;
         sh.res.evictions++;
         log_ev(3, sh.cur_op, o, ad);
         d = splitmix64(d ^ (((uint64_t)(uint32_t)sh.cur_op << 32) | (uint32_t)o));  // R29
@@ -530,7 +591,6 @@ struct Cell {
     int lo = first, hi = last;
     if (lo > 0 && O()[lo - 1] == kFree) --lo;
     if (hi + 1 < nb && O()[hi + 1] == kFree) ++hi;
-    // (window FREE items were already counted in bytes_free; only tensors were added)
     const uint64_t na = A()[lo], nz = A()[hi] + Z()[hi] - A()[lo];
     const int32_t no = kFree;
     splice(lo, hi, 1, &na, &nz, &no);
@@ -548,8 +608,8 @@ struct Cell {
       if (threadIdx.x == 0) {
         O()[b] = t;
         w.taddr[t] = ad;
-        w.tflags[src] &= (uint8_t)~TF_RES;
-        w.tflags[t] |= TF_RES;
+        sh.tfl[src] &= (uint8_t)~TF_RES;
+        sh.tfl[t] |= TF_RES;
         sh.res.inplace_reuse++;
         log_ev(2, op, t, ad);
       }
@@ -588,7 +648,7 @@ struct Cell {
     }
     if (threadIdx.x == 0) {
       w.taddr[t] = at;
-      w.tflags[t] |= TF_RES;
+      sh.tfl[t] |= TF_RES;
       log_ev(kind, op, t, at);
     }
     __syncthreads();
@@ -633,7 +693,7 @@ struct Cell {
       if (sh.st_stage[f] == 1) {
         int j = sh.st_idx[f];
         const int n = nin(op);
-        while (j < n && (w.tflags[in_at(op, j)] & TF_RES)) ++j;
+        while (j < n && (sh.tfl[in_at(op, j)] & TF_RES)) ++j;
         __syncthreads();
         if (threadIdx.x == 0) {
           if (j < n) {
@@ -664,7 +724,7 @@ struct Cell {
         sh.res.total_us += tr.cost[op];
         sh.res.remat++;
         log_ev(7, op, t, w.taddr[t]);
-        if (w.tflags[t] & TF_DEAD) {
+        if (sh.tfl[t] & TF_DEAD) {
           if (sh.ntrans < 4 * tr.T) w.trans[sh.ntrans++] = t;
           else sh.status = COOP_ERR_NOMEM;
         }
@@ -686,7 +746,7 @@ struct Cell {
   __device__ void run(uint64_t budget) {
     const int T = tr.T, M = tr.M;
     for (int t = threadIdx.x; t < T; t += kThreads) {
-      w.tflags[t] = 0;
+      sh.tfl[t] = 0;
       w.pins[t] = 0;
       w.last_access[t] = 0;
       w.taddr[t] = 0;
@@ -728,7 +788,7 @@ struct Cell {
         else lb += tr.size[t];
         if (threadIdx.x == 0) {
           w.taddr[t] = at;
-          w.tflags[t] = TF_RES | TF_BORN;
+          sh.tfl[t] = TF_RES | TF_BORN;
           log_ev(0, -1, t, at);
         }
         __syncthreads();
@@ -742,17 +802,17 @@ struct Cell {
       }
       for (int j = threadIdx.x; j < n; j += kThreads) atomicAdd(&w.pins[in_at(k, j)], 1);
       for (int j = tr.lock_ptr[k] + threadIdx.x; j < tr.lock_ptr[k + 1]; j += kThreads)
-        w.tflags[tr.lock_idx[j]] |= TF_LOCK;  // R36
+        sh.tfl[tr.lock_idx[j]] |= TF_LOCK;  // R36
       __syncthreads();
       for (int j = 0; j < n && ok(); ++j) {
         const int u = in_at(k, j);
-        const bool res = w.tflags[u] & TF_RES;
+        const bool res = sh.tfl[u] & TF_RES;
         __syncthreads();
         if (!res) materialize(u);
       }
       for (int j = tr.lock_ptr[k]; j < tr.lock_ptr[k + 1] && ok(); ++j) {
         const int u = tr.lock_idx[j];
-        const bool res = w.tflags[u] & TF_RES;
+        const bool res = sh.tfl[u] & TF_RES;
         __syncthreads();
         if (!res) materialize(u);
       }
@@ -760,7 +820,7 @@ struct Cell {
       allocate(k, o, true, 1);
       if (!ok()) break;
       if (threadIdx.x == 0) {
-        w.tflags[o] |= TF_BORN;
+        sh.tfl[o] |= TF_BORN;
         sh.clock += tr.cost[k];
         sh.res.base_us += tr.cost[k];
         sh.res.total_us += tr.cost[k];
@@ -777,7 +837,7 @@ struct Cell {
       __syncthreads();
       // deaths after op k (R20) merged with transient dead recomputes (R22), ascending id
       if (threadIdx.x == 0) {
-        for (int j = tr.die_ptr[k]; j < tr.die_ptr[k + 1]; ++j) w.tflags[tr.die_idx[j]] |= TF_DEAD;
+        for (int j = tr.die_ptr[k]; j < tr.die_ptr[k + 1]; ++j) sh.tfl[tr.die_idx[j]] |= TF_DEAD;
         // insertion-sort the transient list (small) and merge with the (sorted) die list
         int *tl = w.trans;
         const int nt = sh.ntrans;
@@ -801,7 +861,7 @@ struct Cell {
           else t = w.trans[pt++];
           if (t == last) continue;
           last = t;
-          const uint8_t f = w.tflags[t];
+          const uint8_t f = sh.tfl[t];
           const bool keep = tr.unevict[t] && t != src;
           __syncthreads();
           if ((f & TF_DEAD) && (f & TF_RES) && !keep) free_tensor(t);
@@ -1119,6 +1179,7 @@ extern "C" int coop_replay_trace(coop_trace_t t, const uint64_t *budgets, int32_
   for (int i = 0; i < n_budgets; ++i)
     if (budgets[i] < 1) return COOP_ERR_INVALID_ARG;
   if (!is_device_ptr(out) || (log && !is_device_ptr(log))) return COOP_ERR_INVALID_ARG;
+  if (t->T > kMaxT) return COOP_ERR_NOMEM;  // per-tensor flags / pins live in shared memory
   const int up = upload_trace(t);
   if (up != COOP_OK) return up;
   cudaStream_t st = (cudaStream_t)stream;

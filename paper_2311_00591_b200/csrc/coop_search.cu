@@ -264,29 +264,16 @@ __device__ __forceinline__ void filter_starts(const PoolView &v, int k0, uint32_
     if (nb < e) continue;  // a PINNED item inside [i, e-1]
     const int nz = mz ? i + __ffs(mz) - 1 : nz_right;
     const int len = e - i;
-    double C, err;
-    bool exact;
-    if (nz >= e) {  // only h = 0 items: exact cost 0
-      C = 0.0;
-      err = 0.0;
-      exact = true;
-    } else if (len <= 2) {  // one IEEE add is correctly rounded
-      const double h0 = fabs(v.v_at(i));
-      C = (len == 1) ? h0 : __dadd_rn(h0, fabs(v.v_at(i + 1)));
-      err = 0.0;
-      exact = true;
-    } else if (len <= 8) {  // direct sum of nonnegative terms: relative error < 7u
-      double acc = 0.0;
-      for (int k = i; k < e; ++k) acc = __dadd_rn(acc, fabs(v.v_at(k)));
-      C = acc;
-      err = 0x1p-50 * acc;
-      exact = false;
-    } else {  // prefix difference: error bounded by the prefix magnitudes
-      const double He = v.H_at(e), Hi = __dadd_rn(H_car, hpre[q]);
-      C = He - Hi;
-      err = v.gerr * (He + Hi);
-      exact = false;
-    }
+    // exact cost for zero-cost windows (only h = 0 items) and windows of <= 2 items (one
+    // IEEE add is correctly rounded); otherwise the fp64 prefix difference with its bound
+    const bool zero = nz >= e;
+    const bool exact = zero || len <= 2;
+    const double h0 = fabs(v.v_at(i));
+    const double h1 = len >= 2 ? fabs(v.v_at(i + 1)) : 0.0;
+    const double He = v.H_at(e), Hi = __dadd_rn(H_car, hpre[q]);
+    const double Cx = zero ? 0.0 : __dadd_rn(h0, h1);
+    const double C = exact ? Cx : He - Hi;
+    const double err = exact ? 0.0 : v.gerr * (He + Hi);
     const double Lb = C - err;
     if (MODE == 0) {
       if (exact) {
@@ -311,6 +298,56 @@ __device__ __forceinline__ void filter_starts(const PoolView &v, int k0, uint32_
       const int slot = atomicAdd(&sc.ncand, 1);
       if (slot < kCandCap) sc.cand[slot] = ((uint32_t)i << 16) | (uint32_t)(e - i);  // n <= 8192
     }
+  }
+}
+
+// Phase A of one thread: decode its K items (pairs via 16-byte conflict-free loads of the
+// swizzled stage), validate (R7; integer tests on the binary64 encodings, same semantics as
+// the oracle's comparisons), h = c/s (R1), local exclusive prefixes of span and h, and the
+// h slot written back in place (FREE -> -0.0, PINNED -> NaN).  FULL: no item past n.
+template <int K, bool FULL>
+__device__ __forceinline__ void phase_a(const PoolView &v, int k0, int n, bool &bad,
+                                        uint32_t &barmask, uint32_t &nzmask, uint64_t (&spre)[K],
+                                        double (&hpre)[K], uint64_t &sacc, double &hacc) {
+#pragma unroll
+  for (int q = 0; q < K; q += 2) {
+    const int k = k0 + q;
+    const uint32_t o = swz((uint32_t)k);
+    ulonglong2 vs = make_ulonglong2(0, 0);
+    double2 vc = make_double2(0.0, 0.0), vt = make_double2(1.0, 1.0);
+    if (FULL || k < n) {
+      vs = sm<ulonglong2>(v.sr, o);
+      vc = sm<double2>(v.hr, o);
+      vt = sm<double2>(v.vr, o);
+    }
+    double hs[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const bool live = FULL || (k + r < n);
+      const uint64_t sv = live ? (r ? vs.y : vs.x) : 0ull;  // padding: FREE, size 0
+      const uint32_t state = (uint32_t)(sv >> 62);
+      const bool ev = (state == COOP_EVICTABLE);
+      const uint64_t size = live ? (sv & kSizeMask) : 0ull;
+      const double cr = r ? vc.y : vc.x, sr_ = r ? vt.y : vt.x;
+      const double c = ev ? cr : 1.0, st = ev ? sr_ : 1.0;  // 1/1: no slow division path
+      const double h = ev ? __ddiv_rn(c, st) : 0.0;  // h(t) = c(t)/s(t), PAPER.md:150 (R1)
+      const uint64_t cb = (uint64_t)__double_as_longlong(c), sb = (uint64_t)__double_as_longlong(st);
+      const uint64_t hb = (uint64_t)__double_as_longlong(h) & 0x7fffffffffffffffull;
+      const bool c_ok = (cb < 0x7ff0000000000000ull) | (cb == 0x8000000000000000ull);   // finite, >= 0
+      const bool s_ok = (sb - 0x3ff0000000000000ull) < 0x4000000000000000ull;          // finite, >= 1
+      const bool h_ok = (hb == 0) | ((hb - 0x3bf0000000000000ull) < 0x07c0000000000000ull);  // 0 or [2^-64, 2^60)
+      if (live)
+        bad |= ((size - 1ull) >= (kSizeLimit - 1ull)) | (state == 3u) | (ev & !(c_ok & s_ok & h_ok));
+      nzmask |= (uint32_t)(hb != 0) << (q + r);
+      barmask |= (uint32_t)(live & (state == COOP_PINNED)) << (q + r);
+      spre[q + r] = sacc;
+      hpre[q + r] = hacc;
+      sacc += size;
+      hacc = __dadd_rn(hacc, h);
+      // FREE: h = 0, sign = not an eviction; PINNED: NaN (never summed)
+      hs[r] = (state == COOP_FREE) ? -0.0 : (state == COOP_PINNED ? __longlong_as_double(0x7ff8000000000000ll) : fabs(h));
+    }
+    if (FULL || k < n) sm<double2>(v.vr, o) = make_double2(hs[0], hs[1]);
   }
 }
 
@@ -345,13 +382,13 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
   }
 
-  int it = 0;
+  int it = 0, s = 0;
+  uint32_t phase = 0;
   for (int64_t p = blockIdx.x; p < a.n_pools; p += gridDim.x, ++it) {
-    const int s = it % a.stages;
     smem_t *stage = base_ptr + (size_t)s * a.stage_bytes;
     const uint64_t Rraw = a.req[p];
     if (a.use_tma) {
-      mbar_wait(smem_u32(&sc.mbar[s]), (uint32_t)((it / a.stages) & 1));
+      mbar_wait(smem_u32(&sc.mbar[s]), phase);
     } else {
       stage_plain(a, stage, p);
       __syncthreads();
@@ -378,47 +415,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
       double hpre[K];
       uint64_t sacc = 0;
       double hacc = 0.0;
-#pragma unroll
-      for (int q = 0; q < K; q += 2) {
-        const int k = k0 + q;
-        uint64_t sv[2] = {0, 0};
-        double cv[2] = {0.0, 0.0}, tv[2] = {1.0, 1.0};
-        const uint32_t o = swz((uint32_t)k);
-        if (k < n) {
-          const ulonglong2 vs = sm<ulonglong2>(v.sr, o);
-          const double2 vc = sm<double2>(v.hr, o);
-          const double2 vt = sm<double2>(v.vr, o);
-          sv[0] = vs.x; sv[1] = vs.y; cv[0] = vc.x; cv[1] = vc.y; tv[0] = vt.x; tv[1] = vt.y;
-        }
-        double hs[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int kk = k + r;
-          uint64_t size = 0;
-          double h = 0.0, hslot = 0.0;
-          if (kk < n) {
-            const uint32_t state = (uint32_t)(sv[r] >> 62);
-            const bool ev = (state == COOP_EVICTABLE);
-            size = sv[r] & kSizeMask;
-            const double c = ev ? cv[r] : 1.0, st = ev ? tv[r] : 1.0;  // 1/1: no slow path
-            h = ev ? __ddiv_rn(c, st) : 0.0;  // h(t) = c(t)/s(t), IEEE RN (R1)
-            bad |= (size == 0) | (size >= kSizeLimit) | (state > 2u) |
-                   (ev & (!(c >= 0.0 && c <= 1.7976931348623157e308) |
-                          !(st >= 1.0 && st <= 1.7976931348623157e308) |
-                          ((h != 0.0) & ((h < 0x1p-64) | (h >= 0x1p60)))));
-            nzmask |= (uint32_t)(h != 0.0) << (q + r);
-            barmask |= (uint32_t)(state == COOP_PINNED) << (q + r);
-            // FREE: h = 0, sign = not an eviction; PINNED: NaN (never summed)
-            hslot = (state == COOP_FREE) ? -0.0 : (state == COOP_PINNED ? __longlong_as_double(0x7ff8000000000000ll) : h);
-          }
-          spre[q + r] = sacc;
-          hpre[q + r] = hacc;
-          sacc += size;
-          hacc = __dadd_rn(hacc, h);
-          hs[r] = hslot;
-        }
-        if (k < n) sm<double2>(v.vr, o) = make_double2(hs[0], hs[1]);
-      }
+      if (k0 + K <= n)  // warp-uniform except in the last warp
+        phase_a<K, true>(v, k0, n, bad, barmask, nzmask, spre, hpre, sacc, hacc);
+      else
+        phase_a<K, false>(v, k0, n, bad, barmask, nzmask, spre, hpre, sacc, hacc);
 
       // ---------------- block scan: S (u64), H^ (fp64), next PINNED / next nonzero-h ------
       uint64_t sinc = sacc;
@@ -515,6 +515,48 @@ __global__ void __launch_bounds__(MAXT, MINB)
       if (bad_any || a.dbg == 2) {
         if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_ERR_INVALID_ARG);
       } else {
+        // ---------------- phase B0: zero-cost windows -------------------------------------
+        // A run of consecutive h = 0 items (FREE, or EVICTABLE with c = 0) is a zero-cost
+        // window iff its span covers R; the lowest such run head is the answer (exact cost
+        // 0 is the global minimum, R4).  Each thread checks the run heads of its chunk.
+        int zi = kInfIdx, ze = -1, znev = 0;
+        {
+          const int cnt = n - k0;
+          const uint32_t valid = cnt >= K ? (K == 32 ? ~0u : ((1u << K) - 1u)) : (cnt > 0 ? (1u << cnt) - 1u : 0u);
+          const uint32_t zm = valid & ~barmask & ~nzmask;
+          const uint32_t heads = zm & ~(zm << 1);
+          int zstop = n;
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            if (zi != kInfIdx || !((heads >> q) & 1u)) continue;
+            const uint32_t mb = barmask >> q, mz = nzmask >> q;
+            const int nb = mb ? k0 + q + __ffs(mb) - 1 : nb_right;
+            const int nz = mz ? k0 + q + __ffs(mz) - 1 : nz_right;
+            const int stop = min(min(nb, nz), n);
+            if (v.S_at(stop) - (S_car + spre[q]) >= v.R) {
+              zi = k0 + q;
+              zstop = stop;
+            }
+          }
+          if (zi != kInfIdx) {
+            const uint64_t target = v.S_at(zi) + v.R;
+            int lo = zi + 1, hi = zstop;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (v.S_at(mid) >= target) hi = mid;
+              else lo = mid + 1;
+            }
+            ze = lo;
+            for (int k = zi; k < ze; ++k) znev += (__double_as_longlong(v.v_at(k)) >= 0);
+          }
+        }
+        const int zw = warp_allreduce(zi, [](int x, int y) { return min(x, y); });
+        if (lane == 0) sc.wZ[warp] = zw;
+        __syncthreads();
+        const int zmin = warp_allreduce(lane < W ? sc.wZ[lane] : kInfIdx, [](int x, int y) { return min(x, y); });
+        if (zmin != kInfIdx) {
+          if (zi == zmin) write_result(a.out + p, zi, ze - 1, v.S_at(ze) - v.S_at(zi), 0.0, znev, COOP_OK);
+        } else {
         // ---------------- phase B: window ends (merge path), then the fp64 filter ----------
         v.merge_path(tid, T);
         __syncthreads();
@@ -678,6 +720,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
             write_result(a.out + p, bfirst, bend - 1, v.S_at(bend) - v.S_at(bfirst),
                          __longlong_as_double((long long)best), bnev, COOP_OK);
         }
+        }
       }
     }
   pool_done:
@@ -687,6 +730,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
       if (pn < a.n_pools)
         issue_stage(a, &m_ss, &m_c, &m_s, base + (uint32_t)s * a.stage_bytes,
                     smem_u32(&sc.mbar[s]), pn);
+    }
+    if (++s == a.stages) {  // next stage of the ring; parity flips on wrap-around
+      s = 0;
+      phase ^= 1u;
     }
   }
 }

@@ -246,6 +246,10 @@ def test_degenerate_cases():
     ]
     for ss, c, s, R in bad:
         assert int(O.search(ss, c, s, R)["status"]) == O.INVALID_ARG
+    # c = -0.0 is a valid (zero) cost; the window cost is +0.0 and the item an eviction
+    w = O.search(G.pack([4], [G.EVICTABLE]), [-0.0], [3.0], 4)
+    assert (int(w["status"]), int(w["n_evict"])) == (O.OK, 1)
+    assert math.copysign(1.0, float(w["cost"])) == 1.0 and float(w["cost"]) == 0.0
     # FREE / PINNED items ignore c and s
     w = O.search(G.pack([3, 3], [G.FREE, G.PINNED]), [float("nan"), -5.0], [0.0, 0.0], 3)
     assert (int(w["status"]), int(w["first"])) == (O.OK, 0)
@@ -278,3 +282,5 @@ def test_fsum_matches_math_fsum():
         if rng.random() < 0.3:  # exact midpoints and heavy cancellation between magnitudes
             x = np.concatenate([x, [2.0 ** 60, 1.0, 2.0 ** -53 * 2.0 ** 60]])
         assert O.fsum(x) == math.fsum(x)
+    for x in ([-0.0], [-0.0, -0.0], [0.0, -0.0], []):  # signed zeros: +0.0, bitwise
+        assert math.copysign(1.0, O.fsum(x)) == math.copysign(1.0, math.fsum(x)) == 1.0

@@ -215,3 +215,23 @@ def test_config4_full_size_sampled():
         hs, hc, hst, hr = G.bench_pools_host(G.MODE_BENCH, 0, int(p), 1, n)
         o = O.search_many(hs, hc, hst, hr, 1, n, n)
         assert_same(g[p:p + 1], o, f"pool {p}")
+
+
+def test_signed_zero_and_zero_runs():
+    """c = -0.0 EVICTABLE items (valid, h = 0, counted as evictions), multi-item zero runs
+    crossing thread chunks, and +0.0 window costs."""
+    rng = np.random.default_rng(4)
+    pools, reqs = [], []
+    n = 600
+    for p in range(64):
+        ss, c, s = G.random_pool(rng, n, p_free=0.2, p_pinned=0.02, max_size=50,
+                                 h_choices=[0.0, 0.0, 1.0, 2.0], coalesced=False)
+        c = np.where((rng.random(n) < 0.3) & (c == 0.0), -0.0, c)
+        pools.append((ss, c, s))
+        reqs.append(int(rng.integers(1, 400)))
+    SS, C, S = G.stack_pools(pools, 608)
+    req = np.array(reqs, np.uint64)
+    g = gpu_search(SS, C, S, req, 64, n, 608)
+    o = O.search_many(SS, C, S, req, 64, n, 608)
+    assert_same(g, o, "signed zero")
+    assert (g["cost"][g["status"] == 0] == 0.0).sum() > 10
