@@ -325,27 +325,39 @@ __device__ __forceinline__ void phase_a(const PoolView &v, int k0, int n, bool &
     for (int r = 0; r < 2; ++r) {
       const bool live = FULL || (k + r < n);
       const uint64_t sv = live ? (r ? vs.y : vs.x) : 0ull;  // padding: FREE, size 0
-      const uint32_t state = (uint32_t)(sv >> 62);
+      const uint32_t svh = (uint32_t)(sv >> 32);
+      const uint32_t state = svh >> 30;
       const bool ev = (state == COOP_EVICTABLE);
-      const uint64_t size = live ? (sv & kSizeMask) : 0ull;
+      const uint64_t size = sv & kSizeMask;
       const double cr = r ? vc.y : vc.x, sr_ = r ? vt.y : vt.x;
       const double c = ev ? cr : 1.0, st = ev ? sr_ : 1.0;  // 1/1: no slow division path
-      const double h = ev ? __ddiv_rn(c, st) : 0.0;  // h(t) = c(t)/s(t), PAPER.md:150 (R1)
-      const uint64_t cb = (uint64_t)__double_as_longlong(c), sb = (uint64_t)__double_as_longlong(st);
-      const uint64_t hb = (uint64_t)__double_as_longlong(h) & 0x7fffffffffffffffull;
-      const bool c_ok = (cb < 0x7ff0000000000000ull) | (cb == 0x8000000000000000ull);   // finite, >= 0
-      const bool s_ok = (sb - 0x3ff0000000000000ull) < 0x4000000000000000ull;          // finite, >= 1
-      const bool h_ok = (hb == 0) | ((hb - 0x3bf0000000000000ull) < 0x07c0000000000000ull);  // 0 or [2^-64, 2^60)
-      if (live)
-        bad |= ((size - 1ull) >= (kSizeLimit - 1ull)) | (state == 3u) | (ev & !(c_ok & s_ok & h_ok));
-      nzmask |= (uint32_t)(hb != 0) << (q + r);
+      const double hq = __ddiv_rn(c, st);                    // h(t) = c(t)/s(t), PAPER.md:150 (R1)
+      // validation (R7) on the high words: the bounds are powers of two, so these are the
+      // exact value ranges of the oracle's comparisons
+      const uint32_t ch = (uint32_t)((uint64_t)__double_as_longlong(c) >> 32);
+      const uint32_t cl = (uint32_t)__double_as_longlong(c);
+      const uint32_t sh_ = (uint32_t)((uint64_t)__double_as_longlong(st) >> 32);
+      const uint32_t hh = (uint32_t)((uint64_t)__double_as_longlong(hq) >> 32) & 0x7fffffffu;
+      const uint32_t hl = (uint32_t)__double_as_longlong(hq);
+      const bool hzero = (hh | hl) == 0u;
+      const bool c_ok = (ch < 0x7ff00000u) | ((ch == 0x80000000u) & (cl == 0u));  // finite, >= 0 (or -0)
+      const bool s_ok = (sh_ - 0x3ff00000u) < 0x40000000u;                       // finite, >= 1
+      const bool h_ok = hzero | ((hh - 0x3bf00000u) < 0x07c00000u);               // 0 or [2^-64, 2^60)
+      const bool size_bad = ((svh & 0x3fff0000u) != 0u) | (size == 0ull);       // size in [1, 2^48)
+      if (live) bad |= size_bad | (state == 3u) | (ev & !(c_ok & s_ok & h_ok));
+      const double h = ev ? hq : 0.0;
+      const bool nzh = ev & !hzero;
+      nzmask |= (uint32_t)nzh << (q + r);
       barmask |= (uint32_t)(live & (state == COOP_PINNED)) << (q + r);
       spre[q + r] = sacc;
       hpre[q + r] = hacc;
-      sacc += size;
+      sacc += live ? size : 0ull;
       hacc = __dadd_rn(hacc, h);
-      // FREE: h = 0, sign = not an eviction; PINNED: NaN (never summed)
-      hs[r] = (state == COOP_FREE) ? -0.0 : (state == COOP_PINNED ? __longlong_as_double(0x7ff8000000000000ll) : fabs(h));
+      // slot: EVICTABLE |h| (sign cleared), FREE -0.0 (h = 0, "not an eviction",
+      // PAPER.md:147), PINNED NaN (never summed)
+      const uint32_t oh = ev ? hh : (state == COOP_PINNED ? 0x7ff80000u : 0x80000000u);
+      const uint32_t ol = ev ? hl : 0u;
+      hs[r] = __hiloint2double((int)oh, (int)ol);
     }
     if (FULL || k < n) sm<double2>(v.vr, o) = make_double2(hs[0], hs[1]);
   }
