@@ -59,7 +59,7 @@ struct TraceDev {
 };
 
 struct WsLayout {  // byte offsets inside one cell's workspace
-  size_t tflags, pins, last_access, taddr, epochs, marks, isz, ih, ist, S, H, B, trans, victims;
+  size_t tflags, pins, last_access, taddr, epochs, marks, isz, ih, ist, S, H, B, trans, victims, memoA, memoD;
   size_t bytes;
 };
 
@@ -76,6 +76,7 @@ struct CellPtrs {
   U192 *H;
   int32_t *B;
   int32_t *trans, *victims;
+  uint64_t *memoA, *memoD;
 };
 
 struct KArgs {
@@ -118,6 +119,7 @@ struct Shared {
   int32_t red32[2][kWarps];
   U192 red192[kWarps];
   int32_t redpar;
+  uint32_t pev;  // pressure-event epoch of the projected-cost memo
 };
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -200,6 +202,8 @@ struct Cell {
     w.B = (int32_t *)(base + a.lay.B);
     w.trans = (int32_t *)(base + a.lay.trans);
     w.victims = (int32_t *)(base + a.lay.victims);
+    w.memoA = (uint64_t *)(base + a.lay.memoA);
+    w.memoD = (uint64_t *)(base + a.lay.memoD);
     log = a.log ? a.log + (size_t)cell * a.log_cap : nullptr;
   }
 
@@ -339,24 +343,38 @@ struct Cell {
   // c(t) = producer cost + the SET of non-resident ancestors reachable through
   // non-resident tensors + the SET of evicted descendants reachable through evicted
   // tensors (R18).  One thread; visited marks = per-thread epochs.
-  __device__ int64_t projected_cost(int t, bool &overflow) {
-    const int op = __ldg(&tr.producer[t]);
-    int64_t c = __ldg(&tr.cost[op]);
-    // quick path: no non-resident input and no evicted consumer output -> c = own cost
-    bool simple = true;
-    for (int j = __ldg(&tr.in_ptr[op]); j < __ldg(&tr.in_ptr[op + 1]) && simple; ++j) {
-      const int u = __ldg(&tr.in_idx[j]);
-      if (!(sh.tfl[u] & TF_RES) && __ldg(&tr.producer[u]) >= 0) simple = false;
-    }
-    for (int j = __ldg(&tr.cons_ptr[t]); j < __ldg(&tr.cons_ptr[t + 1]) && simple; ++j) {
-      const uint8_t f = sh.tfl[__ldg(&tr.out[__ldg(&tr.cons_idx[j])])];
-      if ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD)) simple = false;
-    }
-    if (simple) return c;
-    // Only non-resident tensors contribute and expand, so only they need the visited set
-    // (a resident tensor reached twice is skipped twice).  The set lives in this thread's
-    // shared-memory slots (open addressing, key = tensor + 1); on overflow the closure is
-    // redone with the per-thread global marks.
+  // ---------------- projected cost c(t) (R18) --------------------
+  // c(t) = cost(producer(t)) + cost of Anc(t) + cost of Desc(t) where
+  //   Anc(t)  = the SET of non-resident tensors reachable upward from t's inputs through
+  //             non-resident tensors (parameters stop),
+  //   Desc(t) = the SET of evicted live tensors reachable downward from t's consumers'
+  //             outputs through evicted live tensors.
+  // Within one pressure event residency is fixed, so the closures of single-entry chains
+  // are memoized: Up*(u) = {u} U Up*(v) when v is u's only non-resident input (disjoint in
+  // a DAG), likewise Down*; nodes with two or more entries get an exact set-closure DFS.
+  // Memo words: (event epoch << 40) | value (values >= 2^40 are not memoized).
+  __device__ __forceinline__ bool up_ok(int u) const {  // non-resident, recomputable
+    return !(sh.tfl[u] & TF_RES) && __ldg(&tr.producer[u]) >= 0;
+  }
+  __device__ __forceinline__ bool down_ok(int d) const {  // evicted and live
+    const uint8_t f = sh.tfl[d];
+    return (f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD);
+  }
+  __device__ __forceinline__ bool memo_get(const uint64_t *m, int x, int64_t &v) const {
+    const uint64_t w_ = ((volatile const uint64_t *)m)[x];
+    if ((uint32_t)(w_ >> 40) != sh.pev) return false;
+    v = (int64_t)(w_ & ((1ull << 40) - 1ull));
+    return true;
+  }
+  __device__ __forceinline__ void memo_put(uint64_t *m, int x, int64_t v) const {
+    if (v >= 0 && v < (1ll << 40)) ((volatile uint64_t *)m)[x] = ((uint64_t)sh.pev << 40) | (uint64_t)v;
+  }
+
+  // exact set closure by DFS: UP = ancestors through up_ok, else descendants through
+  // down_ok; roots = x itself (NEIGH false) or x's inputs / consumer outputs (NEIGH true);
+  // returns the summed producer costs of the set
+  template <bool UP, bool NEIGH>
+  __device__ int64_t closure_dfs(int x0, bool &overflow) {
     uint32_t *vs = sh.vis[threadIdx.x];
     for (int k = 0; k < kVisCap; ++k) vs[k] = 0u;
     int nvis = 0;
@@ -384,46 +402,128 @@ struct Cell {
       if (attempt == 1) {
         use_marks = true;
         ep = ++epoch;
-        c = __ldg(&tr.cost[op]);
       }
+      int64_t c = 0;
       bool full = false;
       int stk[kDfsCap];
       int sp = 0;
-      for (int j = __ldg(&tr.in_ptr[op]); j < __ldg(&tr.in_ptr[op + 1]); ++j) {
-        if (sp == kDfsCap) { overflow = true; return c; }
-        stk[sp++] = __ldg(&tr.in_idx[j]);
-      }
-      while (sp > 0 && !full) {
-        const int u = stk[--sp];
-        if ((sh.tfl[u] & TF_RES) || __ldg(&tr.producer[u]) < 0) continue;
-        if (!use_marks && nvis >= kVisCap / 2) { full = true; break; }
-        if (seen(u)) continue;
-        const int pu = __ldg(&tr.producer[u]);
-        c += __ldg(&tr.cost[pu]);
-        for (int j = __ldg(&tr.in_ptr[pu]); j < __ldg(&tr.in_ptr[pu + 1]); ++j) {
+      if (!NEIGH) {
+        stk[sp++] = x0;
+      } else if (UP) {
+        const int p0 = __ldg(&tr.producer[x0]);
+        for (int j = __ldg(&tr.in_ptr[p0]); j < __ldg(&tr.in_ptr[p0 + 1]); ++j) {
           if (sp == kDfsCap) { overflow = true; return c; }
           stk[sp++] = __ldg(&tr.in_idx[j]);
         }
-      }
-      if (full) continue;
-      for (int j = __ldg(&tr.cons_ptr[t]); j < __ldg(&tr.cons_ptr[t + 1]); ++j) {
-        if (sp == kDfsCap) { overflow = true; return c; }
-        stk[sp++] = __ldg(&tr.out[__ldg(&tr.cons_idx[j])]);
-      }
-      while (sp > 0 && !full) {
-        const int d = stk[--sp];
-        const uint8_t f = sh.tfl[d];
-        if (!(f & TF_BORN) || (f & TF_RES) || (f & TF_DEAD)) continue;
-        if (!use_marks && nvis >= kVisCap / 2) { full = true; break; }
-        if (seen(d)) continue;
-        c += __ldg(&tr.cost[__ldg(&tr.producer[d])]);
-        for (int j = __ldg(&tr.cons_ptr[d]); j < __ldg(&tr.cons_ptr[d + 1]); ++j) {
+      } else {
+        for (int j = __ldg(&tr.cons_ptr[x0]); j < __ldg(&tr.cons_ptr[x0 + 1]); ++j) {
           if (sp == kDfsCap) { overflow = true; return c; }
           stk[sp++] = __ldg(&tr.out[__ldg(&tr.cons_idx[j])]);
         }
       }
+      while (sp > 0) {
+        const int x = stk[--sp];
+        if (UP ? !up_ok(x) : !down_ok(x)) continue;
+        if (!use_marks && nvis >= kVisCap / 2) { full = true; break; }
+        if (seen(x)) continue;
+        const int px = __ldg(&tr.producer[x]);
+        c += __ldg(&tr.cost[px]);
+        if (UP) {
+          for (int j = __ldg(&tr.in_ptr[px]); j < __ldg(&tr.in_ptr[px + 1]); ++j) {
+            if (sp == kDfsCap) { overflow = true; return c; }
+            stk[sp++] = __ldg(&tr.in_idx[j]);
+          }
+        } else {
+          for (int j = __ldg(&tr.cons_ptr[x]); j < __ldg(&tr.cons_ptr[x + 1]); ++j) {
+            if (sp == kDfsCap) { overflow = true; return c; }
+            stk[sp++] = __ldg(&tr.out[__ldg(&tr.cons_idx[j])]);
+          }
+        }
+      }
       if (!full) return c;
     }
+    return 0;
+  }
+
+  // entries of x: its non-resident inputs (UP) or its evicted live consumer outputs (down)
+  template <bool UP>
+  __device__ __forceinline__ int entries(int x, int *buf, int cap) const {
+    int k = 0;
+    if (UP) {
+      const int px = __ldg(&tr.producer[x]);
+      for (int j = __ldg(&tr.in_ptr[px]); j < __ldg(&tr.in_ptr[px + 1]); ++j) {
+        const int u = __ldg(&tr.in_idx[j]);
+        if (up_ok(u)) {
+          bool dup = false;
+          for (int q = 0; q < min(k, cap); ++q) dup |= (buf[q] == u);
+          if (!dup) {
+            if (k < cap) buf[k] = u;
+            ++k;
+          }
+        }
+      }
+    } else {
+      for (int j = __ldg(&tr.cons_ptr[x]); j < __ldg(&tr.cons_ptr[x + 1]); ++j) {
+        const int d = __ldg(&tr.out[__ldg(&tr.cons_idx[j])]);
+        if (down_ok(d)) {
+          bool dup = false;
+          for (int q = 0; q < min(k, cap); ++q) dup |= (buf[q] == d);
+          if (!dup) {
+            if (k < cap) buf[k] = d;
+            ++k;
+          }
+        }
+      }
+    }
+    return k;
+  }
+
+  // cost of the closure of node x (x itself included; x satisfies up_ok / down_ok)
+  template <bool UP>
+  __device__ int64_t node_closure(int x0, bool &overflow) {
+    uint64_t *memo = UP ? w.memoA : w.memoD;
+    int chain[64];
+    int nch = 0;
+    int x = x0;
+    int64_t base = 0;
+    while (true) {
+      int64_t mv;
+      if (memo_get(memo, x, mv)) {
+        base = mv;
+        break;
+      }
+      int buf[4];
+      const int k = entries<UP>(x, buf, 4);
+      if (k == 1 && nch < 64) {  // single entry: Up*(x) = {x} U Up*(entry)
+        chain[nch++] = x;
+        x = buf[0];
+        continue;
+      }
+      if (k == 0) {
+        base = __ldg(&tr.cost[__ldg(&tr.producer[x])]);
+      } else {
+        base = closure_dfs<UP, false>(x, overflow);  // two or more entries: exact set closure
+      }
+      memo_put(memo, x, base);
+      break;
+    }
+    while (nch > 0) {
+      const int y = chain[--nch];
+      base += __ldg(&tr.cost[__ldg(&tr.producer[y])]);
+      memo_put(memo, y, base);
+    }
+    return base;
+  }
+
+  __device__ int64_t projected_cost(int t, bool &overflow) {
+    int64_t c = __ldg(&tr.cost[__ldg(&tr.producer[t])]);
+    int buf[4];
+    const int ka = entries<true>(t, buf, 4);
+    if (ka == 1) c += node_closure<true>(buf[0], overflow);
+    else if (ka > 1) c += closure_dfs<true, true>(t, overflow);
+    const int kd = entries<false>(t, buf, 4);
+    if (kd == 1) c += node_closure<false>(buf[0], overflow);
+    else if (kd > 1) c += closure_dfs<false, true>(t, overflow);
     return c;
   }
 
@@ -434,6 +534,13 @@ struct Cell {
   // item states in its owner[]; the exact 192-bit prefix H and h live in global memory.
   __device__ bool evict_window(uint64_t need) {
     const uint64_t t0 = gtimer();
+    if (threadIdx.x == 0) {
+      if (++sh.pev >= (1u << 24)) {  // epoch wrap: clear the memo (never in practice)
+        sh.pev = 1;
+        for (int t = 0; t < tr.T; ++t) w.memoA[t] = w.memoD[t] = 0ull;
+      }
+    }
+    __syncthreads();
     const int nb = sh.nb, nx = sh.cur ^ 1;
     uint64_t *S = sh.addr[nx];
     int32_t *Bc = reinterpret_cast<int32_t *>(sh.size[nx]);
@@ -746,6 +853,8 @@ struct Cell {
   __device__ void run(uint64_t budget) {
     const int T = tr.T, M = tr.M;
     for (int t = threadIdx.x; t < T; t += kThreads) {
+      w.memoA[t] = 0ull;
+      w.memoD[t] = 0ull;
       sh.tfl[t] = 0;
       w.pins[t] = 0;
       w.last_access[t] = 0;
@@ -762,6 +871,7 @@ struct Cell {
       sh.status = COOP_OK;
       sh.cur_op = -1;
       sh.redpar = 0;
+      sh.pev = 0;
       memset(&sh.res, 0, sizeof(sh.res));
       sh.res.fail_op = -1;
       sh.res.digest = 0x9E3779B97F4A7C15ull;
@@ -1050,6 +1160,8 @@ WsLayout make_layout(int T) {
   L.B = take((size_t)(kCap + 1 + kThreads) * 4);
   L.trans = take((size_t)T * 4 * 4);
   L.victims = take((size_t)kCap * 4);
+  L.memoA = take((size_t)T * 8);
+  L.memoD = take((size_t)T * 8);
   L.bytes = o;
   return L;
 }
