@@ -38,6 +38,11 @@ ALGO_BYTES_PER_POOL = 24 * N_BLOCKS + 8 + 32  # size_state+cost+stale, request, 
 SEED = 0
 METRIC = "window-search queries/s"
 UNIT = "queries/s"
+ARM_CONFIG = {"workload": "config4: batched window search, 2^20 pools x 4096 blocks per GPU "
+                          "(BASELINE.json configs[3])",
+              "pools_per_gpu": POOLS_PER_GPU, "n_blocks": N_BLOCKS, "seed": SEED,
+              "l2": "no flush: 96 GiB of inputs per step per GPU >> 126 MB L2",
+              "generator": "gen/coop_gen.cu MODE_BENCH (counter-based)"}
 
 
 def parse():
@@ -161,7 +166,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    per_worker = 4
+    per_worker = 16  # ~60 ms of oracle work per worker per step (bounded sample)
     ctx = mp.get_context("fork")
     times = []
     total = 0
@@ -181,9 +186,8 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config4-sample: batched window search, 4096-block pools "
-                                   "(bounded sample per step)",
-                       "pools_per_step": cores * per_worker, "n_blocks": N_BLOCKS},
+            "config": dict(ARM_CONFIG, sample=f"bounded sample per step: {cores * per_worker} "
+                                                   f"pools of the same workload (global pools from 0)"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{cores * per_worker} pools per step, one process per core"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -427,12 +431,8 @@ def main():
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "config4: batched window search, 2^20 pools x 4096 "
-                                       "blocks per GPU (BASELINE.json configs[3])",
-                           "pools_per_gpu": P, "n_blocks": N_BLOCKS, "seed": SEED,
-                           "parallelism": f"dp{world} (pool shards, weak scaling)",
-                           "l2": "no flush: 96 GiB of inputs per step per GPU >> 126 MB L2",
-                           "generator": "gen/coop_gen.cu MODE_BENCH (counter-based, on device)"},
+                "config": dict(ARM_CONFIG, pools_per_gpu=P,
+                               parallelism=f"dp{world} (pool shards, weak scaling)"),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": args.steps, "clocks": clk, "replay": replay,
                 "results": {"status_counts": stat, "xor_digest": f"{digest:016x}"}}

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcoop.so")
+LIB_PATH = os.environ.get("COOP_LIB_OVERRIDE") or os.path.join(_HERE, "libcoop.so")  # override: A/B kernel builds
 
 OK = 0
 INFEASIBLE = 1

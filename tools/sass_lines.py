@@ -15,6 +15,7 @@ base = int(data[0][idx["Address"]], 16)
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
 line_of = {}
+fns = set()
 for cub in os.listdir(tmp):
     out = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
     cur_fn, cur_line, cur_file = None, None, None
@@ -25,12 +26,17 @@ for cub in os.listdir(tmp):
         m = re.search(r"\.text\.([A-Za-z0-9_]+)", ln)
         if m and ("section" in ln):
             cur_fn = m.group(1)
+            if ksub in cur_fn:
+                fns.add(cur_fn)
         m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
         if m:
             cur_file, cur_line = os.path.basename(m.group(1)), int(m.group(2))
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if m and cur_fn and ksub in cur_fn:
             line_of[int(m.group(1), 16)] = (cur_file, cur_line)
+if len(fns) > 1:
+    sys.exit("kernel substring matches several functions (pass e.g. search_kernelILi8ELi512ELi1E):\n  "
+             + "\n  ".join(sorted(fns)))
 agg_e = collections.Counter(); agg_s = collections.Counter()
 tot_e = tot_s = 0
 for r in data:
