@@ -127,6 +127,43 @@ int orc_replay(const orc_trace *tr, const orc_cfg *cfg, orc_replay_result *res,
 /* Peak of resident bytes in an unbounded, eviction-free replay (R25). */
 uint64_t orc_peak_live(const orc_trace *tr, uint32_t flags);
 
+/* ======================================================================= O3: online calls
+ * One pool [0, budget) driven call by call (R38-R44): orc_pool_alloc creates
+ * tensor ids 0, 1, 2, ... (one op per tensor, the parents are its inputs) through Alg. 1;
+ * free / access / remat follow.  TEST INFRASTRUCTURE ONLY. */
+#define ORC_NEEDS_REMAT 1
+#define ORC_UNKNOWN_ID (-2)
+#define ORC_NOMEM (-6)
+#define ORC_BAD_STATE (-7)
+
+#define ORC_OP_EXPENSIVE 1u   /* class C1 */
+#define ORC_OP_CHEAP 2u       /* class C2 */
+#define ORC_OP_INPLACE 4u     /* mutates inplace_src */
+#define ORC_OP_UNEVICTABLE 8u
+#define ORC_OP_PHASE_FWD 16u
+
+typedef struct {
+  int64_t tensor_id;
+  uint64_t addr, size;
+  int32_t n_evicted, window_first, window_last, reserved;
+  uint64_t window_span;
+  double window_cost;
+} orc_alloc_result;
+
+typedef struct orc_pool_s orc_pool;
+orc_pool *orc_pool_create(uint64_t budget, uint32_t flags, uint32_t class_threshold,
+                          int32_t max_tensors, int32_t max_edges);
+void orc_pool_destroy(orc_pool *p);
+int orc_pool_alloc(orc_pool *p, uint64_t size, uint64_t cost_us, uint32_t op_flags,
+                   int32_t inplace_src, const int32_t *parents, int32_t n_parents,
+                   orc_alloc_result *out, int32_t *evicted, int32_t evicted_cap);
+int orc_pool_free(orc_pool *p, int32_t t);
+int orc_pool_access(orc_pool *p, int32_t t, uint64_t advance_us);
+int orc_pool_remat(orc_pool *p, int32_t t, orc_alloc_result *out, int32_t *evicted,
+                   int32_t evicted_cap);
+int orc_pool_stats(orc_pool *p, orc_replay_result *out);
+int32_t orc_pool_layout(orc_pool *p, uint64_t *addr, uint64_t *size, int32_t *owner, int32_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -151,3 +151,88 @@ def peak_live(tr, flags: int = F_PARTITION | F_INPLACE) -> int:
     L = _replay_lib()
     st, keep = _trace_struct(tr)
     return int(L.orc_peak_live(ctypes.byref(st), int(flags)))
+
+
+# ----------------------------------------------------------------------------- O3 online
+NEEDS_REMAT, UNKNOWN_ID, NOMEM, BAD_STATE = 1, -2, -6, -7
+OP_EXPENSIVE, OP_CHEAP, OP_INPLACE, OP_UNEVICTABLE, OP_PHASE_FWD = 1, 2, 4, 8, 16
+ORC_ALLOC = np.dtype([("tensor_id", "<i8"), ("addr", "<u8"), ("size", "<u8"),
+                      ("n_evicted", "<i4"), ("window_first", "<i4"), ("window_last", "<i4"),
+                      ("reserved", "<i4"), ("window_span", "<u8"), ("window_cost", "<f8")])
+
+
+def _pool_lib():
+    L = lib()
+    if not getattr(L, "_pool_ready", False):
+        vp, i32, u32, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64
+        L.orc_pool_create.argtypes = [u64, u32, u32, i32, i32]
+        L.orc_pool_create.restype = vp
+        L.orc_pool_destroy.argtypes = [vp]
+        L.orc_pool_destroy.restype = None
+        L.orc_pool_alloc.argtypes = [vp, u64, u64, u32, i32, vp, i32, vp, vp, i32]
+        L.orc_pool_free.argtypes = [vp, i32]
+        L.orc_pool_access.argtypes = [vp, i32, u64]
+        L.orc_pool_remat.argtypes = [vp, i32, vp, vp, i32]
+        L.orc_pool_stats.argtypes = [vp, vp]
+        L.orc_pool_layout.argtypes = [vp, vp, vp, vp, i32]
+        for f in ("orc_pool_alloc", "orc_pool_free", "orc_pool_access", "orc_pool_remat",
+                  "orc_pool_stats", "orc_pool_layout"):
+            getattr(L, f).restype = ctypes.c_int
+        L._pool_ready = True
+    return L
+
+
+class Pool:
+    """O3: the online single-pool calls (alloc / free / access / remat), plain C."""
+
+    def __init__(self, budget: int, flags: int = F_PARTITION | F_INPLACE, class_threshold: int = 15,
+                 max_tensors: int = 4096, max_edges: int = 16384):
+        self._L = _pool_lib()
+        self._p = self._L.orc_pool_create(int(budget), int(flags), int(class_threshold),
+                                          int(max_tensors), int(max_edges))
+        if not self._p:
+            raise ValueError("orc_pool_create: bad arguments")
+
+    def __del__(self):
+        if getattr(self, "_p", None):
+            self._L.orc_pool_destroy(self._p)
+            self._p = None
+
+    def _res(self, st, out, ev, cap):
+        o = out[0]
+        n = min(int(o["n_evicted"]), cap) if st == OK else 0
+        return st, o, [int(x) for x in ev[:n]]
+
+    def alloc(self, size, cost_us, op_flags=0, inplace_src=-1, parents=(), evicted_cap=8192):
+        par = np.ascontiguousarray(list(parents) or [0], np.int32)
+        out = np.zeros(1, ORC_ALLOC)
+        ev = np.zeros(max(evicted_cap, 1), np.int32)
+        st = self._L.orc_pool_alloc(self._p, int(size), int(cost_us), int(op_flags), int(inplace_src),
+                                    par.ctypes.data, len(parents), out.ctypes.data, ev.ctypes.data,
+                                    int(evicted_cap))
+        return self._res(st, out, ev, evicted_cap)
+
+    def free(self, t):
+        return self._L.orc_pool_free(self._p, int(t))
+
+    def access(self, t, advance_us=0):
+        return self._L.orc_pool_access(self._p, int(t), int(advance_us))
+
+    def remat(self, t, evicted_cap=8192):
+        out = np.zeros(1, ORC_ALLOC)
+        ev = np.zeros(max(evicted_cap, 1), np.int32)
+        st = self._L.orc_pool_remat(self._p, int(t), out.ctypes.data, ev.ctypes.data, int(evicted_cap))
+        return self._res(st, out, ev, evicted_cap)
+
+    def stats(self):
+        res = np.zeros(1, ORC_RESULT)
+        self._L.orc_pool_stats(self._p, res.ctypes.data)
+        return res[0]
+
+    def layout(self, cap=8192):
+        a = np.zeros(cap, np.uint64)
+        z = np.zeros(cap, np.uint64)
+        o = np.zeros(cap, np.int32)
+        n = self._L.orc_pool_layout(self._p, a.ctypes.data, z.ctypes.data, o.ctypes.data, cap)
+        n = min(n, cap)
+        return a[:n].copy(), z[:n].copy(), o[:n].copy()

@@ -51,6 +51,12 @@ typedef struct {
   orc_event *log;
   int64_t log_cap;
   int status;
+  /* O3 (online calls) only */
+  const uint8_t *cls;       /* per op: 0 = class by threshold, 1 = C1, 2 = C2; NULL = all 0 */
+  int32_t win_first, win_last, nvict;
+  uint64_t win_span;
+  double win_cost;
+  int32_t *victims;         /* the last window's tensors, ascending address; NULL = off */
 } R;
 
 static uint64_t splitmix64(uint64_t x) {
@@ -157,6 +163,7 @@ static int32_t in_at(const orc_trace *tr, int op, int k) { return tr->in_idx[tr-
 
 /* C1 ("expensive", super-linear) iff cost density >= threshold us/MiB (R14, Table 1) */
 static int is_c1(R *r, int op) {
+  if (r->cls && r->cls[op]) return r->cls[op] == 1; /* O3: class given by the caller */
   uint64_t bytes = r->tr->size[r->tr->out[op]];
   return (uint64_t)r->tr->cost_us[op] * 1048576ull >= (uint64_t)r->cfg.class_threshold * bytes;
 }
@@ -256,6 +263,13 @@ static int evict_window(R *r, uint64_t size) {
   int nv = 0;
   for (int i = w.first; i <= w.last; ++i)
     if (r->b[i].owner != NO_OWNER) victims[nv++] = r->b[i].owner;
+  r->win_first = w.first;
+  r->win_last = w.last;
+  r->win_span = w.span;
+  r->win_cost = w.cost;
+  r->nvict = nv;
+  if (r->victims)
+    for (int k = 0; k < nv; ++k) r->victims[k] = victims[k];
   for (int k = 0; k < nv; ++k) evict(r, victims[k]);
   return 0;
 }
@@ -604,4 +618,274 @@ int orc_replay(const orc_trace *tr, const orc_cfg *cfg_in, orc_replay_result *re
   free(r.pins); free(r.last_access); free(r.addr); free(r.mark); free(r.stack);
   free(r.cons_ptr); free(r.cons_idx); free(r.lock_ptr); free(r.lock_idx); free(r.locked); free(r.b); free(r.v_ss); free(r.v_c); free(r.v_s);
   return r.status;
+}
+
+/* ======================================================================= O3: online calls
+ * One pool [0, budget) driven call by call (the framework side of Alg. 1): every
+ * orc_pool_alloc is one op producing one new tensor (op id = tensor id), its parents are
+ * the op's inputs.  The same Alg. 1 / Sec. 3.3-3.5 steps as O2 (allocate, evict_window,
+ * projected_cost, place, release); readings R38-R44 of DESIGN.md.  Plain arrays with a
+ * fixed capacity; the consumer lists are rebuilt from scratch on every call. */
+struct orc_pool_s {
+  R r;
+  orc_trace tr;
+  orc_replay_result res;
+  int32_t T, nnz, max_tensors, max_edges;
+  uint64_t *size;
+  uint8_t *is_param, *phase, *cls;
+  int32_t *producer, *out, *src, *in_ptr, *in_idx;
+  int64_t *cost;
+};
+
+orc_pool *orc_pool_create(uint64_t budget, uint32_t flags, uint32_t class_threshold,
+                          int32_t max_tensors, int32_t max_edges) {
+  if (budget < 1 || (flags & ~7u) || max_tensors < 1 || max_edges < 0) return NULL;
+  orc_pool *p = (orc_pool *)calloc(1, sizeof(orc_pool));
+  int T = max_tensors, E = max_edges;
+  p->max_tensors = T;
+  p->max_edges = E;
+  p->size = (uint64_t *)calloc((size_t)T, sizeof(uint64_t));
+  p->is_param = (uint8_t *)calloc((size_t)T, 1);
+  p->phase = (uint8_t *)calloc((size_t)T, 1);
+  p->cls = (uint8_t *)calloc((size_t)T, 1);
+  p->producer = (int32_t *)calloc((size_t)T, sizeof(int32_t));
+  p->out = (int32_t *)calloc((size_t)T, sizeof(int32_t));
+  p->src = (int32_t *)calloc((size_t)T, sizeof(int32_t));
+  p->in_ptr = (int32_t *)calloc((size_t)T + 1, sizeof(int32_t));
+  p->in_idx = (int32_t *)calloc((size_t)E + 1, sizeof(int32_t));
+  p->cost = (int64_t *)calloc((size_t)T, sizeof(int64_t));
+  p->tr.size = p->size;
+  p->tr.is_param = p->is_param;
+  p->tr.producer = p->producer;
+  p->tr.cost_us = p->cost;
+  p->tr.out = p->out;
+  p->tr.inplace_src = p->src;
+  p->tr.phase = p->phase;
+  p->tr.in_ptr = p->in_ptr;
+  p->tr.in_idx = p->in_idx;
+  R *r = &p->r;
+  r->tr = &p->tr;
+  r->cfg.budget = budget;
+  r->cfg.flags = flags;
+  r->cfg.class_threshold = class_threshold ? class_threshold : 15;
+  r->cfg.max_depth = 512;
+  r->cls = p->cls;
+  r->res = &p->res;
+  r->born = (uint8_t *)calloc((size_t)T, 1);
+  r->resident = (uint8_t *)calloc((size_t)T, 1);
+  r->dead = (uint8_t *)calloc((size_t)T, 1);
+  r->unevict = (uint8_t *)calloc((size_t)T, 1);
+  r->locked = (uint8_t *)calloc((size_t)T, 1);
+  r->pins = (int32_t *)calloc((size_t)T, sizeof(int32_t));
+  r->last_access = (int64_t *)calloc((size_t)T, sizeof(int64_t));
+  r->addr = (uint64_t *)calloc((size_t)T, sizeof(uint64_t));
+  r->mark = (uint32_t *)calloc((size_t)T, sizeof(uint32_t));
+  r->stack = (int32_t *)malloc(sizeof(int32_t) * ((size_t)E + (size_t)T + 16) * 2);
+  r->cons_ptr = (int32_t *)calloc((size_t)T + 1, sizeof(int32_t));
+  r->cons_idx = (int32_t *)calloc((size_t)E + 1, sizeof(int32_t));
+  r->victims = (int32_t *)calloc(8192, sizeof(int32_t));
+  r->cap = 64;
+  r->b = (blk *)malloc(sizeof(blk) * (size_t)r->cap);
+  r->v_ss = (uint64_t *)malloc(sizeof(uint64_t) * 8192);
+  r->v_c = (double *)malloc(sizeof(double) * 8192);
+  r->v_s = (double *)malloc(sizeof(double) * 8192);
+  /* the pool: one free block [0, budget) */
+  r->b[0].addr = 0;
+  r->b[0].size = budget;
+  r->b[0].owner = NO_OWNER;
+  r->nb = 1;
+  r->bytes_free = budget;
+  p->res.fail_op = -1;
+  p->res.digest = 0x9E3779B97F4A7C15ull;
+  p->res.budget = budget;
+  p->res.max_blocks = 1;
+  r->status = ORC_OK;
+  r->cur_op = -1;
+  return p;
+}
+
+void orc_pool_destroy(orc_pool *p) {
+  if (!p) return;
+  R *r = &p->r;
+  free(r->born); free(r->resident); free(r->dead); free(r->unevict); free(r->locked);
+  free(r->pins); free(r->last_access); free(r->addr); free(r->mark); free(r->stack);
+  free(r->cons_ptr); free(r->cons_idx); free(r->victims); free(r->b);
+  free(r->v_ss); free(r->v_c); free(r->v_s);
+  free(p->size); free(p->is_param); free(p->phase); free(p->cls); free(p->producer);
+  free(p->out); free(p->src); free(p->in_ptr); free(p->in_idx); free(p->cost);
+  free(p);
+}
+
+/* consumers CSR over ops [0, n): rebuilt from scratch (plain) */
+static void o3_consumers(orc_pool *p, int n) {
+  R *r = &p->r;
+  for (int t = 0; t <= p->max_tensors; ++t) r->cons_ptr[t] = 0;
+  for (int j = 0; j < p->in_ptr[n]; ++j) r->cons_ptr[p->in_idx[j] + 1]++;
+  for (int t = 0; t < p->max_tensors; ++t) r->cons_ptr[t + 1] += r->cons_ptr[t];
+  int32_t *fill = (int32_t *)calloc((size_t)p->max_tensors, sizeof(int32_t));
+  for (int k = 0; k < n; ++k)
+    for (int j = p->in_ptr[k]; j < p->in_ptr[k + 1]; ++j) {
+      int u = p->in_idx[j];
+      r->cons_idx[r->cons_ptr[u] + fill[u]++] = k;
+    }
+  free(fill);
+}
+
+static void o3_fill(orc_pool *p, int32_t t, orc_alloc_result *out, int32_t *evicted, int32_t cap) {
+  R *r = &p->r;
+  if (!out) return;
+  out->tensor_id = t;
+  out->addr = r->addr[t];
+  out->size = p->size[t];
+  out->n_evicted = r->nvict;
+  out->window_first = r->win_first;
+  out->window_last = r->win_last;
+  out->reserved = 0;
+  out->window_span = r->nvict || r->win_first >= 0 ? r->win_span : 0;
+  out->window_cost = r->win_first >= 0 ? r->win_cost : 0.0;
+  for (int k = 0; k < r->nvict && k < cap; ++k) evicted[k] = r->victims[k];
+}
+
+/* Alg. 1 for one new tensor (R38-R41): validation, parents resident, allocate (in-place
+ * when the op mutates a parent and recomputable in-place is on), then the op runs */
+int orc_pool_alloc(orc_pool *p, uint64_t size, uint64_t cost_us, uint32_t op_flags,
+                   int32_t inplace_src, const int32_t *parents, int32_t n_parents,
+                   orc_alloc_result *out, int32_t *evicted, int32_t evicted_cap) {
+  R *r = &p->r;
+  if (size < 1 || size >= (1ull << 48) || cost_us >= (1ull << 40)) return ORC_INVALID_ARG;
+  if ((op_flags & ~31u) || ((op_flags & ORC_OP_EXPENSIVE) && (op_flags & ORC_OP_CHEAP)))
+    return ORC_INVALID_ARG;
+  if (n_parents < 0 || (n_parents > 0 && !parents) || evicted_cap < 0) return ORC_INVALID_ARG;
+  for (int j = 0; j < n_parents; ++j)
+    if (parents[j] < 0 || parents[j] >= p->T) return ORC_UNKNOWN_ID;
+  if (op_flags & ORC_OP_INPLACE) {
+    int seen = 0;
+    for (int j = 0; j < n_parents; ++j) seen |= (parents[j] == inplace_src);
+    if (!seen || p->size[inplace_src] != size) return ORC_INVALID_ARG;
+  } else if (inplace_src != -1) {
+    return ORC_INVALID_ARG;
+  }
+  if (p->T >= p->max_tensors || p->nnz + n_parents > p->max_edges) return ORC_NOMEM;
+  for (int j = 0; j < n_parents; ++j)
+    if (!r->resident[parents[j]]) {
+      if (out) out->tensor_id = parents[j];
+      return ORC_NEEDS_REMAT;
+    }
+  int32_t t = p->T;
+  p->size[t] = size;
+  p->producer[t] = t;
+  p->out[t] = t;
+  p->cost[t] = (int64_t)cost_us;
+  p->src[t] = (op_flags & ORC_OP_INPLACE) ? inplace_src : -1;
+  p->phase[t] = (op_flags & ORC_OP_PHASE_FWD) ? ORC_PHASE_FWD : ORC_PHASE_BWD;
+  p->cls[t] = (op_flags & ORC_OP_EXPENSIVE) ? 1 : (op_flags & ORC_OP_CHEAP) ? 2 : 0;
+  for (int j = 0; j < n_parents; ++j) p->in_idx[p->nnz + j] = parents[j];
+  p->in_ptr[t + 1] = p->nnz + n_parents;
+  r->unevict[t] = (op_flags & ORC_OP_UNEVICTABLE) || (p->src[t] >= 0 && r->unevict[p->src[t]]);
+  p->tr.n_tensors = p->tr.n_ops = t + 1;
+  o3_consumers(p, t);
+  r->cur_op = t;
+  r->win_first = r->win_last = -1;
+  r->nvict = 0;
+  r->win_span = 0;
+  for (int j = 0; j < n_parents; ++j) r->pins[parents[j]]++; /* the op's inputs (R16) */
+  int rc = allocate(r, t, t, 1, ORC_EV_ALLOC);
+  for (int j = 0; j < n_parents; ++j) r->pins[parents[j]]--;
+  if (rc != 0) {
+    int st = r->status == ORC_OK ? ORC_UNSATISFIABLE : r->status;
+    r->status = ORC_OK; /* the pool stays usable; the tensor is not created */
+    p->tr.n_tensors = p->tr.n_ops = t;
+    r->unevict[t] = 0;
+    return st;
+  }
+  r->born[t] = 1;
+  r->clock += (int64_t)cost_us;
+  p->res.base_us += (int64_t)cost_us;
+  p->res.total_us += (int64_t)cost_us;
+  log_ev(r, ORC_EV_EXEC, t, t, r->addr[t]);
+  for (int j = 0; j < n_parents; ++j) r->last_access[parents[j]] = r->clock;
+  r->last_access[t] = r->clock;
+  p->nnz += n_parents;
+  p->T = t + 1;
+  o3_fill(p, t, out, evicted, evicted_cap);
+  return ORC_OK;
+}
+
+/* the caller frees a tensor (R42): a resident block is released and coalesced */
+int orc_pool_free(orc_pool *p, int32_t t) {
+  R *r = &p->r;
+  if (t < 0 || t >= p->T) return ORC_UNKNOWN_ID;
+  if (r->dead[t] && !r->resident[t]) return ORC_BAD_STATE;
+  r->cur_op = t;
+  if (r->resident[t]) free_tensor(r, t);
+  r->dead[t] = 1;
+  return ORC_OK;
+}
+
+/* the caller reads a tensor (R43): the clock advances; staleness restarts if resident */
+int orc_pool_access(orc_pool *p, int32_t t, uint64_t advance_us) {
+  R *r = &p->r;
+  if (t < 0 || t >= p->T) return ORC_UNKNOWN_ID;
+  if (advance_us >= (1ull << 40)) return ORC_INVALID_ARG;
+  if (r->dead[t] && !r->resident[t]) return ORC_BAD_STATE;
+  r->clock += (int64_t)advance_us;
+  if (!r->resident[t]) return ORC_NEEDS_REMAT;
+  r->last_access[t] = r->clock;
+  return ORC_OK;
+}
+
+/* re-allocate an evicted (or freed) tensor whose parents are resident (R44): Alg. 1
+ * out-of-place (R21), then its producer runs again */
+int orc_pool_remat(orc_pool *p, int32_t t, orc_alloc_result *out, int32_t *evicted,
+                   int32_t evicted_cap) {
+  R *r = &p->r;
+  if (t < 0 || t >= p->T) return ORC_UNKNOWN_ID;
+  if (evicted_cap < 0) return ORC_INVALID_ARG;
+  r->win_first = r->win_last = -1;
+  r->nvict = 0;
+  r->win_span = 0;
+  if (r->resident[t]) {
+    o3_fill(p, t, out, evicted, evicted_cap);
+    return ORC_OK;
+  }
+  for (int j = p->in_ptr[t]; j < p->in_ptr[t + 1]; ++j)
+    if (!r->resident[p->in_idx[j]]) {
+      if (out) out->tensor_id = p->in_idx[j];
+      return ORC_NEEDS_REMAT;
+    }
+  o3_consumers(p, p->T);
+  r->cur_op = t;
+  for (int j = p->in_ptr[t]; j < p->in_ptr[t + 1]; ++j) r->pins[p->in_idx[j]]++;
+  int rc = allocate(r, t, t, 0, ORC_EV_REMAT);
+  for (int j = p->in_ptr[t]; j < p->in_ptr[t + 1]; ++j) r->pins[p->in_idx[j]]--;
+  if (rc != 0) {
+    int st = r->status == ORC_OK ? ORC_UNSATISFIABLE : r->status;
+    r->status = ORC_OK;
+    return st;
+  }
+  r->clock += p->cost[t];
+  p->res.total_us += p->cost[t];
+  p->res.remat++;
+  log_ev(r, ORC_EV_REXEC, t, t, r->addr[t]);
+  for (int j = p->in_ptr[t]; j < p->in_ptr[t + 1]; ++j) r->last_access[p->in_idx[j]] = r->clock;
+  r->last_access[t] = r->clock;
+  o3_fill(p, t, out, evicted, evicted_cap);
+  return ORC_OK;
+}
+
+int orc_pool_stats(orc_pool *p, orc_replay_result *out) {
+  *out = p->res;
+  out->status = ORC_OK;
+  return ORC_OK;
+}
+
+/* the block table, address order: owner -1 = free */
+int32_t orc_pool_layout(orc_pool *p, uint64_t *addr, uint64_t *size, int32_t *owner, int32_t cap) {
+  R *r = &p->r;
+  for (int i = 0; i < r->nb && i < cap; ++i) {
+    addr[i] = r->b[i].addr;
+    size[i] = r->b[i].size;
+    owner[i] = r->b[i].owner;
+  }
+  return r->nb;
 }
