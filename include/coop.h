@@ -17,7 +17,7 @@
  * mutable global state except a per-device cache of kernel attributes.
  *
  * Paper references are PAPER.md:<line> (Sec./Eq./Alg.) of /root/reference/PAPER.md;
- * DESIGN.md "Readings" R1..R35 state every choice the paper leaves open.
+ * DESIGN.md "Readings" R1..R44 state every choice the paper leaves open.
  */
 #ifndef COOP_H
 #define COOP_H
@@ -204,6 +204,110 @@ int coop_replay_trace(coop_trace_t trace, const uint64_t *budgets, int32_t n_bud
                       uint32_t flags, uint32_t class_threshold, int32_t max_depth,
                       coop_replay_result *out, coop_event *log, int64_t log_cap_per_budget,
                       coop_stream_t stream);
+
+
+/* ------------------------------------------------------------------ online single pool
+ * One memory pool [0, budget) driven call by call by a framework -- the user-facing side of
+ * Alg. 1 Allocate(op, size) with the sliding-window eviction of Sec. 3.3
+ * (PAPER.md:141-153), cheap tensor partitioning (Sec. 3.4) and
+ * recomputable in-place (Sec. 3.5).  Readings R38-R44.
+ *
+ * The pool state (block table, tensor graph, residency, clock, counters) is DEVICE-resident;
+ * every call runs one CTA of the same Alg. 1 engine as coop_replay_trace on it, on the
+ * pool's own stream, and is synchronous (results are returned in host memory).  Calls on
+ * one pool must not overlap (one owner per handle).
+ *
+ * Tensors: coop_alloc creates ids 0, 1, 2, ... in call order; each alloc is one op whose
+ * inputs are `parents` (all resident) and whose output is the new tensor (op id = tensor
+ * id).  c(t) = the op's cost plus its evicted neighbourhood (R18); s(t) = clock -
+ * last access (R17); the clock advances by each executed op's cost and by coop_access.
+ * A freed tensor keeps its graph node: it can be recomputed (coop_rematerialize) when an
+ * evicted descendant needs it, and must then be freed again.
+ */
+#define COOP_NEEDS_REMAT 1 /* coop_access / coop_alloc / coop_rematerialize: a tensor (or a
+                              parent) is not resident -- rematerialize it first          */
+
+typedef struct {
+  uint64_t budget;          /* pool bytes, >= 1                                             */
+  uint32_t flags;           /* COOP_F_PARTITION | COOP_F_INPLACE | COOP_F_PARTITION_ALL_PHASES */
+  uint32_t class_threshold; /* us per MiB separating C1 / C2 when no class flag is given;
+                               0 -> 15 (R14)                                              */
+  int32_t max_tensors;      /* id capacity, 1..16384 (device arrays sized once)            */
+  int32_t max_edges;        /* total parent links over all allocs, >= 0                    */
+} coop_pool_config;
+
+typedef struct coop_pool_s *coop_pool_t;
+
+/* op_flags of coop_alloc */
+#define COOP_OP_EXPENSIVE 1u   /* class C1: placed from the left (Sec. 3.4)                  */
+#define COOP_OP_CHEAP 2u       /* class C2: from the right under COOP_F_PARTITION (fwd phase)  */
+#define COOP_OP_INPLACE 4u     /* mutates inplace_src (a parent of the same size, Sec. 3.5)    */
+#define COOP_OP_UNEVICTABLE 8u /* never evicted (parameters, optimizer state: PAPER.md:51)     */
+#define COOP_OP_PHASE_FWD 16u  /* a forward-phase op (partitioning applies, R12)               */
+
+typedef struct {
+  int64_t tensor_id;     /* the tensor allocated (NEEDS_REMAT: the parent to recompute)    */
+  uint64_t addr;         /* byte offset in the pool                                        */
+  uint64_t size;
+  int32_t n_evicted;     /* tensors evicted by this call (ids in evicted_ids)              */
+  int32_t window_first;  /* item indices of the evicted window in the address-ordered     */
+  int32_t window_last;   /*   list before eviction, -1 when no window was needed           */
+  int32_t reserved;
+  uint64_t window_span;  /* bytes of the window                                            */
+  double window_cost;    /* its cost RN(sum h) (R3); 0 when no window                      */
+} coop_alloc_result;     /* 56 bytes */
+
+/* Create a pool with one free block [0, budget) on the current device.  Allocates all
+ * device state once (no allocation in later calls).  COOP_ERR_INVALID_ARG on a bad
+ * config, COOP_ERR_NOMEM / COOP_ERR_CUDA on device failures. */
+int coop_pool_init(const coop_pool_config *cfg, coop_pool_t *out);
+int coop_pool_destroy(coop_pool_t pool);
+
+/*
+ * coop_alloc -- Alg. 1 for a new tensor of `size` bytes produced by an op of cost
+ * `cost_us` reading `parents` (HOST array, n_parents ids, all resident).  With
+ * COOP_OP_INPLACE and COOP_F_INPLACE the output takes inplace_src's block (inplace_src
+ * becomes non-resident, recomputable); otherwise the output is placed by first fit from
+ * its class's end, and on failure the minimum-cost window is evicted (Sec. 3.3) and the
+ * output placed in the coalesced block.  inplace_src must be -1 without COOP_OP_INPLACE.
+ * Returns COOP_OK (out, evicted_ids[0 .. min(n_evicted, evicted_cap)) in ascending
+ * address order), COOP_NEEDS_REMAT (out->tensor_id = the first non-resident parent; no
+ * state change), COOP_ERR_UNSATISFIABLE (no window exists; no tensor is created),
+ * COOP_ERR_INVALID_ARG (size outside [1, 2^48), cost >= 2^40, bad flags, bad in-place
+ * source), COOP_ERR_UNKNOWN_ID (a parent id never allocated), COOP_ERR_NOMEM (capacity,
+ * or a block table beyond 2048 blocks), COOP_ERR_CUDA.
+ */
+int coop_alloc(coop_pool_t pool, uint64_t size, uint64_t cost_us, uint32_t op_flags,
+               int64_t inplace_src, const int64_t *parents, int32_t n_parents,
+               coop_alloc_result *out, int64_t *evicted_ids, int32_t evicted_cap);
+
+/* coop_free -- the framework frees a tensor: a resident block is released and coalesced
+ * with free neighbours.  COOP_ERR_UNKNOWN_ID, or COOP_ERR_BAD_STATE for a
+ * double free (a freed tensor that is not resident). */
+int coop_free(coop_pool_t pool, int64_t tensor_id);
+
+/* coop_access -- the framework reads a tensor after `advance_clock_us` of other work: the
+ * clock advances, and a resident tensor's staleness restarts (R17).  COOP_OK, or
+ * COOP_NEEDS_REMAT when the tensor is not resident (evicted, or its block was taken by an
+ * in-place op); COOP_ERR_BAD_STATE for a freed tensor; COOP_ERR_UNKNOWN_ID;
+ * COOP_ERR_INVALID_ARG for advance >= 2^40. */
+int coop_access(coop_pool_t pool, int64_t tensor_id, uint64_t advance_clock_us);
+
+/* coop_rematerialize -- re-allocate a non-resident tensor through Alg. 1 out of place
+ * (R21); the framework then re-runs its op (its cost is charged to the clock).  Its
+ * parents must be resident: otherwise COOP_NEEDS_REMAT with out->tensor_id = the first
+ * missing parent (rematerialize that first).  A resident tensor: COOP_OK, no change.
+ * Other returns as coop_alloc. */
+int coop_rematerialize(coop_pool_t pool, int64_t tensor_id, coop_alloc_result *out,
+                       int64_t *evicted_ids, int32_t evicted_cap);
+
+/* Counters of the pool so far (the coop_replay_result fields; status = COOP_OK). */
+int coop_pool_stats(coop_pool_t pool, coop_replay_result *out);
+
+/* The block table in address order (SPEC.md debug dump): *n_blocks = count; the first
+ * min(count, cap) blocks are written to the HOST arrays (owner -1 = free). */
+int coop_pool_layout(coop_pool_t pool, uint64_t *addr, uint64_t *size, int64_t *owner,
+                     int32_t cap, int32_t *n_blocks);
 
 #ifdef __cplusplus
 }

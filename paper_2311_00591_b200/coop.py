@@ -237,3 +237,107 @@ class Trace:
         res = out.cpu().numpy().view(REPLAY_RESULT_DTYPE)
         ev = log.cpu().numpy().view(EVENT_DTYPE).reshape(n, log_cap) if log is not None else None
         return res, ev
+
+
+# ----------------------------------------------------------------------------- online pool
+NEEDS_REMAT = 1
+OP_EXPENSIVE, OP_CHEAP, OP_INPLACE, OP_UNEVICTABLE, OP_PHASE_FWD = 1, 2, 4, 8, 16
+
+# struct coop_alloc_result (56 bytes)
+ALLOC_RESULT_DTYPE = np.dtype([("tensor_id", "<i8"), ("addr", "<u8"), ("size", "<u8"),
+                               ("n_evicted", "<i4"), ("window_first", "<i4"),
+                               ("window_last", "<i4"), ("reserved", "<i4"),
+                               ("window_span", "<u8"), ("window_cost", "<f8")])
+assert ALLOC_RESULT_DTYPE.itemsize == 56
+
+
+class PoolConfig(ctypes.Structure):
+    _fields_ = [("budget", ctypes.c_uint64), ("flags", ctypes.c_uint32),
+                ("class_threshold", ctypes.c_uint32), ("max_tensors", ctypes.c_int32),
+                ("max_edges", ctypes.c_int32)]
+
+
+_vp = ctypes.c_void_p
+lib.coop_pool_init.argtypes = [ctypes.POINTER(PoolConfig), ctypes.POINTER(_vp)]
+lib.coop_pool_destroy.argtypes = [_vp]
+lib.coop_alloc.argtypes = [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int64,
+                           _vp, ctypes.c_int32, _vp, _vp, ctypes.c_int32]
+lib.coop_free.argtypes = [_vp, ctypes.c_int64]
+lib.coop_access.argtypes = [_vp, ctypes.c_int64, ctypes.c_uint64]
+lib.coop_rematerialize.argtypes = [_vp, ctypes.c_int64, _vp, _vp, ctypes.c_int32]
+lib.coop_pool_stats.argtypes = [_vp, _vp]
+lib.coop_pool_layout.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
+for _f in ("coop_pool_init", "coop_pool_destroy", "coop_alloc", "coop_free", "coop_access",
+           "coop_rematerialize", "coop_pool_stats", "coop_pool_layout"):
+    getattr(lib, _f).restype = ctypes.c_int
+
+
+class Pool:
+    """One device-resident pool driven call by call (coop_pool_init and friends).  Calls
+    return the library status (errors are returned, not raised, like the C API):
+    alloc / remat -> (status, coop_alloc_result record, evicted ids); free / access ->
+    status."""
+
+    def __init__(self, budget: int, flags: int = F_PARTITION | F_INPLACE, class_threshold: int = 15,
+                 max_tensors: int = 4096, max_edges: int = 16384):
+        cfg = PoolConfig(int(budget), int(flags), int(class_threshold), int(max_tensors), int(max_edges))
+        h = _vp()
+        rc = lib.coop_pool_init(ctypes.byref(cfg), ctypes.byref(h))
+        if rc != OK:
+            raise CoopError(rc, "coop_pool_init")
+        self.handle = h
+        self._ev = np.zeros(8192, np.int64)
+
+    def close(self):
+        if self.handle:
+            lib.coop_pool_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _res(self, st, out, cap):
+        n = min(int(out[0]["n_evicted"]), cap) if st == OK else 0
+        return st, out[0], [int(x) for x in self._ev[:n]]
+
+    def alloc(self, size, cost_us, op_flags=0, inplace_src=-1, parents=(), evicted_cap=8192):
+        par = np.ascontiguousarray(list(parents) or [0], np.int64)
+        out = np.zeros(1, ALLOC_RESULT_DTYPE)
+        cap = min(evicted_cap, len(self._ev))
+        st = lib.coop_alloc(self.handle, int(size), int(cost_us), int(op_flags), int(inplace_src),
+                            par.ctypes.data, len(parents), out.ctypes.data, self._ev.ctypes.data, cap)
+        return self._res(st, out, cap)
+
+    def free(self, t):
+        return lib.coop_free(self.handle, int(t))
+
+    def access(self, t, advance_us=0):
+        return lib.coop_access(self.handle, int(t), int(advance_us))
+
+    def remat(self, t, evicted_cap=8192):
+        out = np.zeros(1, ALLOC_RESULT_DTYPE)
+        cap = min(evicted_cap, len(self._ev))
+        st = lib.coop_rematerialize(self.handle, int(t), out.ctypes.data, self._ev.ctypes.data, cap)
+        return self._res(st, out, cap)
+
+    def stats(self):
+        res = np.zeros(1, REPLAY_RESULT_DTYPE)
+        rc = lib.coop_pool_stats(self.handle, res.ctypes.data)
+        if rc != OK:
+            raise CoopError(rc, "coop_pool_stats")
+        return res[0]
+
+    def layout(self, cap=8192):
+        a = np.zeros(cap, np.uint64)
+        z = np.zeros(cap, np.uint64)
+        o = np.zeros(cap, np.int64)
+        n = ctypes.c_int32()
+        rc = lib.coop_pool_layout(self.handle, a.ctypes.data, z.ctypes.data, o.ctypes.data, cap,
+                                  ctypes.byref(n))
+        if rc != OK:
+            raise CoopError(rc, "coop_pool_layout")
+        k = min(n.value, cap)
+        return a[:k].copy(), z[:k].copy(), o[:k].copy()

@@ -1,0 +1,536 @@
+// coop_pool.cu -- the online single-pool calls of include/coop.h (coop_pool_init, coop_alloc,
+// coop_free, coop_access, coop_rematerialize, coop_pool_stats, coop_pool_layout).
+//
+// The pool is DEVICE-resident: the address-ordered block table, the growing tensor graph
+// (one op per coop_alloc: cost, inputs = parents, output = the new tensor), residency
+// flags, pins, last accesses, the clock and the counters persist in global memory between
+// calls.  Each call is ONE launch of a 256-thread CTA that loads the block table and the
+// tensor flags into shared memory, runs the same Alg. 1 engine as the trace replay
+// (replay_core.cuh: first fit by class side, Sec. 3.3 window search with projected costs
+// and the exact 192-bit scans, eviction, coalescing, in-place transfer) and stores the
+// state back.  Arguments (the parents) and results (status, coop_alloc_result, evicted
+// ids) travel through mapped pinned host memory, so a call is launch + one stream sync.
+// Readings R38-R44; bit-exact with the oracle O3.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <vector>
+
+#include "replay_core.cuh"
+
+namespace coop {
+namespace {
+
+enum : int32_t { PK_ALLOC = 0, PK_FREE = 1, PK_ACCESS = 2, PK_REMAT = 3 };
+
+// persistent pool scalars + block table (global memory)
+struct PoolState {
+  uint64_t addr[kCap + 2], size[kCap + 2];
+  int32_t owner[kCap + 2];
+  int32_t nb, n_tensors, n_edges;
+  uint32_t pev;
+  uint64_t bytes_free;
+  int64_t clock;
+  coop_replay_result res;
+};
+
+// writable view of the graph arrays that TraceDev reads
+struct GraphMut {
+  uint64_t *size;
+  int32_t *producer;
+  uint8_t *unevict;
+  int64_t *cost;
+  int32_t *out, *src;
+  uint8_t *phase, *cls;
+  int32_t *in_ptr, *in_idx;
+  int32_t *cons_head, *cons_next, *cons_op;
+};
+
+// mapped pinned host memory shared by the host and the call's CTA
+struct HostIO {
+  int32_t status, n_victims;
+  int64_t need_parent;
+  coop_alloc_result r;
+};
+
+struct PArgs {
+  KArgs k;
+  GraphMut g;
+  PoolState *ps;
+  int32_t kind, t, src, n_parents;
+  uint64_t size, adv;
+  int64_t cost;
+  uint32_t op_flags;
+  HostIO *io;
+  const int32_t *io_parents;
+  int32_t *io_victims;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Shared &sh = *reinterpret_cast<Shared *>(smem);
+  Cell c(pa.k, sh, 0);
+  PoolState &P = *pa.ps;
+  const GraphMut &g = pa.g;
+  const int tid = threadIdx.x, t = pa.t;
+  const int nb0 = P.nb, nt = P.n_tensors;
+  const int nflag = min(nt + 1, pa.k.tr.T);
+  // ---- load the persistent state into the CTA
+  for (int b = tid; b < nb0; b += kThreads) {
+    sh.addr[0][b] = P.addr[b];
+    sh.size[0][b] = P.size[b];
+    sh.owner[0][b] = P.owner[b];
+  }
+  for (int x = tid; x < nflag; x += kThreads) sh.tfl[x] = c.w.tflags[x];
+  if (tid == 0) {
+    sh.cur = 0;
+    sh.nb = nb0;
+    sh.bytes_free = P.bytes_free;
+    sh.clock = P.clock;
+    sh.status = COOP_OK;
+    sh.cur_op = t;
+    sh.redpar = 0;
+    sh.pev = P.pev;
+    sh.res = P.res;
+    sh.win_first = sh.win_last = -1;
+    sh.nvict = 0;
+    sh.win_span = 0;
+    sh.win_cost = 0;
+  }
+  c.epoch = c.w.epochs[tid];
+  __syncthreads();
+
+  int32_t st = COOP_OK;
+  int64_t need = -1;
+  bool fill = false;
+  if (pa.kind == PK_ALLOC || pa.kind == PK_REMAT) {
+    // the op's inputs: the call's parents (alloc) or the recorded ones (remat)
+    const int np = pa.kind == PK_ALLOC ? pa.n_parents : g.in_ptr[t + 1] - g.in_ptr[t];
+    const int32_t *par = pa.kind == PK_ALLOC ? pa.io_parents : g.in_idx + g.in_ptr[t];
+    bool resident_now = false;
+    if (pa.kind == PK_ALLOC) {
+      if (tid == 0) {  // the new op / tensor t (read below with plain loads only)
+        const int32_t e0 = g.in_ptr[t];
+        for (int j = 0; j < np; ++j) g.in_idx[e0 + j] = par[j];
+        g.in_ptr[t + 1] = e0 + np;
+        g.size[t] = pa.size;
+        g.producer[t] = t;
+        g.out[t] = t;
+        g.cost[t] = pa.cost;
+        g.src[t] = (pa.op_flags & COOP_OP_INPLACE) ? pa.src : -1;
+        g.phase[t] = (pa.op_flags & COOP_OP_PHASE_FWD) ? COOP_PHASE_FWD : COOP_PHASE_BWD;
+        g.cls[t] = (pa.op_flags & COOP_OP_EXPENSIVE) ? 1 : (pa.op_flags & COOP_OP_CHEAP) ? 2 : 0;
+        g.unevict[t] = ((pa.op_flags & COOP_OP_UNEVICTABLE) || (g.src[t] >= 0 && g.unevict[g.src[t]])) ? 1 : 0;
+        sh.tfl[t] = 0;
+        c.w.pins[t] = 0;
+        c.w.last_access[t] = 0;
+      }
+      __syncthreads();
+    } else {
+      resident_now = sh.tfl[t] & TF_RES;
+    }
+    if (resident_now) {
+      fill = true;  // remat of a resident tensor: nothing to do
+    } else {
+      int jbad = 0x7fffffff;
+      for (int j = tid; j < np; j += kThreads)
+        if (!(sh.tfl[par[j]] & TF_RES)) jbad = min(jbad, j);
+      jbad = cta_min_i32(sh, jbad);
+      if (jbad != 0x7fffffff) {
+        st = COOP_NEEDS_REMAT;
+        need = par[jbad];
+      } else {
+        for (int j = tid; j < np; j += kThreads) atomicAdd(&c.w.pins[par[j]], 1);  // R16
+        __syncthreads();
+        if (pa.kind == PK_ALLOC) c.allocate(t, t, true, 1);  // Alg. 1, in-place allowed
+        else c.allocate(t, t, false, 5);                     // out of place (R21)
+        const bool ok = c.ok();
+        if (ok && tid == 0) {
+          const int64_t cost = g.cost[t];
+          sh.clock += cost;
+          sh.res.total_us += cost;
+          if (pa.kind == PK_ALLOC) {
+            sh.tfl[t] |= TF_BORN;
+            sh.res.base_us += cost;
+            c.log_ev(6, t, t, c.w.taddr[t]);
+          } else {
+            sh.res.remat++;
+            c.log_ev(7, t, t, c.w.taddr[t]);
+          }
+        }
+        __syncthreads();
+        const int64_t clk = sh.clock;
+        for (int j = tid; j < np; j += kThreads) {
+          if (ok) c.w.last_access[par[j]] = clk;
+          atomicSub(&c.w.pins[par[j]], 1);
+        }
+        if (ok && tid == 0) c.w.last_access[t] = clk;
+        __syncthreads();
+        if (ok) {
+          fill = true;
+          if (pa.kind == PK_ALLOC && tid == 0) {  // link the op into its parents' consumer lists
+            for (int j = 0; j < np; ++j) {
+              const int e = P.n_edges + j;
+              g.cons_op[e] = t;
+              g.cons_next[e] = g.cons_head[par[j]];
+              g.cons_head[par[j]] = e;
+            }
+            P.n_edges += np;
+            P.n_tensors = t + 1;
+          }
+        } else {
+          st = sh.status == COOP_OK ? COOP_ERR_UNSATISFIABLE : sh.status;
+        }
+      }
+    }
+  } else if (pa.kind == PK_FREE) {
+    const uint8_t f = sh.tfl[t];
+    if ((f & TF_DEAD) && !(f & TF_RES)) {
+      st = COOP_ERR_BAD_STATE;  // double free
+    } else {
+      if (f & TF_RES) c.free_tensor(t);
+      if (tid == 0) sh.tfl[t] |= TF_DEAD;
+    }
+  } else {  // PK_ACCESS
+    const uint8_t f = sh.tfl[t];
+    if ((f & TF_DEAD) && !(f & TF_RES)) {
+      st = COOP_ERR_BAD_STATE;
+    } else {
+      if (tid == 0) {
+        sh.clock += (int64_t)pa.adv;
+        if (f & TF_RES) c.w.last_access[t] = sh.clock;  // staleness restarts (R17)
+      }
+      st = (f & TF_RES) ? COOP_OK : COOP_NEEDS_REMAT;
+    }
+  }
+  __syncthreads();
+
+  // ---- results to the host
+  const int nv = sh.nvict;
+  if (fill)
+    for (int k = tid; k < nv; k += kThreads) pa.io_victims[k] = c.w.victims[k];
+  if (tid == 0) {
+    HostIO &io = *pa.io;
+    io.status = st;
+    io.n_victims = fill ? nv : 0;
+    io.need_parent = need;
+    if (fill) {
+      coop_alloc_result r;
+      r.tensor_id = t;
+      r.addr = c.w.taddr[t];
+      r.size = g.size[t];
+      r.n_evicted = nv;
+      r.window_first = sh.win_first;
+      r.window_last = sh.win_last;
+      r.reserved = 0;
+      r.window_span = sh.win_first >= 0 ? sh.win_span : 0;
+      r.window_cost = sh.win_first >= 0 ? __longlong_as_double((long long)sh.win_cost) : 0.0;
+      io.r = r;
+    }
+  }
+  // ---- store the state back
+  const int nb1 = sh.nb, cur = sh.cur;
+  for (int b = tid; b < nb1; b += kThreads) {
+    P.addr[b] = sh.addr[cur][b];
+    P.size[b] = sh.size[cur][b];
+    P.owner[b] = sh.owner[cur][b];
+  }
+  for (int x = tid; x < nflag; x += kThreads) c.w.tflags[x] = sh.tfl[x];
+  if (tid == 0) {
+    P.nb = nb1;
+    P.bytes_free = sh.bytes_free;
+    P.clock = sh.clock;
+    P.pev = sh.pev;
+    P.res = sh.res;
+  }
+  c.w.epochs[tid] = c.epoch;
+  __threadfence_system();
+}
+
+}  // namespace
+}  // namespace coop
+
+// =============================================================================== host
+using namespace coop;
+
+struct coop_pool_s {
+  coop_pool_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  PoolState *d_ps = nullptr;
+  unsigned char *d_graph = nullptr;
+  GraphMut g{};
+  TraceDev td{};
+  unsigned char *ws = nullptr;
+  WsLayout lay{};
+  unsigned char *io_host = nullptr;  // mapped pinned: HostIO | parents | victims
+  unsigned char *io_dev = nullptr;
+  int32_t n_tensors = 0, n_edges = 0;
+  std::vector<uint64_t> sizes;  // host mirror for argument validation
+};
+
+namespace {
+
+size_t io_bytes(const coop_pool_config &c) {
+  return sizeof(HostIO) + (size_t)(c.max_edges + 1) * 4 + (size_t)(kCap + 2) * 4;
+}
+
+void pool_release(coop_pool_s *p) {
+  if (p->stream) cudaStreamDestroy(p->stream);
+  if (p->d_ps) cudaFree(p->d_ps);
+  if (p->d_graph) cudaFree(p->d_graph);
+  if (p->ws) cudaFree(p->ws);
+  if (p->io_host) cudaFreeHost(p->io_host);
+  delete p;
+}
+
+int launch_call(coop_pool_s *p, int32_t kind, int32_t t, uint64_t size, int64_t cost,
+                uint32_t op_flags, int32_t src, int32_t n_parents, uint64_t adv) {
+  PArgs a{};
+  a.k.tr = p->td;
+  a.k.flags = p->cfg.flags;
+  a.k.thr = p->cfg.class_threshold;
+  a.k.max_depth = 512;
+  a.k.n_cells = 1;
+  a.k.ws = p->ws;
+  a.k.lay = p->lay;
+  a.g = p->g;
+  a.ps = p->d_ps;
+  a.kind = kind;
+  a.t = t;
+  a.src = src;
+  a.n_parents = n_parents;
+  a.size = size;
+  a.adv = adv;
+  a.cost = cost;
+  a.op_flags = op_flags;
+  a.io = reinterpret_cast<HostIO *>(p->io_dev);
+  a.io_parents = reinterpret_cast<const int32_t *>(p->io_dev + sizeof(HostIO));
+  a.io_victims = reinterpret_cast<int32_t *>(p->io_dev + sizeof(HostIO) + (size_t)(p->cfg.max_edges + 1) * 4);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != p->device) cudaSetDevice(p->device);
+  pool_kernel<<<1, kThreads, sizeof(Shared), p->stream>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  if (prev != p->device) cudaSetDevice(prev);
+  return e == cudaSuccess ? COOP_OK : COOP_ERR_CUDA;
+}
+
+HostIO &io_of(coop_pool_s *p) { return *reinterpret_cast<HostIO *>(p->io_host); }
+
+int finish(coop_pool_s *p, coop_alloc_result *out, int64_t *evicted, int32_t cap) {
+  HostIO &io = io_of(p);
+  const int st = io.status;
+  if (st == COOP_OK && out) *out = io.r;
+  if (st == COOP_NEEDS_REMAT && out) {
+    memset(out, 0, sizeof(*out));
+    out->tensor_id = io.need_parent;
+    out->window_first = out->window_last = -1;
+  }
+  if (st == COOP_OK && evicted) {
+    const int32_t *v = reinterpret_cast<const int32_t *>(p->io_host + sizeof(HostIO) +
+                                                         (size_t)(p->cfg.max_edges + 1) * 4);
+    for (int k = 0; k < std::min(io.n_victims, cap); ++k) evicted[k] = v[k];
+  }
+  return st;
+}
+
+}  // namespace
+
+extern "C" int coop_pool_init(const coop_pool_config *cfg, coop_pool_t *out) {
+  if (!cfg || !out || cfg->budget < 1 || (cfg->flags & ~7u) || cfg->max_tensors < 1 ||
+      cfg->max_tensors > kMaxT || cfg->max_edges < 0)
+    return COOP_ERR_INVALID_ARG;
+  coop_pool_s *p = new (std::nothrow) coop_pool_s();
+  if (!p) return COOP_ERR_NOMEM;
+  p->cfg = *cfg;
+  if (!p->cfg.class_threshold) p->cfg.class_threshold = 15;
+  cudaGetDevice(&p->device);
+  const int T = cfg->max_tensors, E = cfg->max_edges;
+  // graph arrays: one allocation, 256-byte aligned pieces
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t r = off;
+    off = (off + bytes + 255) / 256 * 256;
+    return r;
+  };
+  const size_t o_size = take((size_t)T * 8), o_prod = take((size_t)T * 4), o_unev = take((size_t)T),
+               o_cost = take((size_t)T * 8), o_out = take((size_t)T * 4), o_src = take((size_t)T * 4),
+               o_phase = take((size_t)T), o_cls = take((size_t)T), o_inp = take((size_t)(T + 1) * 4),
+               o_ini = take((size_t)(E + 1) * 4), o_ch = take((size_t)T * 4),
+               o_cn = take((size_t)(E + 1) * 4), o_co = take((size_t)(E + 1) * 4);
+  int rc = COOP_OK;
+  if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&p->d_ps, sizeof(PoolState)) != cudaSuccess || cudaMalloc(&p->d_graph, off) != cudaSuccess) {
+    rc = COOP_ERR_NOMEM;
+  }
+  p->lay = make_layout(T);
+  if (rc == COOP_OK && cudaMalloc(&p->ws, p->lay.bytes) != cudaSuccess) rc = COOP_ERR_NOMEM;
+  if (rc == COOP_OK && cudaHostAlloc(&p->io_host, io_bytes(p->cfg), cudaHostAllocMapped) != cudaSuccess) {
+    p->io_host = nullptr;
+    rc = COOP_ERR_NOMEM;
+  }
+  if (rc == COOP_OK && cudaHostGetDevicePointer((void **)&p->io_dev, p->io_host, 0) != cudaSuccess) rc = COOP_ERR_CUDA;
+  if (rc == COOP_OK && cudaFuncSetAttribute(pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)sizeof(Shared)) != cudaSuccess)
+    rc = COOP_ERR_CUDA;
+  if (rc != COOP_OK) {
+    pool_release(p);
+    return rc;
+  }
+  unsigned char *b = p->d_graph;
+  GraphMut &g = p->g;
+  g.size = (uint64_t *)(b + o_size);
+  g.producer = (int32_t *)(b + o_prod);
+  g.unevict = (uint8_t *)(b + o_unev);
+  g.cost = (int64_t *)(b + o_cost);
+  g.out = (int32_t *)(b + o_out);
+  g.src = (int32_t *)(b + o_src);
+  g.phase = (uint8_t *)(b + o_phase);
+  g.cls = (uint8_t *)(b + o_cls);
+  g.in_ptr = (int32_t *)(b + o_inp);
+  g.in_idx = (int32_t *)(b + o_ini);
+  g.cons_head = (int32_t *)(b + o_ch);
+  g.cons_next = (int32_t *)(b + o_cn);
+  g.cons_op = (int32_t *)(b + o_co);
+  TraceDev &td = p->td;
+  td.T = T;
+  td.M = T;
+  td.n_params = 0;
+  td.size = g.size;
+  td.producer = g.producer;
+  td.unevict = g.unevict;
+  td.cost = g.cost;
+  td.out = g.out;
+  td.src = g.src;
+  td.phase = g.phase;
+  td.in_ptr = g.in_ptr;
+  td.in_idx = g.in_idx;
+  td.cons_head = g.cons_head;
+  td.cons_next = g.cons_next;
+  td.cons_op = g.cons_op;
+  td.cls = g.cls;
+  // initial state: one free block [0, budget)
+  PoolState *h = new (std::nothrow) PoolState();
+  if (!h) {
+    pool_release(p);
+    return COOP_ERR_NOMEM;
+  }
+  memset(h, 0, sizeof(*h));
+  h->nb = 1;
+  h->addr[0] = 0;
+  h->size[0] = cfg->budget;
+  h->owner[0] = kFree;
+  h->bytes_free = cfg->budget;
+  h->res.fail_op = -1;
+  h->res.digest = 0x9E3779B97F4A7C15ull;
+  h->res.budget = cfg->budget;
+  h->res.max_blocks = 1;
+  bool ok = cudaMemcpy(p->d_ps, h, sizeof(PoolState), cudaMemcpyHostToDevice) == cudaSuccess &&
+            cudaMemset(p->d_graph, 0, off) == cudaSuccess &&
+            cudaMemset(g.cons_head, 0xff, (size_t)T * 4) == cudaSuccess &&
+            cudaMemset(p->ws, 0, p->lay.bytes) == cudaSuccess;
+  delete h;
+  if (!ok) {
+    pool_release(p);
+    return COOP_ERR_CUDA;
+  }
+  memset(p->io_host, 0, io_bytes(p->cfg));
+  p->sizes.reserve((size_t)T);
+  *out = p;
+  return COOP_OK;
+}
+
+extern "C" int coop_pool_destroy(coop_pool_t p) {
+  if (!p) return COOP_ERR_INVALID_ARG;
+  pool_release(p);
+  return COOP_OK;
+}
+
+extern "C" int coop_alloc(coop_pool_t p, uint64_t size, uint64_t cost_us, uint32_t op_flags,
+                          int64_t inplace_src, const int64_t *parents, int32_t n_parents,
+                          coop_alloc_result *out, int64_t *evicted_ids, int32_t evicted_cap) {
+  if (!p) return COOP_ERR_INVALID_ARG;
+  if (size < 1 || size >= (1ull << 48) || cost_us >= (1ull << 40)) return COOP_ERR_INVALID_ARG;
+  if ((op_flags & ~31u) || ((op_flags & COOP_OP_EXPENSIVE) && (op_flags & COOP_OP_CHEAP)))
+    return COOP_ERR_INVALID_ARG;
+  if (n_parents < 0 || (n_parents > 0 && !parents) || evicted_cap < 0 || (evicted_cap > 0 && !evicted_ids))
+    return COOP_ERR_INVALID_ARG;
+  for (int j = 0; j < n_parents; ++j)
+    if (parents[j] < 0 || parents[j] >= p->n_tensors) return COOP_ERR_UNKNOWN_ID;
+  if (op_flags & COOP_OP_INPLACE) {
+    bool seen = false;
+    for (int j = 0; j < n_parents; ++j) seen |= parents[j] == inplace_src;
+    if (!seen || p->sizes[(size_t)inplace_src] != size) return COOP_ERR_INVALID_ARG;
+  } else if (inplace_src != -1) {
+    return COOP_ERR_INVALID_ARG;
+  }
+  if (p->n_tensors >= p->cfg.max_tensors || (int64_t)p->n_edges + n_parents > p->cfg.max_edges)
+    return COOP_ERR_NOMEM;
+  int32_t *par = reinterpret_cast<int32_t *>(p->io_host + sizeof(HostIO));
+  for (int j = 0; j < n_parents; ++j) par[j] = (int32_t)parents[j];
+  const int32_t t = p->n_tensors;
+  const int rc = launch_call(p, PK_ALLOC, t, size, (int64_t)cost_us, op_flags,
+                             (op_flags & COOP_OP_INPLACE) ? (int32_t)inplace_src : -1, n_parents, 0);
+  if (rc != COOP_OK) return rc;
+  const int st = finish(p, out, evicted_ids, evicted_cap);
+  if (st == COOP_OK) {
+    p->n_tensors = t + 1;
+    p->n_edges += n_parents;
+    p->sizes.push_back(size);
+  }
+  return st;
+}
+
+extern "C" int coop_free(coop_pool_t p, int64_t t) {
+  if (!p) return COOP_ERR_INVALID_ARG;
+  if (t < 0 || t >= p->n_tensors) return COOP_ERR_UNKNOWN_ID;
+  const int rc = launch_call(p, PK_FREE, (int32_t)t, 0, 0, 0, -1, 0, 0);
+  return rc != COOP_OK ? rc : io_of(p).status;
+}
+
+extern "C" int coop_access(coop_pool_t p, int64_t t, uint64_t advance_clock_us) {
+  if (!p) return COOP_ERR_INVALID_ARG;
+  if (t < 0 || t >= p->n_tensors) return COOP_ERR_UNKNOWN_ID;
+  if (advance_clock_us >= (1ull << 40)) return COOP_ERR_INVALID_ARG;
+  const int rc = launch_call(p, PK_ACCESS, (int32_t)t, 0, 0, 0, -1, 0, advance_clock_us);
+  return rc != COOP_OK ? rc : io_of(p).status;
+}
+
+extern "C" int coop_rematerialize(coop_pool_t p, int64_t t, coop_alloc_result *out,
+                                  int64_t *evicted_ids, int32_t evicted_cap) {
+  if (!p) return COOP_ERR_INVALID_ARG;
+  if (t < 0 || t >= p->n_tensors) return COOP_ERR_UNKNOWN_ID;
+  if (evicted_cap < 0 || (evicted_cap > 0 && !evicted_ids)) return COOP_ERR_INVALID_ARG;
+  const int rc = launch_call(p, PK_REMAT, (int32_t)t, 0, 0, 0, -1, 0, 0);
+  if (rc != COOP_OK) return rc;
+  return finish(p, out, evicted_ids, evicted_cap);
+}
+
+extern "C" int coop_pool_stats(coop_pool_t p, coop_replay_result *out) {
+  if (!p || !out) return COOP_ERR_INVALID_ARG;
+  if (cudaMemcpy(out, &p->d_ps->res, sizeof(*out), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return COOP_ERR_CUDA;
+  out->status = COOP_OK;
+  return COOP_OK;
+}
+
+extern "C" int coop_pool_layout(coop_pool_t p, uint64_t *addr, uint64_t *size, int64_t *owner,
+                                int32_t cap, int32_t *n_blocks) {
+  if (!p || !n_blocks || cap < 0 || (cap > 0 && (!addr || !size || !owner))) return COOP_ERR_INVALID_ARG;
+  int32_t nb = 0;
+  if (cudaMemcpy(&nb, &p->d_ps->nb, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return COOP_ERR_CUDA;
+  const int n = std::min(nb, cap);
+  std::vector<int32_t> ow((size_t)std::max(n, 1));
+  if (n > 0 && (cudaMemcpy(addr, p->d_ps->addr, (size_t)n * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+                cudaMemcpy(size, p->d_ps->size, (size_t)n * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+                cudaMemcpy(ow.data(), p->d_ps->owner, (size_t)n * 4, cudaMemcpyDeviceToHost) != cudaSuccess))
+    return COOP_ERR_CUDA;
+  for (int i = 0; i < n; ++i) owner[i] = ow[(size_t)i];
+  *n_blocks = nb;
+  return COOP_OK;
+}

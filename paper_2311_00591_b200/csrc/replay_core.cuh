@@ -1,0 +1,1019 @@
+// replay_core.cuh -- the device side of the Alg. 1 engine shared by the trace replay
+// (coop_replay.cu, one CTA per (trace, budget) cell) and the online single-pool calls
+// (coop_pool.cu, one CTA per call on a persistent device-resident pool).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <new>
+#include <vector>
+
+#include "coop.h"
+#include "coop_internal.h"
+#include "fixed192.cuh"
+
+namespace coop {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kCap = 2048;       // blocks per pool held by the kernel (COOP_ERR_NOMEM beyond)
+constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
+constexpr int kDfsCap = 512;     // per-thread DFS stack (projected-cost closures)
+constexpr int kFree = -1;
+constexpr int kMaxT = 16384;     // tensors per trace whose flags live in shared memory
+constexpr int kVisCap = 64;      // per-thread DFS visited set in shared memory (power of 2)
+
+enum : uint8_t { TF_RES = 1, TF_BORN = 2, TF_DEAD = 4, TF_LOCK = 8 };
+
+struct TraceDev {
+  int32_t T, M, n_params;
+  const uint64_t *size;
+  const int32_t *producer;
+  const uint8_t *unevict;
+  const int64_t *cost;
+  const int32_t *out;
+  const int32_t *src;
+  const uint8_t *phase;
+  const int32_t *in_ptr, *in_idx;
+  // consumers as singly linked edge lists (the online pool appends edges as tensors
+  // are created): the ops reading x are cons_op[e] for e = cons_head[x], cons_next[e], ...
+  // until -1
+  const int32_t *cons_head, *cons_next, *cons_op;
+  const uint8_t *cls;  // per op: 0 = class by threshold (R14), 1 = C1, 2 = C2; NULL = all 0
+  const int32_t *lock_ptr, *lock_idx;
+  const int32_t *die_ptr, *die_idx;
+  const int32_t *params;
+};
+
+struct WsLayout {  // byte offsets inside one cell's workspace
+  size_t tflags, pins, last_access, taddr, epochs, marks, isz, ih, ist, S, H, B, trans, victims, memoA, memoD;
+  size_t bytes;
+};
+
+struct CellPtrs {
+  uint8_t *tflags;
+  int32_t *pins;
+  int64_t *last_access;
+  uint64_t *taddr;
+  uint32_t *epochs, *marks;
+  uint64_t *isz;
+  double *ih;
+  uint8_t *ist;
+  uint64_t *S;
+  U192 *H;
+  int32_t *B;
+  int32_t *trans, *victims;
+  uint64_t *memoA, *memoD;
+};
+
+struct KArgs {
+  TraceDev tr;
+  const uint64_t *budgets;
+  uint32_t flags, thr;
+  int32_t max_depth;
+  int32_t n_cells;
+  coop_replay_result *out;
+  coop_event *log;
+  int64_t log_cap;
+  unsigned char *ws;
+  WsLayout lay;
+};
+
+struct Shared {
+  uint64_t addr[2][kCap + 2];  // the inactive buffer doubles as search scratch (S, B, state)
+  uint64_t size[2][kCap + 2];
+  int32_t owner[2][kCap + 2];
+  uint8_t tfl[kMaxT];          // per-tensor flags TF_*
+  uint32_t vis[kThreads][kVisCap];  // per-thread open-addressing set of visited tensors (DFS)
+  uint64_t wS[kWarps];
+  U192 wH[kWarps];
+  int32_t wB[kWarps];
+  int32_t cur, nb;
+  // CTA-uniform scalars (written by thread 0, published by a barrier)
+  uint64_t bytes_free;
+  int64_t clock;
+  int32_t status, fail_op, cur_op;
+  int32_t sp;
+  int32_t ntrans;
+  int32_t bcast_i;
+  uint64_t bcast_u;
+  // counters (thread 0 only)
+  coop_replay_result res;
+  // rematerialization stack
+  int32_t st_t[kStackCap], st_stage[kStackCap], st_idx[kStackCap], st_depth[kStackCap];
+  // reductions
+  uint64_t red64[2][kWarps];
+  int32_t red32[2][kWarps];
+  U192 red192[kWarps];
+  int32_t redpar;
+  uint32_t pev;  // pressure-event epoch of the projected-cost memo
+  // the last evicted window (read by the online calls): items, span, cost bits, victims
+  int32_t win_first, win_last, nvict;
+  uint64_t win_span, win_cost;
+};
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ------------------------------------------------------------------ CTA reductions
+// Each returns the reduced value to every thread (two barriers-worth of ordering via a
+// parity-double-buffered scratch: one __syncthreads per call).
+__device__ __forceinline__ int32_t cta_min_i32(Shared &sh, int32_t v) {
+  for (int d = 16; d > 0; d >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, d));
+  const int par = sh.redpar;
+  if ((threadIdx.x & 31) == 0) sh.red32[par][threadIdx.x >> 5] = v;
+  __syncthreads();
+  int32_t r = sh.red32[par][0];
+  for (int w = 1; w < kWarps; ++w) r = min(r, sh.red32[par][w]);
+  if (threadIdx.x == 0) sh.redpar = par ^ 1;  // next call uses the other buffer
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ int32_t cta_max_i32(Shared &sh, int32_t v) { return -cta_min_i32(sh, -v); }
+__device__ __forceinline__ int32_t cta_sum_i32(Shared &sh, int32_t v) {
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  const int par = sh.redpar;
+  if ((threadIdx.x & 31) == 0) sh.red32[par][threadIdx.x >> 5] = v;
+  __syncthreads();
+  int32_t r = 0;
+  for (int w = 0; w < kWarps; ++w) r += sh.red32[par][w];
+  if (threadIdx.x == 0) sh.redpar = par ^ 1;
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ uint64_t cta_min_u64(Shared &sh, uint64_t v) {
+  for (int d = 16; d > 0; d >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, v, d);
+    v = o < v ? o : v;
+  }
+  const int par = sh.redpar;
+  if ((threadIdx.x & 31) == 0) sh.red64[par][threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint64_t r = sh.red64[par][0];
+  for (int w = 1; w < kWarps; ++w) r = sh.red64[par][w] < r ? sh.red64[par][w] : r;
+  if (threadIdx.x == 0) sh.redpar = par ^ 1;
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------ the replay cell
+struct Cell {
+  const KArgs &a;
+  const TraceDev &tr;
+  Shared &sh;
+  CellPtrs w;
+  int cell;
+  uint32_t epoch;  // per-thread DFS epoch
+  coop_event *log;
+
+  __device__ Cell(const KArgs &a_, Shared &sh_, int cell_) : a(a_), tr(a_.tr), sh(sh_), cell(cell_) {
+    unsigned char *base = a.ws + (size_t)blockIdx.x * a.lay.bytes;  // this CTA's slot
+    w.tflags = (uint8_t *)(base + a.lay.tflags);
+    w.pins = (int32_t *)(base + a.lay.pins);
+    w.last_access = (int64_t *)(base + a.lay.last_access);
+    w.taddr = (uint64_t *)(base + a.lay.taddr);
+    w.epochs = (uint32_t *)(base + a.lay.epochs);
+    w.marks = (uint32_t *)(base + a.lay.marks);
+    w.isz = (uint64_t *)(base + a.lay.isz);
+    w.ih = (double *)(base + a.lay.ih);
+    w.ist = (uint8_t *)(base + a.lay.ist);
+    w.S = (uint64_t *)(base + a.lay.S);
+    w.H = (U192 *)(base + a.lay.H);
+    w.B = (int32_t *)(base + a.lay.B);
+    w.trans = (int32_t *)(base + a.lay.trans);
+    w.victims = (int32_t *)(base + a.lay.victims);
+    w.memoA = (uint64_t *)(base + a.lay.memoA);
+    w.memoD = (uint64_t *)(base + a.lay.memoD);
+    log = a.log ? a.log + (size_t)cell * a.log_cap : nullptr;
+  }
+
+  __device__ __forceinline__ bool ok() const { return sh.status == COOP_OK; }
+  __device__ __forceinline__ int nin(int op) const { return tr.in_ptr[op + 1] - tr.in_ptr[op]; }
+  __device__ __forceinline__ int in_at(int op, int j) const { return tr.in_idx[tr.in_ptr[op] + j]; }
+  __device__ __forceinline__ uint64_t *A() { return sh.addr[sh.cur]; }
+  __device__ __forceinline__ uint64_t *Z() { return sh.size[sh.cur]; }
+  __device__ __forceinline__ int32_t *O() { return sh.owner[sh.cur]; }
+
+  __device__ void log_ev(int kind, int op, int t, uint64_t addr) {  // thread 0 only
+    const int64_t i = sh.res.n_events++;
+    if (log && i < a.log_cap) {
+      coop_event e;
+      e.kind = kind;
+      e.op = op;
+      e.tensor = t;
+      e.pad = 0;
+      e.addr = addr;
+      log[i] = e;
+    }
+  }
+
+  // ---------------------------------------------------------------- block table ops
+  // lowest (right = false) / highest (right = true) free block with size >= need, or -1
+  __device__ int find_fit(uint64_t need, bool right) {
+    const int nb = sh.nb;
+    int best = right ? -1 : 0x7fffffff;
+    for (int b = threadIdx.x; b < nb; b += kThreads)
+      if (O()[b] == kFree && Z()[b] >= need) best = right ? max(best, b) : min(best, b);
+    if (right) return cta_max_i32(sh, best);
+    const int r = cta_min_i32(sh, best);
+    return r == 0x7fffffff ? -1 : r;
+  }
+
+  // replace blocks [lo, hi] (hi >= lo - 1; hi = lo - 1 means pure insertion at lo) by the
+  // m new blocks nb_[0..m) -- one parallel copy into the other buffer
+  __device__ void splice(int lo, int hi, int m, const uint64_t *na, const uint64_t *nz, const int32_t *no) {
+    const int nb = sh.nb, cur = sh.cur, nxt = cur ^ 1;
+    const int removed = hi - lo + 1;
+    const int nnb = nb - removed + m;
+    for (int j = threadIdx.x; j < nnb; j += kThreads) {
+      uint64_t ad, sz;
+      int32_t ow;
+      if (j < lo) {
+        ad = sh.addr[cur][j]; sz = sh.size[cur][j]; ow = sh.owner[cur][j];
+      } else if (j < lo + m) {
+        ad = na[j - lo]; sz = nz[j - lo]; ow = no[j - lo];
+      } else {
+        const int s = j - m + removed;
+        ad = sh.addr[cur][s]; sz = sh.size[cur][s]; ow = sh.owner[cur][s];
+      }
+      sh.addr[nxt][j] = ad;
+      sh.size[nxt][j] = sz;
+      sh.owner[nxt][j] = ow;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sh.cur = nxt;
+      sh.nb = nnb;
+      if (nnb > sh.res.max_blocks) sh.res.max_blocks = nnb;
+    }
+    __syncthreads();
+  }
+
+  // place `need` bytes of tensor t into free block i (left end, or right end - need)
+  __device__ uint64_t place(int i, uint64_t need, bool right, int t) {
+    const uint64_t fa = A()[i], fz = Z()[i];
+    uint64_t at;
+    if (fz == need) {
+      __syncthreads();
+      if (threadIdx.x == 0) O()[i] = t;
+      at = fa;
+      __syncthreads();
+    } else if (sh.nb + 1 > kCap) {
+      if (threadIdx.x == 0) sh.status = COOP_ERR_NOMEM;
+      __syncthreads();
+      return 0;
+    } else if (!right) {
+      const uint64_t na[2] = {fa, fa + need}, nz[2] = {need, fz - need};
+      const int32_t no[2] = {t, kFree};
+      splice(i, i, 2, na, nz, no);
+      at = fa;
+    } else {
+      const uint64_t na[2] = {fa, fa + fz - need}, nz[2] = {fz - need, need};
+      const int32_t no[2] = {kFree, t};
+      splice(i, i, 2, na, nz, no);
+      at = fa + fz - need;
+    }
+    if (threadIdx.x == 0) sh.bytes_free -= need;
+    return at;
+  }
+
+  __device__ int block_of_addr(uint64_t ad) {  // binary search (uniform)
+    int lo = 0, hi = sh.nb - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (A()[mid] <= ad) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  }
+
+  // free block i and merge with free neighbours
+  __device__ void release(int i) {
+    const int nb = sh.nb;
+    int lo = i, hi = i;
+    if (i > 0 && O()[i - 1] == kFree) lo = i - 1;
+    if (i + 1 < nb && O()[i + 1] == kFree) hi = i + 1;
+    const uint64_t na = A()[lo], nz = A()[hi] + Z()[hi] - A()[lo];
+    const int32_t no = kFree;
+    if (threadIdx.x == 0) sh.bytes_free += Z()[i];
+    splice(lo, hi, 1, &na, &nz, &no);
+  }
+
+  __device__ void free_tensor(int t) {  // resident tensor -> freed (R20, R22)
+    const uint64_t ad = w.taddr[t];
+    const int b = block_of_addr(ad);
+    release(b);
+    if (threadIdx.x == 0) {
+      sh.tfl[t] &= (uint8_t)~TF_RES;
+      log_ev(4, sh.cur_op, t, ad);
+    }
+    __syncthreads();
+  }
+
+  // ---------------------------------------------------------------- heuristics
+  __device__ bool is_c1(int op) const {  // R14: C1 iff cost * 2^20 >= thr * out bytes
+    if (tr.cls && tr.cls[op]) return tr.cls[op] == 1;  // online calls: explicit class (R41)
+    return (uint64_t)tr.cost[op] * 1048576ull >= (uint64_t)a.thr * tr.size[tr.out[op]];
+  }
+  __device__ bool goes_right(int op) const {  // PAPER.md:173; R12-R13
+    if (!(a.flags & COOP_F_PARTITION)) return false;
+    if (tr.phase[op] != COOP_PHASE_FWD && !(a.flags & COOP_F_PARTITION_ALL_PHASES)) return false;
+    return !is_c1(op);
+  }
+
+  // c(t) = producer cost + the SET of non-resident ancestors reachable through
+  // non-resident tensors + the SET of evicted descendants reachable through evicted
+  // tensors (R18).  One thread; visited marks = per-thread epochs.
+  // ---------------- projected cost c(t) (R18) --------------------
+  // c(t) = cost(producer(t)) + cost of Anc(t) + cost of Desc(t) where
+  //   Anc(t)  = the SET of non-resident tensors reachable upward from t's inputs through
+  //             non-resident tensors (parameters stop),
+  //   Desc(t) = the SET of evicted live tensors reachable downward from t's consumers'
+  //             outputs through evicted live tensors.
+  // Within one pressure event residency is fixed, so the closures of single-entry chains
+  // are memoized: Up*(u) = {u} U Up*(v) when v is u's only non-resident input (disjoint in
+  // a DAG), likewise Down*; nodes with two or more entries get an exact set-closure DFS.
+  // Memo words: (event epoch << 40) | value (values >= 2^40 are not memoized).
+  __device__ __forceinline__ bool up_ok(int u) const {  // non-resident, recomputable
+    return !(sh.tfl[u] & TF_RES) && __ldg(&tr.producer[u]) >= 0;
+  }
+  __device__ __forceinline__ bool down_ok(int d) const {  // evicted and live
+    const uint8_t f = sh.tfl[d];
+    return (f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD);
+  }
+  __device__ __forceinline__ bool memo_get(const uint64_t *m, int x, int64_t &v) const {
+    const uint64_t w_ = ((volatile const uint64_t *)m)[x];
+    if ((uint32_t)(w_ >> 40) != sh.pev) return false;
+    v = (int64_t)(w_ & ((1ull << 40) - 1ull));
+    return true;
+  }
+  __device__ __forceinline__ void memo_put(uint64_t *m, int x, int64_t v) const {
+    if (v >= 0 && v < (1ll << 40)) ((volatile uint64_t *)m)[x] = ((uint64_t)sh.pev << 40) | (uint64_t)v;
+  }
+
+  // exact set closure by DFS: UP = ancestors through up_ok, else descendants through
+  // down_ok; roots = x itself (NEIGH false) or x's inputs / consumer outputs (NEIGH true);
+  // returns the summed producer costs of the set
+  template <bool UP, bool NEIGH>
+  __device__ int64_t closure_dfs(int x0, bool &overflow) {
+    uint32_t *vs = sh.vis[threadIdx.x];
+    for (int k = 0; k < kVisCap; ++k) vs[k] = 0u;
+    int nvis = 0;
+    bool use_marks = false;
+    uint32_t *mk = w.marks + (size_t)threadIdx.x * tr.T;
+    uint32_t ep = 0;
+    auto seen = [&](int x) -> bool {  // test-and-insert
+      if (use_marks) {
+        if (mk[x] == ep) return true;
+        mk[x] = ep;
+        return false;
+      }
+      uint32_t hsh = ((uint32_t)x * 2654435761u) & (kVisCap - 1);
+      while (true) {
+        const uint32_t k = vs[hsh];
+        if (k == (uint32_t)x + 1u) return true;
+        if (k == 0u) break;
+        hsh = (hsh + 1) & (kVisCap - 1);
+      }
+      vs[hsh] = (uint32_t)x + 1u;
+      ++nvis;
+      return false;
+    };
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (attempt == 1) {
+        use_marks = true;
+        ep = ++epoch;
+      }
+      int64_t c = 0;
+      bool full = false;
+      int stk[kDfsCap];
+      int sp = 0;
+      if (!NEIGH) {
+        stk[sp++] = x0;
+      } else if (UP) {
+        const int p0 = __ldg(&tr.producer[x0]);
+        for (int j = __ldg(&tr.in_ptr[p0]); j < __ldg(&tr.in_ptr[p0 + 1]); ++j) {
+          if (sp == kDfsCap) { overflow = true; return c; }
+          stk[sp++] = __ldg(&tr.in_idx[j]);
+        }
+      } else {
+        for (int e = __ldg(&tr.cons_head[x0]); e >= 0; e = __ldg(&tr.cons_next[e])) {
+          if (sp == kDfsCap) { overflow = true; return c; }
+          stk[sp++] = __ldg(&tr.out[__ldg(&tr.cons_op[e])]);
+        }
+      }
+      while (sp > 0) {
+        const int x = stk[--sp];
+        if (UP ? !up_ok(x) : !down_ok(x)) continue;
+        if (!use_marks && nvis >= kVisCap / 2) { full = true; break; }
+        if (seen(x)) continue;
+        const int px = __ldg(&tr.producer[x]);
+        c += __ldg(&tr.cost[px]);
+        if (UP) {
+          for (int j = __ldg(&tr.in_ptr[px]); j < __ldg(&tr.in_ptr[px + 1]); ++j) {
+            if (sp == kDfsCap) { overflow = true; return c; }
+            stk[sp++] = __ldg(&tr.in_idx[j]);
+          }
+        } else {
+          for (int e = __ldg(&tr.cons_head[x]); e >= 0; e = __ldg(&tr.cons_next[e])) {
+            if (sp == kDfsCap) { overflow = true; return c; }
+            stk[sp++] = __ldg(&tr.out[__ldg(&tr.cons_op[e])]);
+          }
+        }
+      }
+      if (!full) return c;
+    }
+    return 0;
+  }
+
+  // entries of x: its non-resident inputs (UP) or its evicted live consumer outputs (down)
+  template <bool UP>
+  __device__ __forceinline__ int entries(int x, int *buf, int cap) const {
+    int k = 0;
+    if (UP) {
+      const int px = __ldg(&tr.producer[x]);
+      for (int j = __ldg(&tr.in_ptr[px]); j < __ldg(&tr.in_ptr[px + 1]); ++j) {
+        const int u = __ldg(&tr.in_idx[j]);
+        if (up_ok(u)) {
+          bool dup = false;
+          for (int q = 0; q < min(k, cap); ++q) dup |= (buf[q] == u);
+          if (!dup) {
+            if (k < cap) buf[k] = u;
+            ++k;
+          }
+        }
+      }
+    } else {
+      for (int e = __ldg(&tr.cons_head[x]); e >= 0; e = __ldg(&tr.cons_next[e])) {
+        const int d = __ldg(&tr.out[__ldg(&tr.cons_op[e])]);
+        if (down_ok(d)) {
+          bool dup = false;
+          for (int q = 0; q < min(k, cap); ++q) dup |= (buf[q] == d);
+          if (!dup) {
+            if (k < cap) buf[k] = d;
+            ++k;
+          }
+        }
+      }
+    }
+    return k;
+  }
+
+  // cost of the closure of node x (x itself included; x satisfies up_ok / down_ok)
+  template <bool UP>
+  __device__ int64_t node_closure(int x0, bool &overflow) {
+    uint64_t *memo = UP ? w.memoA : w.memoD;
+    int chain[64];
+    int nch = 0;
+    int x = x0;
+    int64_t base = 0;
+    while (true) {
+      int64_t mv;
+      if (memo_get(memo, x, mv)) {
+        base = mv;
+        break;
+      }
+      int buf[4];
+      const int k = entries<UP>(x, buf, 4);
+      if (k == 1 && nch < 64) {  // single entry: Up*(x) = {x} U Up*(entry)
+        chain[nch++] = x;
+        x = buf[0];
+        continue;
+      }
+      if (k == 0) {
+        base = __ldg(&tr.cost[__ldg(&tr.producer[x])]);
+      } else {
+        base = closure_dfs<UP, false>(x, overflow);  // two or more entries: exact set closure
+      }
+      memo_put(memo, x, base);
+      break;
+    }
+    while (nch > 0) {
+      const int y = chain[--nch];
+      base += __ldg(&tr.cost[__ldg(&tr.producer[y])]);
+      memo_put(memo, y, base);
+    }
+    return base;
+  }
+
+  __device__ int64_t projected_cost(int t, bool &overflow) {
+    int64_t c = __ldg(&tr.cost[__ldg(&tr.producer[t])]);
+    int buf[4];
+    const int ka = entries<true>(t, buf, 4);
+    if (ka == 1) c += node_closure<true>(buf[0], overflow);
+    else if (ka > 1) c += closure_dfs<true, true>(t, overflow);
+    const int kd = entries<false>(t, buf, 4);
+    if (kd == 1) c += node_closure<false>(buf[0], overflow);
+    else if (kd > 1) c += closure_dfs<false, true>(t, overflow);
+    return c;
+  }
+
+  // ---------------------------------------------------------------- Sec. 3.3 search
+  // Sliding-window search over the address-ordered item view and eviction of the window;
+  // returns false when no window exists (R24).  Scratch: the inactive block buffer holds
+  // S (span prefix, u64) in its addr[], B (barrier count prefix) in its size[] and the
+  // item states in its owner[]; the exact 192-bit prefix H and h live in global memory.
+  __device__ bool evict_window(uint64_t need) {
+    const uint64_t t0 = gtimer();
+    if (threadIdx.x == 0) {
+      if (++sh.pev >= (1u << 24)) {  // epoch wrap: clear the memo (never in practice)
+        sh.pev = 1;
+        for (int t = 0; t < tr.T; ++t) w.memoA[t] = w.memoD[t] = 0ull;
+      }
+    }
+    __syncthreads();
+    const int nb = sh.nb, nx = sh.cur ^ 1;
+    uint64_t *S = sh.addr[nx];
+    int32_t *Bc = reinterpret_cast<int32_t *>(sh.size[nx]);
+    int32_t *St = sh.owner[nx];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // item view (contiguous chunk per thread): FREE -> h = 0; unevictable / pinned /
+    // locked -> barrier; else h = c/s with the projected cost and the staleness
+    const int chunk = (nb + kThreads - 1) / kThreads;
+    const int b0 = min(nb, (int)threadIdx.x * chunk), b1 = min(nb, b0 + chunk);
+    int nev = 0;
+    bool overflow = false;
+    uint64_t ls = 0;
+    U192 lh = u192_zero();
+    int lb = 0;
+    for (int b = b0; b < b1; ++b) {
+      const int o = O()[b];
+      int st;
+      double h = 0.0;
+      if (o == kFree) {
+        st = COOP_FREE;
+      } else if (__ldg(&tr.unevict[o]) || w.pins[o] > 0 || (sh.tfl[o] & TF_LOCK)) {
+        st = COOP_PINNED;
+      } else {
+        st = COOP_EVICTABLE;
+        int64_t s = sh.clock - w.last_access[o];  // staleness (R17)
+        if (s < 1) s = 1;
+        h = __ddiv_rn((double)projected_cost(o, overflow), (double)s);
+        ++nev;
+      }
+      w.ih[b] = h;
+      St[b] = st;
+      ls += Z()[b];
+      lh = u192_add(lh, u192_from_double(h));
+      lb += (st == COOP_PINNED);
+    }
+    // exclusive scans of the thread totals: warp shuffles, then the <= 8 warp totals
+    uint64_t is = ls;
+    U192 ih = lh;
+    int ib = lb;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t so = __shfl_up_sync(0xffffffffu, is, d);
+      U192 ho;
+      ho.w0 = __shfl_up_sync(0xffffffffu, ih.w0, d);
+      ho.w1 = __shfl_up_sync(0xffffffffu, ih.w1, d);
+      ho.w2 = __shfl_up_sync(0xffffffffu, ih.w2, d);
+      const int bo = __shfl_up_sync(0xffffffffu, ib, d);
+      if (lane >= d) {
+        is += so;
+        ih = u192_add(ih, ho);
+        ib += bo;
+      }
+    }
+    if (lane == 31) {
+      sh.wS[warp] = is;
+      sh.wH[warp] = ih;
+      sh.wB[warp] = ib;
+    }
+    nev = cta_sum_i32(sh, nev);  // (its barrier also publishes the warp totals)
+    if (cta_max_i32(sh, overflow ? 1 : 0)) {
+      if (threadIdx.x == 0) sh.status = COOP_ERR_NOMEM;
+      __syncthreads();
+      return false;
+    }
+    uint64_t cs = is - ls;  // exclusive within the warp
+    U192 ch = u192_sub(ih, lh);
+    int cb = ib - lb;
+    for (int w2 = 0; w2 < warp; ++w2) {
+      cs += sh.wS[w2];
+      ch = u192_add(ch, sh.wH[w2]);
+      cb += sh.wB[w2];
+    }
+    for (int b = b0; b < b1; ++b) {
+      S[b] = cs;
+      w.H[b] = ch;
+      Bc[b] = cb;
+      cs += Z()[b];
+      ch = u192_add(ch, u192_from_double(w.ih[b]));
+      cb += (St[b] == COOP_PINNED);
+    }
+    if (b1 == nb && b0 < b1) {
+      S[nb] = cs;
+      w.H[nb] = ch;
+      Bc[nb] = cb;
+    }
+    if (nb == 0 && threadIdx.x == 0) {
+      S[0] = 0;
+      Bc[0] = 0;
+    }
+    __syncthreads();
+    // per start: minimal end by bisection on S, barrier check, exact cost RN(H[e] - H[i]);
+    // argmin over (cost bits, start) (R3, R4)
+    const uint64_t Stot = S[nb];
+    uint64_t bestc = ~0ull;
+    int besti = 0x7fffffff;
+    for (int i = threadIdx.x; i < nb; i += kThreads) {
+      if (St[i] == COOP_PINNED) continue;
+      const uint64_t target = S[i] + need;
+      if (target > Stot) continue;
+      int lo = i + 1, hi = nb;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (S[mid] >= target) hi = mid;
+        else lo = mid + 1;
+      }
+      const int e = lo;
+      if (Bc[e] != Bc[i]) continue;
+      const uint64_t cb2 = (uint64_t)__double_as_longlong(u192_round_to_double(u192_sub(w.H[e], w.H[i])));
+      if (cb2 < bestc || (cb2 == bestc && i < besti)) {
+        bestc = cb2;
+        besti = i;
+      }
+    }
+    const uint64_t cmin = cta_min_u64(sh, bestc);
+    const int first = cta_min_i32(sh, bestc == cmin ? besti : 0x7fffffff);
+    if (threadIdx.x == 0) {
+      sh.res.heuristic_evals += nev;
+      const int64_t dt = (int64_t)(gtimer() - t0);
+      sh.res.search_ns_total += dt;
+      if (dt > sh.res.search_ns_max) sh.res.search_ns_max = dt;
+    }
+    if (cmin == ~0ull) {
+      __syncthreads();
+      return false;
+    }
+    // window end of the winner; evict its tensors in ascending address order (R10)
+    int last;
+    {
+      const uint64_t target = S[first] + need;
+      int lo = first + 1, hi = nb;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (S[mid] >= target) hi = mid;
+        else lo = mid + 1;
+      }
+      last = lo - 1;
+    }
+    if (threadIdx.x == 0) {
+      sh.win_first = first;
+      sh.win_last = last;
+      sh.win_span = S[last + 1] - S[first];
+      sh.win_cost = cmin;
+      sh.nvict = 0;
+      uint64_t d = sh.res.digest;
+      for (int b = first; b <= last; ++b) {
+        const int o = O()[b];
+        if (o == kFree) continue;
+        w.victims[sh.nvict++] = o;
+        const uint64_t ad = A()[b];
+        sh.tfl[o] &= (uint8_t)~TF_RES;
+        sh.res.evictions++;
+        log_ev(3, sh.cur_op, o, ad);
+        d = splitmix64(d ^ (((uint64_t)(uint32_t)sh.cur_op << 32) | (uint32_t)o));  // R29
+        d = splitmix64(d ^ ad);
+        sh.bytes_free += Z()[b];
+      }
+      sh.res.digest = d;
+    }
+    __syncthreads();
+    // the window and its free neighbours coalesce into one free block
+    int lo = first, hi = last;
+    if (lo > 0 && O()[lo - 1] == kFree) --lo;
+    if (hi + 1 < nb && O()[hi + 1] == kFree) ++hi;
+    const uint64_t na = A()[lo], nz = A()[hi] + Z()[hi] - A()[lo];
+    const int32_t no = kFree;
+    splice(lo, hi, 1, &na, &nz, &no);
+    return true;
+  }
+
+  // ---------------------------------------------------------------- Alg. 1
+  __device__ void allocate(int op, int t, bool allow_inplace, int kind) {
+    const uint64_t need = tr.size[t];
+    const int src = tr.src[op];
+    if (allow_inplace && src >= 0 && (a.flags & COOP_F_INPLACE)) {  // addr <- input.addr
+      const uint64_t ad = w.taddr[src];
+      const int b = block_of_addr(ad);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        O()[b] = t;
+        w.taddr[t] = ad;
+        sh.tfl[src] &= (uint8_t)~TF_RES;
+        sh.tfl[t] |= TF_RES;
+        sh.res.inplace_reuse++;
+        log_ev(2, op, t, ad);
+      }
+      __syncthreads();
+      return;
+    }
+    const bool right = goes_right(op);
+    int i = find_fit(need, right);
+    uint64_t at;
+    if (i < 0) {
+      if (threadIdx.x == 0) {
+        sh.res.pressure++;
+        if (sh.bytes_free >= need) sh.res.frag_fail++;
+      }
+      if (!evict_window(need)) {
+        if (threadIdx.x == 0) {
+          if (sh.status == COOP_OK) sh.status = COOP_ERR_UNSATISFIABLE;
+          sh.res.fail_op = sh.cur_op;
+        }
+        __syncthreads();
+        return;
+      }
+      i = find_fit(need, right);  // the unique coalesced block >= need
+      at = place(i, need, right, t);
+      if (!ok()) return;
+      int nfree = 0;
+      for (int b = threadIdx.x; b < sh.nb; b += kThreads) nfree += (O()[b] == kFree);
+      nfree = cta_sum_i32(sh, nfree);
+      if (threadIdx.x == 0) {
+        sh.res.sum_free_bytes_after += sh.bytes_free;  // R27
+        sh.res.sum_free_blocks_after += nfree;
+      }
+    } else {
+      at = place(i, need, right, t);
+      if (!ok()) return;
+    }
+    if (threadIdx.x == 0) {
+      w.taddr[t] = at;
+      sh.tfl[t] |= TF_RES;
+      log_ev(kind, op, t, at);
+    }
+    __syncthreads();
+  }
+
+  // ---------------------------------------------------------------- rematerialization
+  // M(t): explicit stack (R21-R23); a dead tensor recomputed here stays resident until
+  // the end of the current trace op (R22).
+  __device__ void materialize(int t0) {
+    if (threadIdx.x == 0) {
+      sh.sp = 1;
+      sh.st_t[0] = t0;
+      sh.st_stage[0] = 0;
+      sh.st_idx[0] = 0;
+      sh.st_depth[0] = 0;
+    }
+    __syncthreads();
+    while (sh.sp > 0 && ok()) {
+      const int f = sh.sp - 1;
+      const int t = sh.st_t[f], depth = sh.st_depth[f];
+      const int op = tr.producer[t];
+      if (sh.st_stage[f] == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          if (depth > a.max_depth) {
+            sh.status = COOP_ERR_THRASHED;  // R23
+            sh.res.fail_op = sh.cur_op;
+          } else if (op < 0) {
+            sh.status = COOP_ERR_UNSATISFIABLE;
+            sh.res.fail_op = sh.cur_op;
+          } else {
+            if (depth > sh.res.max_depth) sh.res.max_depth = depth;
+            sh.st_stage[f] = 1;
+          }
+        }
+        __syncthreads();
+        if (!ok()) return;
+        for (int j = threadIdx.x; j < nin(op); j += kThreads) atomicAdd(&w.pins[in_at(op, j)], 1);
+        __syncthreads();
+        continue;
+      }
+      if (sh.st_stage[f] == 1) {
+        int j = sh.st_idx[f];
+        const int n = nin(op);
+        while (j < n && (sh.tfl[in_at(op, j)] & TF_RES)) ++j;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          if (j < n) {
+            sh.st_idx[f] = j + 1;
+            if (sh.sp >= kStackCap) {
+              sh.status = COOP_ERR_THRASHED;
+              sh.res.fail_op = sh.cur_op;
+            } else {
+              const int g = sh.sp++;
+              sh.st_t[g] = in_at(op, j);
+              sh.st_stage[g] = 0;
+              sh.st_idx[g] = 0;
+              sh.st_depth[g] = depth + 1;
+            }
+          } else {
+            sh.st_stage[f] = 2;
+          }
+        }
+        __syncthreads();
+        continue;
+      }
+      // stage 2: recompute t out-of-place (R21)
+      allocate(op, t, false, 5);
+      if (!ok()) return;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        sh.clock += tr.cost[op];
+        sh.res.total_us += tr.cost[op];
+        sh.res.remat++;
+        log_ev(7, op, t, w.taddr[t]);
+        if (sh.tfl[t] & TF_DEAD) {
+          if (sh.ntrans < 4 * tr.T) w.trans[sh.ntrans++] = t;
+          else sh.status = COOP_ERR_NOMEM;
+        }
+        sh.sp--;
+      }
+      __syncthreads();
+      const int64_t clk = sh.clock;
+      for (int j = threadIdx.x; j < nin(op); j += kThreads) {
+        const int u = in_at(op, j);
+        w.last_access[u] = clk;
+        atomicSub(&w.pins[u], 1);
+      }
+      if (threadIdx.x == 0) w.last_access[t] = clk;
+      __syncthreads();
+    }
+  }
+
+  // ---------------------------------------------------------------- the op loop
+  __device__ void run(uint64_t budget) {
+    const int T = tr.T, M = tr.M;
+    for (int t = threadIdx.x; t < T; t += kThreads) {
+      w.memoA[t] = 0ull;
+      w.memoD[t] = 0ull;
+      sh.tfl[t] = 0;
+      w.pins[t] = 0;
+      w.last_access[t] = 0;
+      w.taddr[t] = 0;
+    }
+    if (threadIdx.x == 0) {
+      sh.cur = 0;
+      sh.nb = 1;
+      sh.addr[0][0] = 0;
+      sh.size[0][0] = budget;
+      sh.owner[0][0] = kFree;
+      sh.bytes_free = budget;
+      sh.clock = 0;
+      sh.status = COOP_OK;
+      sh.cur_op = -1;
+      sh.redpar = 0;
+      sh.pev = 0;
+      memset(&sh.res, 0, sizeof(sh.res));
+      sh.res.fail_op = -1;
+      sh.res.digest = 0x9E3779B97F4A7C15ull;
+      sh.res.budget = budget;
+      sh.res.max_blocks = 1;
+    }
+    epoch = w.epochs[threadIdx.x];
+    __syncthreads();
+    // parameters to the two ends (R15)
+    {
+      uint64_t lb = 0, rb = 0;
+      for (int j = 0; j < tr.n_params && ok(); ++j) {
+        const int t = tr.params[j];
+        const bool right = (a.flags & COOP_F_INPLACE) ? (rb < lb) : false;
+        const int i = find_fit(tr.size[t], right);
+        if (i < 0) {
+          if (threadIdx.x == 0) sh.status = COOP_ERR_UNSATISFIABLE;
+          __syncthreads();
+          break;
+        }
+        const uint64_t at = place(i, tr.size[t], right, t);
+        if (!ok()) break;
+        if (right) rb += tr.size[t];
+        else lb += tr.size[t];
+        if (threadIdx.x == 0) {
+          w.taddr[t] = at;
+          sh.tfl[t] = TF_RES | TF_BORN;
+          log_ev(0, -1, t, at);
+        }
+        __syncthreads();
+      }
+    }
+    for (int k = 0; k < M && ok(); ++k) {
+      const int n = nin(k), o = tr.out[k], src = tr.src[k];
+      if (threadIdx.x == 0) {
+        sh.cur_op = k;
+        sh.ntrans = 0;
+      }
+      for (int j = threadIdx.x; j < n; j += kThreads) atomicAdd(&w.pins[in_at(k, j)], 1);
+      for (int j = tr.lock_ptr[k] + threadIdx.x; j < tr.lock_ptr[k + 1]; j += kThreads)
+        sh.tfl[tr.lock_idx[j]] |= TF_LOCK;  // R36
+      __syncthreads();
+      for (int j = 0; j < n && ok(); ++j) {
+        const int u = in_at(k, j);
+        const bool res = sh.tfl[u] & TF_RES;
+        __syncthreads();
+        if (!res) materialize(u);
+      }
+      for (int j = tr.lock_ptr[k]; j < tr.lock_ptr[k + 1] && ok(); ++j) {
+        const int u = tr.lock_idx[j];
+        const bool res = sh.tfl[u] & TF_RES;
+        __syncthreads();
+        if (!res) materialize(u);
+      }
+      if (!ok()) break;
+      allocate(k, o, true, 1);
+      if (!ok()) break;
+      if (threadIdx.x == 0) {
+        sh.tfl[o] |= TF_BORN;
+        sh.clock += tr.cost[k];
+        sh.res.base_us += tr.cost[k];
+        sh.res.total_us += tr.cost[k];
+        log_ev(6, k, o, w.taddr[o]);
+      }
+      __syncthreads();
+      const int64_t clk = sh.clock;
+      for (int j = threadIdx.x; j < n; j += kThreads) {
+        const int u = in_at(k, j);
+        w.last_access[u] = clk;
+        atomicSub(&w.pins[u], 1);
+      }
+      if (threadIdx.x == 0) w.last_access[o] = clk;
+      __syncthreads();
+      // deaths after op k (R20) merged with transient dead recomputes (R22), ascending id
+      if (threadIdx.x == 0) {
+        for (int j = tr.die_ptr[k]; j < tr.die_ptr[k + 1]; ++j) sh.tfl[tr.die_idx[j]] |= TF_DEAD;
+        // insertion-sort the transient list (small) and merge with the (sorted) die list
+        int *tl = w.trans;
+        const int nt = sh.ntrans;
+        for (int x = 1; x < nt; ++x) {
+          const int v = tl[x];
+          int y = x - 1;
+          while (y >= 0 && tl[y] > v) { tl[y + 1] = tl[y]; --y; }
+          tl[y + 1] = v;
+        }
+      }
+      __syncthreads();
+      {
+        int pd = tr.die_ptr[k];
+        const int pe = tr.die_ptr[k + 1];
+        int pt = 0;
+        const int nt = sh.ntrans;
+        int last = -1;
+        while (pd < pe || pt < nt) {
+          int t;
+          if (pt >= nt || (pd < pe && tr.die_idx[pd] <= w.trans[pt])) t = tr.die_idx[pd++];
+          else t = w.trans[pt++];
+          if (t == last) continue;
+          last = t;
+          const uint8_t f = sh.tfl[t];
+          const bool keep = tr.unevict[t] && t != src;
+          __syncthreads();
+          if ((f & TF_DEAD) && (f & TF_RES) && !keep) free_tensor(t);
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      sh.res.status = sh.status;
+      if (sh.status != COOP_OK && sh.res.fail_op < 0 && sh.cur_op >= 0) sh.res.fail_op = sh.cur_op;
+    }
+    w.epochs[threadIdx.x] = epoch;
+    __syncthreads();
+  }
+};
+
+// Per-cell workspace layout for T tensors (host).
+WsLayout make_layout(int T) {
+  WsLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = (o + bytes + 255) / 256 * 256;
+    return r;
+  };
+  L.tflags = take((size_t)T);
+  L.pins = take((size_t)T * 4);
+  L.last_access = take((size_t)T * 8);
+  L.taddr = take((size_t)T * 8);
+  L.epochs = take((size_t)kThreads * 4);
+  L.marks = take((size_t)kThreads * T * 4);
+  L.isz = take((size_t)(kCap + 1) * 8);
+  L.ih = take((size_t)(kCap + 1) * 8);
+  L.ist = take((size_t)(kCap + 1));
+  L.S = take((size_t)(kCap + 1 + kThreads) * 8);
+  L.H = take((size_t)(kCap + 1 + kThreads) * sizeof(U192));
+  L.B = take((size_t)(kCap + 1 + kThreads) * 4);
+  L.trans = take((size_t)T * 4 * 4);
+  L.victims = take((size_t)kCap * 4);
+  L.memoA = take((size_t)T * 8);
+  L.memoD = take((size_t)T * 8);
+  L.bytes = o;
+  return L;
+}
+
+}  // namespace
+}  // namespace coop

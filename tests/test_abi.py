@@ -71,3 +71,25 @@ def test_cuda_exact_sum_arithmetic_on_host():
         cases.append([b] + [v for v in extra if v >= 2.0 ** -64])
     for xs in cases:
         assert coop._fixed_round_sum_host(np.array(xs, np.float64)) == math.fsum(xs), xs
+
+
+def test_pool_argument_checks_without_gpu():
+    """coop_pool_init validates its config, and every online call rejects a NULL pool,
+    before touching the device."""
+    from paper_2311_00591_b200 import coop
+    lib = coop.lib
+    h = ctypes.c_void_p()
+    assert lib.coop_pool_init(None, ctypes.byref(h)) == coop.ERR_INVALID_ARG
+    for cfg in [coop.PoolConfig(0, 0, 0, 16, 16), coop.PoolConfig(100, 8, 0, 16, 16),
+                coop.PoolConfig(100, 0, 0, 0, 16), coop.PoolConfig(100, 0, 0, 16385, 16),
+                coop.PoolConfig(100, 0, 0, 16, -1)]:
+        assert lib.coop_pool_init(ctypes.byref(cfg), ctypes.byref(h)) == coop.ERR_INVALID_ARG
+    assert lib.coop_alloc(None, 1, 1, 0, -1, None, 0, None, None, 0) == coop.ERR_INVALID_ARG
+    assert lib.coop_free(None, 0) == coop.ERR_INVALID_ARG
+    assert lib.coop_access(None, 0, 0) == coop.ERR_INVALID_ARG
+    assert lib.coop_rematerialize(None, 0, None, None, 0) == coop.ERR_INVALID_ARG
+    assert lib.coop_pool_stats(None, None) == coop.ERR_INVALID_ARG
+    n = ctypes.c_int32()
+    assert lib.coop_pool_layout(None, None, None, None, 0, ctypes.byref(n)) == coop.ERR_INVALID_ARG
+    assert lib.coop_pool_destroy(None) == coop.ERR_INVALID_ARG
+    assert coop.ALLOC_RESULT_DTYPE.itemsize == 56
