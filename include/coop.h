@@ -275,7 +275,7 @@ int coop_pool_destroy(coop_pool_t pool);
  * state change), COOP_ERR_UNSATISFIABLE (no window exists; no tensor is created),
  * COOP_ERR_INVALID_ARG (size outside [1, 2^48), cost >= 2^40, bad flags, bad in-place
  * source), COOP_ERR_UNKNOWN_ID (a parent id never allocated), COOP_ERR_NOMEM (capacity,
- * or a block table beyond 2048 blocks), COOP_ERR_CUDA.
+ * or a block table beyond 4096 blocks), COOP_ERR_CUDA.
  */
 int coop_alloc(coop_pool_t pool, uint64_t size, uint64_t cost_us, uint32_t op_flags,
                int64_t inplace_src, const int64_t *parents, int32_t n_parents,

@@ -31,7 +31,6 @@ struct PoolState {
   uint64_t addr[kCap + 2], size[kCap + 2];
   int32_t owner[kCap + 2];
   int32_t nb, n_tensors, n_edges;
-  uint32_t pev;
   uint64_t bytes_free;
   int64_t clock;
   coop_replay_result res;
@@ -46,7 +45,8 @@ struct GraphMut {
   int32_t *out, *src;
   uint8_t *phase, *cls;
   int32_t *in_ptr, *in_idx;
-  int32_t *cons_head, *cons_next, *cons_op;
+  int32_t *cons_head, *cons_next, *cons_out;
+  int4 *rec;
 };
 
 // mapped pinned host memory shared by the host and the call's CTA
@@ -93,7 +93,6 @@ __global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
     sh.status = COOP_OK;
     sh.cur_op = t;
     sh.redpar = 0;
-    sh.pev = P.pev;
     sh.res = P.res;
     sh.win_first = sh.win_last = -1;
     sh.nvict = 0;
@@ -123,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
         g.src[t] = (pa.op_flags & COOP_OP_INPLACE) ? pa.src : -1;
         g.phase[t] = (pa.op_flags & COOP_OP_PHASE_FWD) ? COOP_PHASE_FWD : COOP_PHASE_BWD;
         g.cls[t] = (pa.op_flags & COOP_OP_EXPENSIVE) ? 1 : (pa.op_flags & COOP_OP_CHEAP) ? 2 : 0;
+        g.rec[t] = make_int4((int)(uint32_t)(uint64_t)pa.cost, (int)(uint32_t)((uint64_t)pa.cost >> 32), e0, e0 + np);
         g.unevict[t] = ((pa.op_flags & COOP_OP_UNEVICTABLE) || (g.src[t] >= 0 && g.unevict[g.src[t]])) ? 1 : 0;
         sh.tfl[t] = 0;
         c.w.pins[t] = 0;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
           if (pa.kind == PK_ALLOC && tid == 0) {  // link the op into its parents' consumer lists
             for (int j = 0; j < np; ++j) {
               const int e = P.n_edges + j;
-              g.cons_op[e] = t;
+              g.cons_out[e] = t;  // out[t] == t
               g.cons_next[e] = g.cons_head[par[j]];
               g.cons_head[par[j]] = e;
             }
@@ -243,7 +243,6 @@ __global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
     P.nb = nb1;
     P.bytes_free = sh.bytes_free;
     P.clock = sh.clock;
-    P.pev = sh.pev;
     P.res = sh.res;
   }
   c.w.epochs[tid] = c.epoch;
@@ -362,7 +361,8 @@ extern "C" int coop_pool_init(const coop_pool_config *cfg, coop_pool_t *out) {
                o_cost = take((size_t)T * 8), o_out = take((size_t)T * 4), o_src = take((size_t)T * 4),
                o_phase = take((size_t)T), o_cls = take((size_t)T), o_inp = take((size_t)(T + 1) * 4),
                o_ini = take((size_t)(E + 1) * 4), o_ch = take((size_t)T * 4),
-               o_cn = take((size_t)(E + 1) * 4), o_co = take((size_t)(E + 1) * 4);
+               o_cn = take((size_t)(E + 1) * 4), o_co = take((size_t)(E + 1) * 4),
+               o_rec = take((size_t)T * 16);
   int rc = COOP_OK;
   if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&p->d_ps, sizeof(PoolState)) != cudaSuccess || cudaMalloc(&p->d_graph, off) != cudaSuccess) {
@@ -396,7 +396,8 @@ extern "C" int coop_pool_init(const coop_pool_config *cfg, coop_pool_t *out) {
   g.in_idx = (int32_t *)(b + o_ini);
   g.cons_head = (int32_t *)(b + o_ch);
   g.cons_next = (int32_t *)(b + o_cn);
-  g.cons_op = (int32_t *)(b + o_co);
+  g.cons_out = (int32_t *)(b + o_co);
+  g.rec = (int4 *)(b + o_rec);
   TraceDev &td = p->td;
   td.T = T;
   td.M = T;
@@ -412,7 +413,8 @@ extern "C" int coop_pool_init(const coop_pool_config *cfg, coop_pool_t *out) {
   td.in_idx = g.in_idx;
   td.cons_head = g.cons_head;
   td.cons_next = g.cons_next;
-  td.cons_op = g.cons_op;
+  td.cons_out = g.cons_out;
+  td.rec = g.rec;
   td.cls = g.cls;
   // initial state: one free block [0, budget)
   PoolState *h = new (std::nothrow) PoolState();

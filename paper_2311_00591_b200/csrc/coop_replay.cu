@@ -54,7 +54,8 @@ struct coop_trace_s {
   std::vector<int64_t> cost;
   std::vector<uint8_t> phase;
   std::vector<int32_t> cons_ptr, cons_idx, lock_ptr, lock_idx, die_ptr, die_idx;
-  std::vector<int32_t> cons_head, cons_next;  // the CSR as linked lists (device layout)
+  std::vector<int32_t> cons_head, cons_next, cons_out;  // the CSR as linked lists (device layout)
+  std::vector<int32_t> rec;  // per tensor {cost lo, cost hi, in_beg, in_end} (device layout)
   void *dev = nullptr;
   TraceDev td{};
   unsigned char *ws = nullptr;
@@ -122,6 +123,17 @@ int validate_and_prepare(coop_trace_s &t) {
   }
   t.cons_head.assign(T, -1);
   t.cons_next.assign(t.cons_idx.size(), -1);
+  t.cons_out.assign(t.cons_idx.size(), 0);
+  for (size_t e = 0; e < t.cons_idx.size(); ++e) t.cons_out[e] = t.out[t.cons_idx[e]];
+  t.rec.assign((size_t)T * 4, 0);
+  for (int i = 0; i < T; ++i) {
+    const int p = t.producer[i];
+    const uint64_t c = p >= 0 ? (uint64_t)t.cost[p] : 0ull;
+    t.rec[(size_t)i * 4 + 0] = (int32_t)(uint32_t)c;
+    t.rec[(size_t)i * 4 + 1] = (int32_t)(uint32_t)(c >> 32);
+    t.rec[(size_t)i * 4 + 2] = p >= 0 ? t.in_ptr[p] : -1;
+    t.rec[(size_t)i * 4 + 3] = p >= 0 ? t.in_ptr[p + 1] : -1;
+  }
   for (int i = 0; i < T; ++i) {
     if (t.cons_ptr[i + 1] > t.cons_ptr[i]) t.cons_head[i] = t.cons_ptr[i];
     for (int j = t.cons_ptr[i]; j + 1 < t.cons_ptr[i + 1]; ++j) t.cons_next[j] = j + 1;
@@ -200,7 +212,7 @@ static int upload_trace(coop_trace_s *t) {
   const size_t o_size = put(blob, t->size), o_prod = put(blob, t->producer), o_unev = put(blob, t->unevict),
                o_cost = put(blob, t->cost), o_out = put(blob, t->out), o_src = put(blob, t->src),
                o_phase = put(blob, t->phase), o_inp = put(blob, t->in_ptr), o_ini = put(blob, t->in_idx),
-               o_cp = put(blob, t->cons_head), o_cn = put(blob, t->cons_next), o_ci = put(blob, t->cons_idx), o_lp = put(blob, t->lock_ptr),
+               o_cp = put(blob, t->cons_head), o_cn = put(blob, t->cons_next), o_ci = put(blob, t->cons_out), o_rec = put(blob, t->rec), o_lp = put(blob, t->lock_ptr),
                o_li = put(blob, t->lock_idx), o_dp = put(blob, t->die_ptr), o_di = put(blob, t->die_idx),
                o_par = put(blob, t->params);
   cudaGetDevice(&t->device);
@@ -229,7 +241,8 @@ static int upload_trace(coop_trace_s *t) {
   td.in_idx = (const int32_t *)(b + o_ini);
   td.cons_head = (const int32_t *)(b + o_cp);
   td.cons_next = (const int32_t *)(b + o_cn);
-  td.cons_op = (const int32_t *)(b + o_ci);
+  td.cons_out = (const int32_t *)(b + o_ci);
+  td.rec = (const int4 *)(b + o_rec);
   td.cls = nullptr;
   td.lock_ptr = (const int32_t *)(b + o_lp);
   td.lock_idx = (const int32_t *)(b + o_li);

@@ -18,12 +18,10 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kCap = 2048;       // blocks per pool held by the kernel (COOP_ERR_NOMEM beyond)
+constexpr int kCap = 4096;       // blocks per pool held by the kernel (COOP_ERR_NOMEM beyond)
 constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
-constexpr int kDfsCap = 512;     // per-thread DFS stack (projected-cost closures)
 constexpr int kFree = -1;
 constexpr int kMaxT = 16384;     // tensors per trace whose flags live in shared memory
-constexpr int kVisCap = 64;      // per-thread DFS visited set in shared memory (power of 2)
 
 enum : uint8_t { TF_RES = 1, TF_BORN = 2, TF_DEAD = 4, TF_LOCK = 8 };
 
@@ -38,9 +36,13 @@ struct TraceDev {
   const uint8_t *phase;
   const int32_t *in_ptr, *in_idx;
   // consumers as singly linked edge lists (the online pool appends edges as tensors
-  // are created): the ops reading x are cons_op[e] for e = cons_head[x], cons_next[e], ...
-  // until -1
-  const int32_t *cons_head, *cons_next, *cons_op;
+  // are created): the OUTPUTS of the ops reading x are cons_out[e] for e = cons_head[x],
+  // cons_next[e], ... until -1
+  const int32_t *cons_head, *cons_next, *cons_out;
+  // per tensor, packed for the projected-cost DFS (one 16-byte load per visited node):
+  // {cost of its producer (lo, hi words), producer's inputs [in_beg, in_end) of in_idx};
+  // in_beg = -1 for tensors without a producer (parameters)
+  const int4 *rec;
   const uint8_t *cls;  // per op: 0 = class by threshold (R14), 1 = C1, 2 = C2; NULL = all 0
   const int32_t *lock_ptr, *lock_idx;
   const int32_t *die_ptr, *die_idx;
@@ -48,7 +50,7 @@ struct TraceDev {
 };
 
 struct WsLayout {  // byte offsets inside one cell's workspace
-  size_t tflags, pins, last_access, taddr, epochs, marks, isz, ih, ist, S, H, B, trans, victims, memoA, memoD;
+  size_t tflags, pins, last_access, taddr, epochs, marks, stack, isz, ih, ist, S, H, B, trans, victims, cand;
   size_t bytes;
 };
 
@@ -58,6 +60,7 @@ struct CellPtrs {
   int64_t *last_access;
   uint64_t *taddr;
   uint32_t *epochs, *marks;
+  int32_t *stack;
   uint64_t *isz;
   double *ih;
   uint8_t *ist;
@@ -65,7 +68,7 @@ struct CellPtrs {
   U192 *H;
   int32_t *B;
   int32_t *trans, *victims;
-  uint64_t *memoA, *memoD;
+  int32_t *cand;
 };
 
 struct KArgs {
@@ -86,7 +89,6 @@ struct Shared {
   uint64_t size[2][kCap + 2];
   int32_t owner[2][kCap + 2];
   uint8_t tfl[kMaxT];          // per-tensor flags TF_*
-  uint32_t vis[kThreads][kVisCap];  // per-thread open-addressing set of visited tensors (DFS)
   uint64_t wS[kWarps];
   U192 wH[kWarps];
   int32_t wB[kWarps];
@@ -108,7 +110,7 @@ struct Shared {
   int32_t red32[2][kWarps];
   U192 red192[kWarps];
   int32_t redpar;
-  uint32_t pev;  // pressure-event epoch of the projected-cost memo
+  int32_t ncand, cand_next;  // projected-cost work list of the current pressure event
   // the last evicted window (read by the online calls): items, span, cost bits, victims
   int32_t win_first, win_last, nvict;
   uint64_t win_span, win_cost;
@@ -186,6 +188,7 @@ struct Cell {
     w.taddr = (uint64_t *)(base + a.lay.taddr);
     w.epochs = (uint32_t *)(base + a.lay.epochs);
     w.marks = (uint32_t *)(base + a.lay.marks);
+    w.stack = (int32_t *)(base + a.lay.stack);
     w.isz = (uint64_t *)(base + a.lay.isz);
     w.ih = (double *)(base + a.lay.ih);
     w.ist = (uint8_t *)(base + a.lay.ist);
@@ -194,8 +197,7 @@ struct Cell {
     w.B = (int32_t *)(base + a.lay.B);
     w.trans = (int32_t *)(base + a.lay.trans);
     w.victims = (int32_t *)(base + a.lay.victims);
-    w.memoA = (uint64_t *)(base + a.lay.memoA);
-    w.memoD = (uint64_t *)(base + a.lay.memoD);
+    w.cand = (int32_t *)(base + a.lay.cand);
     log = a.log ? a.log + (size_t)cell * a.log_cap : nullptr;
   }
 
@@ -333,191 +335,101 @@ struct Cell {
     return !is_c1(op);
   }
 
-  // c(t) = producer cost + the SET of non-resident ancestors reachable through
-  // non-resident tensors + the SET of evicted descendants reachable through evicted
-  // tensors (R18).  One thread; visited marks = per-thread epochs.
   // ---------------- projected cost c(t) (R18) --------------------
   // c(t) = cost(producer(t)) + cost of Anc(t) + cost of Desc(t) where
   //   Anc(t)  = the SET of non-resident tensors reachable upward from t's inputs through
   //             non-resident tensors (parameters stop),
   //   Desc(t) = the SET of evicted live tensors reachable downward from t's consumers'
   //             outputs through evicted live tensors.
-  // Within one pressure event residency is fixed, so the closures of single-entry chains
-  // are memoized: Up*(u) = {u} U Up*(v) when v is u's only non-resident input (disjoint in
-  // a DAG), likewise Down*; nodes with two or more entries get an exact set-closure DFS.
-  // Memo words: (event epoch << 40) | value (values >= 2^40 are not memoized).
-  __device__ __forceinline__ bool up_ok(int u) const {  // non-resident, recomputable
-    return !(sh.tfl[u] & TF_RES) && __ldg(&tr.producer[u]) >= 0;
-  }
+  // All candidates of a pressure event are evaluated by ONE flat loop per thread: each
+  // iteration either starts the next candidate (fetched from a shared counter, so threads
+  // stay busy whatever the closure sizes), switches a candidate from its ancestors to its
+  // descendants, or pops one DFS node.  No nested data-dependent loops, so the lanes of a
+  // warp stay converged while their closures differ in size.  Visited marks: per-thread
+  // epoch words in global memory (one epoch per candidate).
   __device__ __forceinline__ bool down_ok(int d) const {  // evicted and live
     const uint8_t f = sh.tfl[d];
     return (f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD);
   }
-  __device__ __forceinline__ bool memo_get(const uint64_t *m, int x, int64_t &v) const {
-    const uint64_t w_ = ((volatile const uint64_t *)m)[x];
-    if ((uint32_t)(w_ >> 40) != sh.pev) return false;
-    v = (int64_t)(w_ & ((1ull << 40) - 1ull));
-    return true;
-  }
-  __device__ __forceinline__ void memo_put(uint64_t *m, int x, int64_t v) const {
-    if (v >= 0 && v < (1ll << 40)) ((volatile uint64_t *)m)[x] = ((uint64_t)sh.pev << 40) | (uint64_t)v;
+  static __device__ __forceinline__ int64_t rec_cost(const int4 r) {
+    return (int64_t)(((uint64_t)(uint32_t)r.y << 32) | (uint32_t)r.x);
   }
 
-  // exact set closure by DFS: UP = ancestors through up_ok, else descendants through
-  // down_ok; roots = x itself (NEIGH false) or x's inputs / consumer outputs (NEIGH true);
-  // returns the summed producer costs of the set
-  template <bool UP, bool NEIGH>
-  __device__ int64_t closure_dfs(int x0, bool &overflow) {
-    uint32_t *vs = sh.vis[threadIdx.x];
-    for (int k = 0; k < kVisCap; ++k) vs[k] = 0u;
-    int nvis = 0;
-    bool use_marks = false;
+  // cand[0..ncand): block indices of EVICTABLE items; writes w.ih[b] = RN(c(t) / s(t)).
+  // A node is marked when pushed, so every node enters a candidate's stack at most once:
+  // the per-thread stack (global workspace, T entries) cannot overflow.
+  __device__ void projected_costs(const int32_t *cand, int ncand) {
     uint32_t *mk = w.marks + (size_t)threadIdx.x * tr.T;
+    int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
+    int sp = 0, ci = -1, t = -1, stage = 0;
+    int64_t acc = 0;
     uint32_t ep = 0;
-    auto seen = [&](int x) -> bool {  // test-and-insert
-      if (use_marks) {
-        if (mk[x] == ep) return true;
-        mk[x] = ep;
-        return false;
-      }
-      uint32_t hsh = ((uint32_t)x * 2654435761u) & (kVisCap - 1);
-      while (true) {
-        const uint32_t k = vs[hsh];
-        if (k == (uint32_t)x + 1u) return true;
-        if (k == 0u) break;
-        hsh = (hsh + 1) & (kVisCap - 1);
-      }
-      vs[hsh] = (uint32_t)x + 1u;
-      ++nvis;
-      return false;
-    };
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      if (attempt == 1) {
-        use_marks = true;
-        ep = ++epoch;
-      }
-      int64_t c = 0;
-      bool full = false;
-      int stk[kDfsCap];
-      int sp = 0;
-      if (!NEIGH) {
-        stk[sp++] = x0;
-      } else if (UP) {
-        const int p0 = __ldg(&tr.producer[x0]);
-        for (int j = __ldg(&tr.in_ptr[p0]); j < __ldg(&tr.in_ptr[p0 + 1]); ++j) {
-          if (sp == kDfsCap) { overflow = true; return c; }
-          stk[sp++] = __ldg(&tr.in_idx[j]);
-        }
-      } else {
-        for (int e = __ldg(&tr.cons_head[x0]); e >= 0; e = __ldg(&tr.cons_next[e])) {
-          if (sp == kDfsCap) { overflow = true; return c; }
-          stk[sp++] = __ldg(&tr.out[__ldg(&tr.cons_op[e])]);
-        }
-      }
-      while (sp > 0) {
-        const int x = stk[--sp];
-        if (UP ? !up_ok(x) : !down_ok(x)) continue;
-        if (!use_marks && nvis >= kVisCap / 2) { full = true; break; }
-        if (seen(x)) continue;
-        const int px = __ldg(&tr.producer[x]);
-        c += __ldg(&tr.cost[px]);
-        if (UP) {
-          for (int j = __ldg(&tr.in_ptr[px]); j < __ldg(&tr.in_ptr[px + 1]); ++j) {
-            if (sp == kDfsCap) { overflow = true; return c; }
-            stk[sp++] = __ldg(&tr.in_idx[j]);
-          }
-        } else {
-          for (int e = __ldg(&tr.cons_head[x]); e >= 0; e = __ldg(&tr.cons_next[e])) {
-            if (sp == kDfsCap) { overflow = true; return c; }
-            stk[sp++] = __ldg(&tr.out[__ldg(&tr.cons_op[e])]);
-          }
-        }
-      }
-      if (!full) return c;
-    }
-    return 0;
-  }
-
-  // entries of x: its non-resident inputs (UP) or its evicted live consumer outputs (down)
-  template <bool UP>
-  __device__ __forceinline__ int entries(int x, int *buf, int cap) const {
-    int k = 0;
-    if (UP) {
-      const int px = __ldg(&tr.producer[x]);
-      for (int j = __ldg(&tr.in_ptr[px]); j < __ldg(&tr.in_ptr[px + 1]); ++j) {
-        const int u = __ldg(&tr.in_idx[j]);
-        if (up_ok(u)) {
-          bool dup = false;
-          for (int q = 0; q < min(k, cap); ++q) dup |= (buf[q] == u);
-          if (!dup) {
-            if (k < cap) buf[k] = u;
-            ++k;
-          }
-        }
-      }
-    } else {
-      for (int e = __ldg(&tr.cons_head[x]); e >= 0; e = __ldg(&tr.cons_next[e])) {
-        const int d = __ldg(&tr.out[__ldg(&tr.cons_op[e])]);
-        if (down_ok(d)) {
-          bool dup = false;
-          for (int q = 0; q < min(k, cap); ++q) dup |= (buf[q] == d);
-          if (!dup) {
-            if (k < cap) buf[k] = d;
-            ++k;
-          }
-        }
-      }
-    }
-    return k;
-  }
-
-  // cost of the closure of node x (x itself included; x satisfies up_ok / down_ok)
-  template <bool UP>
-  __device__ int64_t node_closure(int x0, bool &overflow) {
-    uint64_t *memo = UP ? w.memoA : w.memoD;
-    int chain[64];
-    int nch = 0;
-    int x = x0;
-    int64_t base = 0;
     while (true) {
-      int64_t mv;
-      if (memo_get(memo, x, mv)) {
-        base = mv;
-        break;
-      }
-      int buf[4];
-      const int k = entries<UP>(x, buf, 4);
-      if (k == 1 && nch < 64) {  // single entry: Up*(x) = {x} U Up*(entry)
-        chain[nch++] = x;
-        x = buf[0];
+      if (sp == 0) {
+        if (ci >= 0 && stage == 0) {  // ancestors done: the descendants' roots
+          stage = 1;
+          for (int e = __ldg(&tr.cons_head[t]); e >= 0; e = __ldg(&tr.cons_next[e])) {
+            const int y = __ldg(&tr.cons_out[e]);
+            if (mk[y] != ep) {
+              mk[y] = ep;
+              stk[sp++] = y;
+            }
+          }
+          if (sp > 0) continue;
+        }
+        if (ci >= 0) {
+          const int b = cand[ci];
+          int64_t s = sh.clock - w.last_access[t];  // staleness (R17)
+          if (s < 1) s = 1;
+          w.ih[b] = __ddiv_rn((double)acc, (double)s);  // h = c/s (R1)
+        }
+        ci = atomicAdd(&sh.cand_next, 1);
+        if (ci >= ncand) break;
+        t = O()[cand[ci]];
+        const int4 r = __ldg(&tr.rec[t]);
+        acc = rec_cost(r);
+        ep = ++epoch;
+        if (ep == 0) {  // epoch wrap: clear this thread's marks (never in practice)
+          for (int x = 0; x < tr.T; ++x) mk[x] = 0u;
+          ep = epoch = 1;
+        }
+        mk[t] = ep;
+        stage = 0;
+        for (int j = r.z; j < r.w; ++j) {
+          const int y = __ldg(&tr.in_idx[j]);
+          if (mk[y] != ep) {
+            mk[y] = ep;
+            stk[sp++] = y;
+          }
+        }
         continue;
       }
-      if (k == 0) {
-        base = __ldg(&tr.cost[__ldg(&tr.producer[x])]);
+      const int x = stk[--sp];
+      const uint8_t f = sh.tfl[x];
+      const int4 r = __ldg(&tr.rec[x]);
+      // ancestors: non-resident and recomputable; descendants: evicted and live
+      const bool ok = stage == 0 ? (!(f & TF_RES) && r.z >= 0)
+                                 : ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD));
+      if (!ok) continue;
+      acc += rec_cost(r);
+      if (stage == 0) {
+        for (int j = r.z; j < r.w; ++j) {
+          const int y = __ldg(&tr.in_idx[j]);
+          if (mk[y] != ep) {
+            mk[y] = ep;
+            stk[sp++] = y;
+          }
+        }
       } else {
-        base = closure_dfs<UP, false>(x, overflow);  // two or more entries: exact set closure
+        for (int e = __ldg(&tr.cons_head[x]); e >= 0; e = __ldg(&tr.cons_next[e])) {
+          const int y = __ldg(&tr.cons_out[e]);
+          if (mk[y] != ep) {
+            mk[y] = ep;
+            stk[sp++] = y;
+          }
+        }
       }
-      memo_put(memo, x, base);
-      break;
     }
-    while (nch > 0) {
-      const int y = chain[--nch];
-      base += __ldg(&tr.cost[__ldg(&tr.producer[y])]);
-      memo_put(memo, y, base);
-    }
-    return base;
-  }
-
-  __device__ int64_t projected_cost(int t, bool &overflow) {
-    int64_t c = __ldg(&tr.cost[__ldg(&tr.producer[t])]);
-    int buf[4];
-    const int ka = entries<true>(t, buf, 4);
-    if (ka == 1) c += node_closure<true>(buf[0], overflow);
-    else if (ka > 1) c += closure_dfs<true, true>(t, overflow);
-    const int kd = entries<false>(t, buf, 4);
-    if (kd == 1) c += node_closure<false>(buf[0], overflow);
-    else if (kd > 1) c += closure_dfs<false, true>(t, overflow);
-    return c;
   }
 
   // ---------------------------------------------------------------- Sec. 3.3 search
@@ -528,10 +440,8 @@ struct Cell {
   __device__ bool evict_window(uint64_t need) {
     const uint64_t t0 = gtimer();
     if (threadIdx.x == 0) {
-      if (++sh.pev >= (1u << 24)) {  // epoch wrap: clear the memo (never in practice)
-        sh.pev = 1;
-        for (int t = 0; t < tr.T; ++t) w.memoA[t] = w.memoD[t] = 0ull;
-      }
+      sh.ncand = 0;
+      sh.cand_next = 0;
     }
     __syncthreads();
     const int nb = sh.nb, nx = sh.cur ^ 1;
@@ -544,30 +454,32 @@ struct Cell {
     const int chunk = (nb + kThreads - 1) / kThreads;
     const int b0 = min(nb, (int)threadIdx.x * chunk), b1 = min(nb, b0 + chunk);
     int nev = 0;
-    bool overflow = false;
-    uint64_t ls = 0;
-    U192 lh = u192_zero();
-    int lb = 0;
     for (int b = b0; b < b1; ++b) {
       const int o = O()[b];
       int st;
-      double h = 0.0;
       if (o == kFree) {
         st = COOP_FREE;
       } else if (__ldg(&tr.unevict[o]) || w.pins[o] > 0 || (sh.tfl[o] & TF_LOCK)) {
         st = COOP_PINNED;
       } else {
         st = COOP_EVICTABLE;
-        int64_t s = sh.clock - w.last_access[o];  // staleness (R17)
-        if (s < 1) s = 1;
-        h = __ddiv_rn((double)projected_cost(o, overflow), (double)s);
+        w.cand[atomicAdd(&sh.ncand, 1)] = b;
         ++nev;
       }
-      w.ih[b] = h;
+      w.ih[b] = 0.0;
       St[b] = st;
+    }
+    __syncthreads();
+    projected_costs(w.cand, sh.ncand);
+    __syncthreads();
+    uint64_t ls = 0;
+    U192 lh = u192_zero();
+    int lb = 0;
+    for (int b = b0; b < b1; ++b) {
+      const double h = w.ih[b];
       ls += Z()[b];
       lh = u192_add(lh, u192_from_double(h));
-      lb += (st == COOP_PINNED);
+      lb += (St[b] == COOP_PINNED);
     }
     // exclusive scans of the thread totals: warp shuffles, then the <= 8 warp totals
     uint64_t is = ls;
@@ -593,11 +505,6 @@ struct Cell {
       sh.wB[warp] = ib;
     }
     nev = cta_sum_i32(sh, nev);  // (its barrier also publishes the warp totals)
-    if (cta_max_i32(sh, overflow ? 1 : 0)) {
-      if (threadIdx.x == 0) sh.status = COOP_ERR_NOMEM;
-      __syncthreads();
-      return false;
-    }
     uint64_t cs = is - ls;  // exclusive within the warp
     U192 ch = u192_sub(ih, lh);
     int cb = ib - lb;
@@ -852,8 +759,6 @@ struct Cell {
   __device__ void run(uint64_t budget) {
     const int T = tr.T, M = tr.M;
     for (int t = threadIdx.x; t < T; t += kThreads) {
-      w.memoA[t] = 0ull;
-      w.memoD[t] = 0ull;
       sh.tfl[t] = 0;
       w.pins[t] = 0;
       w.last_access[t] = 0;
@@ -870,7 +775,6 @@ struct Cell {
       sh.status = COOP_OK;
       sh.cur_op = -1;
       sh.redpar = 0;
-      sh.pev = 0;
       memset(&sh.res, 0, sizeof(sh.res));
       sh.res.fail_op = -1;
       sh.res.digest = 0x9E3779B97F4A7C15ull;
@@ -1001,6 +905,7 @@ WsLayout make_layout(int T) {
   L.taddr = take((size_t)T * 8);
   L.epochs = take((size_t)kThreads * 4);
   L.marks = take((size_t)kThreads * T * 4);
+  L.stack = take((size_t)kThreads * T * 4);
   L.isz = take((size_t)(kCap + 1) * 8);
   L.ih = take((size_t)(kCap + 1) * 8);
   L.ist = take((size_t)(kCap + 1));
@@ -1009,8 +914,7 @@ WsLayout make_layout(int T) {
   L.B = take((size_t)(kCap + 1 + kThreads) * 4);
   L.trans = take((size_t)T * 4 * 4);
   L.victims = take((size_t)kCap * 4);
-  L.memoA = take((size_t)T * 8);
-  L.memoD = take((size_t)T * 8);
+  L.cand = take((size_t)(kCap + 2) * 4);
   L.bytes = o;
   return L;
 }

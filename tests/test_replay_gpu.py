@@ -89,3 +89,16 @@ def test_ablation_flags_dnn():
         for flags in (0, coop.F_INPLACE, coop.F_PARTITION, 7):
             peak = O.peak_live(tr, flags)
             check(tr, [int(peak * 0.6), int(peak * 0.85)], flags, ctx=f"{name} flags {flags}")
+
+
+@pytest.mark.parametrize("name,ks", [("bilstm", (48, 100, 180, 255)), ("inception_v3", (0, 40, 120)),
+                                     ("spos", (0, 64, 200))])
+def test_config5_budget_samples(name, ks):
+    """BASELINE config 5 budgets (k = 0..255 -> 20..100 % of peak): samples including
+    heavily thrashing cells (bilstm k = 48: ~9 K pressure events, projected-cost closures of
+    up to ~2.6 K tensors)."""
+    tr = dnn.dnn(name)
+    flags = O.F_PARTITION | O.F_INPLACE
+    peak = O.peak_live(tr, flags)
+    budgets = [peak * (20 * 255 + 80 * k) // (100 * 255) for k in ks]
+    check(tr, budgets, flags, ctx=f"config5 {name}")

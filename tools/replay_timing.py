@@ -6,7 +6,7 @@ from gen import dnn
 from paper_2311_00591_b200 import coop
 flags = 3
 nb = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-for name in dnn.DNNS:
+for name in (sys.argv[2].split(",") if len(sys.argv) > 2 else dnn.DNNS):
     tr = dnn.dnn(name)
     h = coop.Trace(tr)
     peak = h.peak_live(flags)
