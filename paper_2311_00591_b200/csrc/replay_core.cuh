@@ -413,11 +413,24 @@ struct Cell {
       if (!ok) continue;
       acc += rec_cost(r);
       if (stage == 0) {
-        for (int j = r.z; j < r.w; ++j) {
-          const int y = __ldg(&tr.in_idx[j]);
-          if (mk[y] != ep) {
-            mk[y] = ep;
-            stk[sp++] = y;
+        // inputs in batches of 4: all index loads, then all mark loads, then the pushes
+        // (duplicates inside a batch are skipped explicitly: their marks were read early)
+        for (int j0 = r.z; j0 < r.w; j0 += 4) {
+          int y[4];
+          uint32_t m[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) y[k] = j0 + k < r.w ? __ldg(&tr.in_idx[j0 + k]) : -1;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) m[k] = y[k] >= 0 ? mk[y[k]] : ep;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            bool fresh = m[k] != ep;
+#pragma unroll
+            for (int q = 0; q < k; ++q) fresh &= y[q] != y[k];
+            if (fresh) {
+              mk[y[k]] = ep;
+              stk[sp++] = y[k];
+            }
           }
         }
       } else {
