@@ -541,6 +541,15 @@ __global__ void __launch_bounds__(MAXT, MINB)
 #pragma unroll
           for (int q = 0; q < K; ++q) {
             if (zi != kInfIdx || !((heads >> q) & 1u)) continue;
+            if (q + 1 < K && !((zm >> (q + 1)) & 1u)) {
+              // a one-item run inside the chunk (the common case: FREE items are isolated):
+              // its span is the item's size, from the thread's own prefix registers
+              if (spre[q + 1 < K ? q + 1 : q] - spre[q] >= v.R) {
+                zi = k0 + q;
+                zstop = k0 + q + 1;
+              }
+              continue;
+            }
             const uint32_t mb = barmask >> q, mz = nzmask >> q;
             const int nb = mb ? k0 + q + __ffs(mb) - 1 : nb_right;
             const int nz = mz ? k0 + q + __ffs(mz) - 1 : nz_right;
