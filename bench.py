@@ -297,6 +297,19 @@ def replay_bench(world: int, rank: int, steps: int, with_config5: bool):
             "search_latency_us_max_rank0": float(res["search_ns_max"][ok].max() / 1e3) if ok.any() else None,
             "gpu_launches_per_sweep": len(per),
         }
+    # NEXT-3: minimum / cutoff budgets (R45) of the config-2 and config-3 traces, rank 0 only
+    if rank == 0:
+        for name in ("resnet50", "gpt3_2.7b"):
+            t0 = time.perf_counter()
+            b = coop.budget_search(handles[name], flags, coarse=64, fine=64)
+            dt = time.perf_counter() - t0
+            pk = float(b["peak"])
+            out.setdefault("budgets", {})[name] = {
+                "peak_bytes": int(b["peak"]),
+                "min_budget_frac": (int(b["min_budget"]) / pk) if b["min_status"] == 0 else None,
+                "cutoff_budget_frac": (int(b["cutoff_budget"]) / pk) if b["cutoff_status"] == 0 else None,
+                "replays": int(b["replays"]), "wall_ms": dt * 1e3,
+                "grid": "64 coarse x 64 fine budgets (DESIGN.md R45)"}
     for h in handles.values():
         h.close()
     return out

@@ -206,6 +206,31 @@ int coop_replay_trace(coop_trace_t trace, const uint64_t *budgets, int32_t n_bud
                       coop_stream_t stream);
 
 
+/*
+ * coop_budget_search -- the two budget metrics of Sec. 4.2 and App. C
+ * for one trace, by waves of coop_replay_trace (one CTA per budget):
+ *   min budget    = the smallest budget at which the replay completes (status COOP_OK),
+ *   cutoff budget = the smallest budget at which it completes with zero evictions.
+ * Grid (R45): P = peak_live(flags) (R25); coarse budgets B_k = max(1, floor(P * k / Kc)),
+ * k = 1..Kc; for each metric, k* = the smallest k whose replay satisfies it; then the fine
+ * budgets B_{k*-1} + floor((B_{k*} - B_{k*-1}) * j / Kf), j = 1..Kf (B_0 = 0, budgets
+ * clamped to >= 1), and the result is the smallest fine budget that satisfies it.  A metric
+ * that no coarse budget satisfies gets status COOP_INFEASIBLE and budget 0.  Synchronous;
+ * allocates (and frees) device result buffers.  Kc, Kf in [1, 4096].
+ */
+typedef struct {
+  uint64_t peak;           /* P */
+  uint64_t min_budget;     /* 0 when min_status != COOP_OK */
+  uint64_t cutoff_budget;  /* 0 when cutoff_status != COOP_OK */
+  int32_t min_status, cutoff_status;
+  int32_t replays;         /* replay cells run (coarse + fine waves) */
+  int32_t reserved;
+} coop_budget_result;      /* 40 bytes */
+
+int coop_budget_search(coop_trace_t trace, uint32_t flags, uint32_t class_threshold,
+                       int32_t max_depth, int32_t coarse_steps, int32_t fine_steps,
+                       coop_budget_result *out);
+
 /* ------------------------------------------------------------------ online single pool
  * One memory pool [0, budget) driven call by call by a framework -- the user-facing side of
  * Alg. 1 Allocate(op, size) with the sliding-window eviction of Sec. 3.3

@@ -127,6 +127,16 @@ int orc_replay(const orc_trace *tr, const orc_cfg *cfg, orc_replay_result *res,
 /* Peak of resident bytes in an unbounded, eviction-free replay (R25). */
 uint64_t orc_peak_live(const orc_trace *tr, uint32_t flags);
 
+/* ======================================================================= O4: budget searches
+ * Minimum budget (replay completes) and cutoff budget (completes without eviction) on the
+ * coarse / fine grids of DESIGN.md R45.  TEST INFRASTRUCTURE ONLY. */
+typedef struct {
+  uint64_t peak, min_budget, cutoff_budget;
+  int32_t min_status, cutoff_status, replays, reserved;
+} orc_budget_result;
+int orc_budget_search(const orc_trace *tr, uint32_t flags, uint32_t class_threshold, int32_t max_depth,
+                      int32_t kc, int32_t kf, orc_budget_result *out);
+
 /* ======================================================================= O3: online calls
  * One pool [0, budget) driven call by call (R38-R44): orc_pool_alloc creates
  * tensor ids 0, 1, 2, ... (one op per tensor, the parents are its inputs) through Alg. 1;

@@ -236,3 +236,25 @@ class Pool:
         n = self._L.orc_pool_layout(self._p, a.ctypes.data, z.ctypes.data, o.ctypes.data, cap)
         n = min(n, cap)
         return a[:n].copy(), z[:n].copy(), o[:n].copy()
+
+
+# ----------------------------------------------------------------------------- O4 budgets
+ORC_BUDGET = np.dtype([("peak", "<u8"), ("min_budget", "<u8"), ("cutoff_budget", "<u8"),
+                       ("min_status", "<i4"), ("cutoff_status", "<i4"), ("replays", "<i4"),
+                       ("reserved", "<i4")])
+
+
+def budget_search(tr, flags: int = F_PARTITION | F_INPLACE, class_threshold: int = 15,
+                  max_depth: int = 512, coarse: int = 64, fine: int = 64):
+    """O4 -> orc_budget_result record (min / cutoff budgets on the R45 grids)"""
+    L = _replay_lib()
+    if not getattr(L, "_budget_ready", False):
+        L.orc_budget_search.argtypes = [ctypes.POINTER(_OrcTrace), ctypes.c_uint32, ctypes.c_uint32,
+                                        ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
+        L.orc_budget_search.restype = ctypes.c_int
+        L._budget_ready = True
+    st, keep = _trace_struct(tr)
+    out = np.zeros(1, ORC_BUDGET)
+    L.orc_budget_search(ctypes.byref(st), int(flags), int(class_threshold), int(max_depth),
+                        int(coarse), int(fine), out.ctypes.data)
+    return out[0]

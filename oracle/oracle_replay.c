@@ -889,3 +889,59 @@ int32_t orc_pool_layout(orc_pool *p, uint64_t *addr, uint64_t *size, int32_t *ow
   }
   return r->nb;
 }
+
+/* ======================================================================= O4: budget searches
+ * Sec. 4.2 minimum budget and App. C cutoff budget on
+ * the grid of DESIGN.md R45, every grid point replayed by O2 (plain loops). */
+static uint64_t o4_grid(uint64_t lo, uint64_t hi, int64_t j, int64_t steps) {
+  unsigned __int128 d = (unsigned __int128)(hi - lo) * (unsigned __int128)j / (unsigned __int128)steps;
+  uint64_t b = lo + (uint64_t)d;
+  return b < 1 ? 1 : b;
+}
+
+static int o4_meets(const orc_replay_result *r, int metric) {
+  return r->status == ORC_OK && (metric == 0 || r->evictions == 0);
+}
+
+int orc_budget_search(const orc_trace *tr, uint32_t flags, uint32_t class_threshold, int32_t max_depth,
+                      int32_t kc, int32_t kf, orc_budget_result *out) {
+  if (!tr || !out || kc < 1 || kf < 1) return ORC_INVALID_ARG;
+  memset(out, 0, sizeof(*out));
+  uint64_t peak = orc_peak_live(tr, flags);
+  out->peak = peak;
+  orc_cfg cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.flags = flags;
+  cfg.class_threshold = class_threshold;
+  cfg.max_depth = max_depth;
+  for (int m = 0; m < 2; ++m) {
+    uint64_t *dst = m == 0 ? &out->min_budget : &out->cutoff_budget;
+    int32_t *st = m == 0 ? &out->min_status : &out->cutoff_status;
+    /* coarse grid: the smallest k whose replay satisfies the metric */
+    int kstar = -1;
+    orc_replay_result r;
+    for (int k = 1; k <= kc && kstar < 0; ++k) {
+      cfg.budget = o4_grid(0, peak, k, kc);
+      orc_replay(tr, &cfg, &r, NULL, 0);
+      if (o4_meets(&r, m)) kstar = k;
+    }
+    if (kstar < 0) {
+      *st = ORC_INFEASIBLE;
+      *dst = 0;
+      continue;
+    }
+    /* fine grid inside (B_{k*-1}, B_{k*}] */
+    uint64_t lo = kstar > 1 ? o4_grid(0, peak, kstar - 1, kc) : 0, hi = o4_grid(0, peak, kstar, kc);
+    *st = ORC_OK;
+    *dst = hi;
+    for (int j = 1; j <= kf; ++j) {
+      cfg.budget = o4_grid(lo, hi, j, kf);
+      orc_replay(tr, &cfg, &r, NULL, 0);
+      if (o4_meets(&r, m)) {
+        *dst = cfg.budget;
+        break;
+      }
+    }
+  }
+  return ORC_OK;
+}

@@ -341,3 +341,24 @@ class Pool:
             raise CoopError(rc, "coop_pool_layout")
         k = min(n.value, cap)
         return a[:k].copy(), z[:k].copy(), o[:k].copy()
+
+
+# ----------------------------------------------------------------------------- budget searches
+BUDGET_RESULT_DTYPE = np.dtype([("peak", "<u8"), ("min_budget", "<u8"), ("cutoff_budget", "<u8"),
+                                ("min_status", "<i4"), ("cutoff_status", "<i4"), ("replays", "<i4"),
+                                ("reserved", "<i4")])
+assert BUDGET_RESULT_DTYPE.itemsize == 40
+lib.coop_budget_search.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int32,
+                                   ctypes.c_int32, _vp]
+lib.coop_budget_search.restype = ctypes.c_int
+
+
+def budget_search(trace: "Trace", flags: int, coarse: int = 64, fine: int = 64, class_threshold: int = 0,
+                  max_depth: int = 0):
+    """coop_budget_search -> coop_budget_result record (min / cutoff budgets, R45)."""
+    out = np.zeros(1, BUDGET_RESULT_DTYPE)
+    rc = lib.coop_budget_search(trace.handle, int(flags), int(class_threshold), int(max_depth),
+                                int(coarse), int(fine), out.ctypes.data)
+    if rc != OK:
+        raise CoopError(rc, "coop_budget_search")
+    return out[0]

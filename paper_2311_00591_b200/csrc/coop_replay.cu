@@ -373,3 +373,85 @@ extern "C" int coop_replay_trace(coop_trace_t t, const uint64_t *budgets, int32_
   replay_kernel<<<(unsigned)cells, kThreads, smem, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? COOP_OK : COOP_ERR_CUDA;
 }
+
+// ------------------------------------------------------------------ budget searches (R45)
+namespace {
+
+uint64_t grid_budget(uint64_t lo, uint64_t hi, int64_t j, int64_t steps) {
+  const unsigned __int128 d = (unsigned __int128)(hi - lo) * (unsigned __int128)j / (unsigned __int128)steps;
+  const uint64_t b = lo + (uint64_t)d;
+  return b < 1 ? 1 : b;
+}
+
+// one wave of replays on the default stream; results copied to the host
+int run_wave(coop_trace_t t, const std::vector<uint64_t> &budgets, uint32_t flags, uint32_t thr,
+             int32_t depth, std::vector<coop_replay_result> &res) {
+  res.assign(budgets.size(), coop_replay_result{});
+  if (budgets.empty()) return COOP_OK;
+  coop_replay_result *d = nullptr;
+  if (cudaMalloc(&d, budgets.size() * sizeof(coop_replay_result)) != cudaSuccess) return COOP_ERR_NOMEM;
+  int rc = coop_replay_trace(t, budgets.data(), (int32_t)budgets.size(), flags, thr, depth, d, nullptr, 0, nullptr);
+  if (rc == COOP_OK &&
+      cudaMemcpy(res.data(), d, budgets.size() * sizeof(coop_replay_result), cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = COOP_ERR_CUDA;
+  cudaFree(d);
+  return rc;
+}
+
+bool meets(const coop_replay_result &r, int metric) {  // 0: completes, 1: completes without eviction
+  return r.status == COOP_OK && (metric == 0 || r.evictions == 0);
+}
+
+}  // namespace
+
+extern "C" int coop_budget_search(coop_trace_t t, uint32_t flags, uint32_t thr, int32_t depth,
+                                  int32_t kc, int32_t kf, coop_budget_result *out) {
+  if (!t || !out || kc < 1 || kc > 4096 || kf < 1 || kf > 4096 || (flags & ~7u) || depth > 1024)
+    return COOP_ERR_INVALID_ARG;
+  uint64_t peak = 0;
+  int rc = coop_trace_peak_live(t, flags, &peak);
+  if (rc != COOP_OK) return rc;
+  coop_budget_result r{};
+  r.peak = peak;
+  std::vector<uint64_t> coarse((size_t)kc);
+  for (int k = 1; k <= kc; ++k) coarse[(size_t)k - 1] = grid_budget(0, peak, k, kc);
+  std::vector<coop_replay_result> cres;
+  rc = run_wave(t, coarse, flags, thr, depth, cres);
+  if (rc != COOP_OK) return rc;
+  r.replays = kc;
+  int kstar[2] = {-1, -1};
+  for (int m = 0; m < 2; ++m)
+    for (int k = 0; k < kc && kstar[m] < 0; ++k)
+      if (meets(cres[(size_t)k], m)) kstar[m] = k;
+  // both metrics' fine grids in one wave
+  std::vector<uint64_t> fine;
+  for (int m = 0; m < 2; ++m) {
+    if (kstar[m] < 0) continue;
+    const uint64_t lo = kstar[m] > 0 ? coarse[(size_t)kstar[m] - 1] : 0, hi = coarse[(size_t)kstar[m]];
+    for (int j = 1; j <= kf; ++j) fine.push_back(grid_budget(lo, hi, j, kf));
+  }
+  std::vector<coop_replay_result> fres;
+  rc = run_wave(t, fine, flags, thr, depth, fres);
+  if (rc != COOP_OK) return rc;
+  r.replays += (int32_t)fine.size();
+  size_t base = 0;
+  for (int m = 0; m < 2; ++m) {
+    uint64_t *dst = m == 0 ? &r.min_budget : &r.cutoff_budget;
+    int32_t *st = m == 0 ? &r.min_status : &r.cutoff_status;
+    if (kstar[m] < 0) {
+      *dst = 0;
+      *st = COOP_INFEASIBLE;
+      continue;
+    }
+    *st = COOP_OK;
+    *dst = coarse[(size_t)kstar[m]];
+    for (int j = 0; j < kf; ++j)
+      if (meets(fres[base + (size_t)j], m)) {
+        *dst = fine[base + (size_t)j];
+        break;
+      }
+    base += (size_t)kf;
+  }
+  *out = r;
+  return COOP_OK;
+}
