@@ -65,6 +65,8 @@ double orc_fsum(const double *x, int64_t n);
 #define ORC_F_PARTITION 1u            /* cheap tensor partitioning (Sec. 3.4)          */
 #define ORC_F_INPLACE 2u              /* recomputable in-place (Sec. 3.5); off = COW    */
 #define ORC_F_PARTITION_ALL_PHASES 4u /* partition backward/update ops too (R13)       */
+#define ORC_F_DTR 8u   /* baseline policy: DTR's argmin loop, h = c / (m s) (R46)              */
+#define ORC_F_DTE 16u  /* baseline policy: DTE, h = c / ((m + adjacent free bytes) s) (R46)    */
 
 typedef struct {
   int32_t n_tensors, n_ops;

@@ -88,7 +88,7 @@ class _OrcCfg(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
-F_PARTITION, F_INPLACE, F_PARTITION_ALL_PHASES = 1, 2, 4
+F_PARTITION, F_INPLACE, F_PARTITION_ALL_PHASES, F_DTR, F_DTE = 1, 2, 4, 8, 16
 UNSATISFIABLE, THRASHED = -3, -4
 EV_PARAM, EV_ALLOC, EV_INPLACE, EV_EVICT, EV_FREE, EV_REMAT, EV_EXEC, EV_REXEC = range(8)
 

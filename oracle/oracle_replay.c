@@ -223,10 +223,54 @@ static void evict(R *r, int32_t t) {
   r->res->digest = d;
 }
 
+/* The baselines the paper compares against (R46):
+ * repeat { h(t) for every resident evictable tensor -- DTR: c / (m s); DTE: c / ((m + the
+ * free bytes adjacent to t's block) s) -- and evict the argmin (ties: lowest address) }
+ * until some free block can hold `size` ("This process runs several times until the
+ * released memory is sufficient for the new tensor"). */
+static int evict_loop(R *r, uint64_t size) {
+  int dte = (r->cfg.flags & ORC_F_DTE) != 0;
+  r->win_first = r->win_last = -1;
+  r->win_span = 0;
+  r->win_cost = 0.0;
+  r->nvict = 0;
+  while (find_fit(r, size, 0) < 0) {
+    int best = -1;
+    double bh = 0.0;
+    for (int i = 0; i < r->nb; ++i) {
+      int32_t o = r->b[i].owner;
+      if (o == NO_OWNER || r->unevict[o] || r->pins[o] > 0 || r->locked[o]) continue;
+      int64_t s = r->clock - r->last_access[o]; /* staleness (R17) */
+      if (s < 1) s = 1;
+      uint64_t m = r->b[i].size;
+      if (dte) {
+        if (i > 0 && r->b[i - 1].owner == NO_OWNER) m += r->b[i - 1].size;
+        if (i + 1 < r->nb && r->b[i + 1].owner == NO_OWNER) m += r->b[i + 1].size;
+      }
+      double h = (double)projected_cost(r, o) / ((double)m * (double)s);
+      r->res->heuristic_evals++;
+      if (best < 0 || h < bh) {
+        best = i;
+        bh = h;
+      }
+    }
+    if (best < 0) {
+      r->status = ORC_UNSATISFIABLE; /* nothing left to evict */
+      return -1;
+    }
+    int32_t v = r->b[best].owner;
+    if (r->victims && r->nvict < 8192) r->victims[r->nvict] = v;
+    r->nvict++;
+    evict(r, v);
+  }
+  return 0;
+}
+
 /* sliding-window search over the address-ordered item list and eviction of the window
  * (Alg. 1 line "evict(sliding_window_search(size))"); returns 0 on success. */
 static int evict_window(R *r, uint64_t size) {
   const orc_trace *tr = r->tr;
+  if (r->cfg.flags & (ORC_F_DTR | ORC_F_DTE)) return evict_loop(r, size);
   int n = r->nb;
   if (n > 8192) {
     r->status = ORC_UNSATISFIABLE; /* beyond the search domain (R7) */
@@ -639,7 +683,9 @@ struct orc_pool_s {
 
 orc_pool *orc_pool_create(uint64_t budget, uint32_t flags, uint32_t class_threshold,
                           int32_t max_tensors, int32_t max_edges) {
-  if (budget < 1 || (flags & ~7u) || max_tensors < 1 || max_edges < 0) return NULL;
+  if (budget < 1 || (flags & ~31u) || ((flags & ORC_F_DTR) && (flags & ORC_F_DTE)) || max_tensors < 1 ||
+      max_edges < 0)
+    return NULL;
   orc_pool *p = (orc_pool *)calloc(1, sizeof(orc_pool));
   int T = max_tensors, E = max_edges;
   p->max_tensors = T;

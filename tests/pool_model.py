@@ -150,6 +150,33 @@ class OnlineModel:
         self.win = (i, j, span, cost)
         return [items[k][2] for k in range(i, j + 1) if items[k][2] != FREE]
 
+    def evict_loop(self, size):
+        """DTR / DTE baselines (R46), as tests/replay_model.py"""
+        dte = bool(self.flags & 16)
+        victims = []
+        while self.fit(size, False) is None:
+            best = None
+            runs = self.runs()
+            for idx, (a, sz, o) in enumerate(runs):
+                if o == FREE or self.unev[o] or self.pins[o] > 0:
+                    continue
+                st = max(1, self.clock - self.last_access[o])
+                m = sz
+                if dte:
+                    if idx > 0 and runs[idx - 1][2] == FREE:
+                        m += runs[idx - 1][1]
+                    if idx + 1 < len(runs) and runs[idx + 1][2] == FREE:
+                        m += runs[idx + 1][1]
+                h = float(self.projected(o)) / (float(m) * float(st))
+                self.c["heuristic_evals"] += 1
+                if best is None or h < best[0]:
+                    best = (h, o)
+            if best is None:
+                return None
+            victims.append(best[1])
+            self.evict(best[1])
+        return victims
+
     def evict(self, t):
         a = self.clear(t)
         self.c["evictions"] += 1
@@ -178,12 +205,16 @@ class OnlineModel:
             self.c["pressure"] += 1
             if sum(1 for x in self.mem if x == FREE) >= self.size[t]:
                 self.c["frag_fail"] += 1
-            victims = self.search(self.size[t])
+            if self.flags & 24:
+                victims = self.evict_loop(self.size[t])
+            else:
+                victims = self.search(self.size[t])
+                if victims is not None:
+                    for v in victims:
+                        self.evict(v)
             if victims is None:
                 self.c["fail_op"] = self.cur
                 return None, False
-            for v in victims:
-                self.evict(v)
             a = self.fit(self.size[t], right)
             self.put(t, a)
             fr = [s for _, s, o in self.runs() if o == FREE]

@@ -183,6 +183,31 @@ class Model:
             raise Unsat()
         return [items[k][2] for k in range(best[1], best[2] + 1) if items[k][2] != FREE]
 
+    def evict_loop(self, size):
+        """DTR / DTE baselines (R46): evict argmin h one tensor at a time until a free
+        block can hold `size`; h = c / (m s), DTE adds the adjacent free bytes to m."""
+        dte = bool(self.flags & 16)
+        while self.fit(size, False) is None:
+            best = None
+            runs = self.runs()
+            for idx, (a, sz, o) in enumerate(runs):
+                if o == FREE or self.unev[o] or self.pins[o] > 0 or self.locked[o]:
+                    continue
+                st = max(1, self.clock - self.last_access[o])
+                m = sz
+                if dte:
+                    if idx > 0 and runs[idx - 1][2] == FREE:
+                        m += runs[idx - 1][1]
+                    if idx + 1 < len(runs) and runs[idx + 1][2] == FREE:
+                        m += runs[idx + 1][1]
+                h = float(self.projected(o)) / (float(m) * float(st))
+                self.c["heuristic_evals"] += 1
+                if best is None or h < best[0]:
+                    best = (h, o)
+            if best is None:
+                raise Unsat()
+            self.evict(best[1])
+
     def evict(self, t):
         a = self.clear(t)
         self.c["evictions"] += 1
@@ -211,8 +236,11 @@ class Model:
             self.c["pressure"] += 1
             if sum(1 for x in self.mem if x == FREE) >= self.size[t]:
                 self.c["frag_fail"] += 1
-            for v in self.search(self.size[t]):
-                self.evict(v)
+            if self.flags & 24:
+                self.evict_loop(self.size[t])
+            else:
+                for v in self.search(self.size[t]):
+                    self.evict(v)
             a = self.fit(self.size[t], right)
             self.put(t, a)
             fr = [s for _, s, o in self.runs() if o == FREE]

@@ -216,3 +216,35 @@ def test_random_sessions_vs_model(flags):
             assert s[k].item() == v, (flags, seed, k)
         a, z, ow = o.layout()
         assert [(int(x), int(y), int(w)) for x, y, w in zip(a, z, ow)] == m.layout()
+
+
+def test_dtr_dte_worked_example():
+    """SPEC.md:390-402 (hand-derived): layout a[0,10) x[10,20) free[20,30) b[30,40) c[40,50),
+    x and c unevictable, a and b with equal c, m, s.  A 20-byte request: DTR ties a and b
+    (lowest address first) and needs both (evicting a alone frees no 20-byte block); DTE's
+    denominator counts b's free neighbour (m + 10), so it evicts b alone."""
+    for pol, want in ((O.F_DTR, [0, 3]), (O.F_DTE, [3])):
+        P = O.Pool(50, pol)
+        a = P.alloc(10, 100)[1]["tensor_id"]
+        P.alloc(10, 100, O.OP_UNEVICTABLE)
+        f = P.alloc(10, 100)[1]["tensor_id"]
+        b = P.alloc(10, 100)[1]["tensor_id"]
+        P.alloc(10, 100, O.OP_UNEVICTABLE)
+        assert P.free(f) == O.OK
+        assert P.access(a, 7) == O.OK and P.access(b, 0) == O.OK  # equal staleness
+        st, r, ev = P.alloc(20, 1)
+        assert st == O.OK and ev == want and r["window_first"] == -1
+        assert r["addr"] == 20 and (a, b) == (0, 3)  # first fit: [0,10) is too small
+
+
+@pytest.mark.parametrize("flags", [8, 16, 11, 19])
+def test_random_sessions_vs_model_baselines(flags):
+    for seed in range(6):
+        budget = 150 + (seed * 41) % 400
+        calls = PM.random_session(5000 + 100 * flags + seed, 100, budget=budget, flags=flags)
+        m = PM.OnlineModel(budget, flags)
+        o = O.Pool(budget, flags)
+        assert PM.drive(o, calls) == PM.drive(m, calls), (flags, seed)
+        s = o.stats()
+        for k, v in m.c.items():
+            assert s[k].item() == v, (flags, seed, k)

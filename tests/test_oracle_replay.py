@@ -195,3 +195,19 @@ def test_invalid_traces_rejected():
     b.op([x], 20, 1, inplace=x)  # size mismatch
     r, _ = O.replay(b.build(), 1000)
     assert int(r["status"]) == O.INVALID_ARG
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_dtr_dte_baselines_vs_model(seed):
+    """NEXT-1 baselines (R46): DTR / DTE argmin loops, same comparison with the independent
+    Python model (counters incl. heuristic evaluations, digest, full event log)."""
+    for tr, flags, budget in _random_cases(15, 700 + seed):
+        for pol in (O.F_DTR, O.F_DTE):
+            f = (flags & 7) | pol
+            r, log = O.replay(tr, budget, f, log_cap=100000)
+            m = Model(tr, budget, f)
+            status, fail_op = m.run()
+            got = {k: int(r[k]) for k in RESULT_FIELDS}
+            want = dict(m.c, status=status, fail_op=fail_op)
+            assert got == {k: int(want[k]) for k in RESULT_FIELDS}, (f, budget)
+            assert ev_tuples(log) == m.events
