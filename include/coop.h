@@ -165,6 +165,13 @@ int coop_trace_peak_live(coop_trace_t trace, uint32_t flags, uint64_t *out);
 #define COOP_F_PARTITION 1u            /* cheap tensor partitioning, Sec. 3.4 */
 #define COOP_F_INPLACE 2u              /* recomputable in-place, Sec. 3.5; off = copy-on-write */
 #define COOP_F_PARTITION_ALL_PHASES 4u /* partition backward/update ops too (R13)          */
+/* eviction policy (default: Coop's sliding window, Sec. 3.3).  The paper's baselines
+ * (R46), mutually exclusive: evict the argmin-h tensor one at a time,
+ * re-evaluating all candidates, until a free block fits -- DTR h = c / (m s); DTE
+ * h = c / ((m + adjacent free bytes) s).  Usually combined with no other flag (their
+ * systems have neither partitioning nor recomputable in-place). */
+#define COOP_F_POLICY_DTR 8u
+#define COOP_F_POLICY_DTE 16u
 
 typedef struct {
   int32_t status;              /* COOP_OK, COOP_ERR_UNSATISFIABLE, COOP_ERR_THRASHED,

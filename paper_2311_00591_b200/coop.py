@@ -147,6 +147,7 @@ class TraceDesc(ctypes.Structure):
 
 
 F_PARTITION, F_INPLACE, F_PARTITION_ALL_PHASES = 1, 2, 4
+F_POLICY_DTR, F_POLICY_DTE = 8, 16  # the paper's baseline eviction policies (R46)
 
 REPLAY_RESULT_DTYPE = np.dtype([
     ("status", "<i4"), ("fail_op", "<i4"), ("base_us", "<i8"), ("total_us", "<i8"),

@@ -341,7 +341,7 @@ int finish(coop_pool_s *p, coop_alloc_result *out, int64_t *evicted, int32_t cap
 }  // namespace
 
 extern "C" int coop_pool_init(const coop_pool_config *cfg, coop_pool_t *out) {
-  if (!cfg || !out || cfg->budget < 1 || (cfg->flags & ~7u) || cfg->max_tensors < 1 ||
+  if (!cfg || !out || cfg->budget < 1 || bad_flags(cfg->flags) || cfg->max_tensors < 1 ||
       cfg->max_tensors > kMaxT || cfg->max_edges < 0)
     return COOP_ERR_INVALID_ARG;
   coop_pool_s *p = new (std::nothrow) coop_pool_s();

@@ -322,7 +322,7 @@ extern "C" int coop_replay_trace(coop_trace_t t, const uint64_t *budgets, int32_
                                  coop_replay_result *out, coop_event *log, int64_t log_cap,
                                  coop_stream_t stream) {
   if (!t || n_budgets < 0 || (n_budgets > 0 && (!budgets || !out)) || log_cap < 0 ||
-      (flags & ~7u) || max_depth > 1024)
+      bad_flags(flags) || max_depth > 1024)
     return COOP_ERR_INVALID_ARG;
   if (n_budgets == 0) return COOP_OK;
   for (int i = 0; i < n_budgets; ++i)
@@ -406,7 +406,7 @@ bool meets(const coop_replay_result &r, int metric) {  // 0: completes, 1: compl
 
 extern "C" int coop_budget_search(coop_trace_t t, uint32_t flags, uint32_t thr, int32_t depth,
                                   int32_t kc, int32_t kf, coop_budget_result *out) {
-  if (!t || !out || kc < 1 || kc > 4096 || kf < 1 || kf > 4096 || (flags & ~7u) || depth > 1024)
+  if (!t || !out || kc < 1 || kc > 4096 || kf < 1 || kf > 4096 || bad_flags(flags) || depth > 1024)
     return COOP_ERR_INVALID_ARG;
   uint64_t peak = 0;
   int rc = coop_trace_peak_live(t, flags, &peak);

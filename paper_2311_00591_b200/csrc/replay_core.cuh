@@ -21,6 +21,11 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kCap = 4096;       // blocks per pool held by the kernel (COOP_ERR_NOMEM beyond)
 constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
 constexpr int kFree = -1;
+
+// replay / pool flag validation: known bits, at most one baseline policy
+inline bool bad_flags(uint32_t f) {
+  return (f & ~31u) || ((f & COOP_F_POLICY_DTR) && (f & COOP_F_POLICY_DTE));
+}
 constexpr int kMaxT = 16384;     // tensors per trace whose flags live in shared memory
 
 enum : uint8_t { TF_RES = 1, TF_BORN = 2, TF_DEAD = 4, TF_LOCK = 8 };
@@ -358,7 +363,7 @@ struct Cell {
   // cand[0..ncand): block indices of EVICTABLE items; writes w.ih[b] = RN(c(t) / s(t)).
   // A node is marked when pushed, so every node enters a candidate's stack at most once:
   // the per-thread stack (global workspace, T entries) cannot overflow.
-  __device__ void projected_costs(const int32_t *cand, int ncand) {
+  __device__ void projected_costs(const int32_t *cand, int ncand, int pol = 0) {
     uint32_t *mk = w.marks + (size_t)threadIdx.x * tr.T;
     int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
     int sp = 0, ci = -1, t = -1, stage = 0;
@@ -381,7 +386,16 @@ struct Cell {
           const int b = cand[ci];
           int64_t s = sh.clock - w.last_access[t];  // staleness (R17)
           if (s < 1) s = 1;
-          w.ih[b] = __ddiv_rn((double)acc, (double)s);  // h = c/s (R1)
+          double den = (double)s;  // Coop: h = c/s (R1)
+          if (pol) {               // DTR: c / (m s); DTE: m + the adjacent free bytes (R46)
+            uint64_t m = Z()[b];
+            if (pol == 2) {
+              if (b > 0 && O()[b - 1] == kFree) m += Z()[b - 1];
+              if (b + 1 < sh.nb && O()[b + 1] == kFree) m += Z()[b + 1];
+            }
+            den = __dmul_rn((double)m, (double)s);
+          }
+          w.ih[b] = __ddiv_rn((double)acc, den);
         }
         ci = atomicAdd(&sh.cand_next, 1);
         if (ci >= ncand) break;
@@ -450,7 +464,77 @@ struct Cell {
   // returns false when no window exists (R24).  Scratch: the inactive block buffer holds
   // S (span prefix, u64) in its addr[], B (barrier count prefix) in its size[] and the
   // item states in its owner[]; the exact 192-bit prefix H and h live in global memory.
+  // The baselines of the paper's comparison (R46): DTR / DTE evict
+  // the argmin-h tensor (ties: lowest address), one at a time, re-evaluating every
+  // candidate, until a free block can hold `need`.
+  __device__ bool evict_loop(uint64_t need, int pol) {
+    const uint64_t t0 = gtimer();
+    if (threadIdx.x == 0) {
+      sh.win_first = sh.win_last = -1;
+      sh.win_span = 0;
+      sh.win_cost = 0;
+      sh.nvict = 0;
+    }
+    __syncthreads();
+    bool ok = true;
+    while (find_fit(need, false) < 0) {
+      if (threadIdx.x == 0) {
+        sh.ncand = 0;
+        sh.cand_next = 0;
+      }
+      __syncthreads();
+      for (int b = threadIdx.x; b < sh.nb; b += kThreads) {
+        const int o = O()[b];
+        if (o != kFree && !__ldg(&tr.unevict[o]) && w.pins[o] == 0 && !(sh.tfl[o] & TF_LOCK))
+          w.cand[atomicAdd(&sh.ncand, 1)] = b;
+      }
+      __syncthreads();
+      const int nc = sh.ncand;
+      if (nc == 0) {  // nothing left to evict
+        ok = false;
+        break;
+      }
+      projected_costs(w.cand, nc, pol);
+      __syncthreads();
+      uint64_t best = ~0ull;
+      int bi = 0x7fffffff;
+      for (int c = threadIdx.x; c < nc; c += kThreads) {
+        const int b = w.cand[c];
+        const uint64_t hb = (uint64_t)__double_as_longlong(w.ih[b]);  // h >= 0: bit order
+        if (hb < best || (hb == best && b < bi)) {
+          best = hb;
+          bi = b;
+        }
+      }
+      const uint64_t hmin = cta_min_u64(sh, best);
+      const int bmin = cta_min_i32(sh, best == hmin ? bi : 0x7fffffff);
+      if (threadIdx.x == 0) {
+        sh.res.heuristic_evals += nc;
+        const int o = O()[bmin];
+        const uint64_t ad = A()[bmin];
+        sh.tfl[o] &= (uint8_t)~TF_RES;
+        sh.res.evictions++;
+        log_ev(3, sh.cur_op, o, ad);
+        uint64_t d = sh.res.digest;  // R29
+        d = splitmix64(d ^ (((uint64_t)(uint32_t)sh.cur_op << 32) | (uint32_t)o));
+        sh.res.digest = splitmix64(d ^ ad);
+        w.victims[sh.nvict++] = o;
+      }
+      __syncthreads();
+      release(bmin);  // free + coalesce
+    }
+    if (threadIdx.x == 0) {
+      const int64_t dt = (int64_t)(gtimer() - t0);
+      sh.res.search_ns_total += dt;
+      if (dt > sh.res.search_ns_max) sh.res.search_ns_max = dt;
+    }
+    __syncthreads();
+    return ok;
+  }
+
   __device__ bool evict_window(uint64_t need) {
+    if (a.flags & (COOP_F_POLICY_DTR | COOP_F_POLICY_DTE))
+      return evict_loop(need, (a.flags & COOP_F_POLICY_DTE) ? 2 : 1);
     const uint64_t t0 = gtimer();
     if (threadIdx.x == 0) {
       sh.ncand = 0;

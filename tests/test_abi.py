@@ -80,7 +80,8 @@ def test_pool_argument_checks_without_gpu():
     lib = coop.lib
     h = ctypes.c_void_p()
     assert lib.coop_pool_init(None, ctypes.byref(h)) == coop.ERR_INVALID_ARG
-    for cfg in [coop.PoolConfig(0, 0, 0, 16, 16), coop.PoolConfig(100, 8, 0, 16, 16),
+    for cfg in [coop.PoolConfig(0, 0, 0, 16, 16), coop.PoolConfig(100, 32, 0, 16, 16),
+                coop.PoolConfig(100, 24, 0, 16, 16),
                 coop.PoolConfig(100, 0, 0, 0, 16), coop.PoolConfig(100, 0, 0, 16385, 16),
                 coop.PoolConfig(100, 0, 0, 16, -1)]:
         assert lib.coop_pool_init(ctypes.byref(cfg), ctypes.byref(h)) == coop.ERR_INVALID_ARG

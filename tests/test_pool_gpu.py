@@ -36,7 +36,7 @@ def _same_state(g, o):
     assert np.array_equal(ag, ao) and np.array_equal(zg, zo) and np.array_equal(og, oo.astype(np.int64))
 
 
-@pytest.mark.parametrize("flags", [0, 1, 2, 3, 7])
+@pytest.mark.parametrize("flags", [0, 1, 2, 3, 7, 8, 16, 19])
 def test_random_sessions_parity(flags):
     coop = _coop()
     for seed in range(8):

@@ -102,3 +102,26 @@ def test_config5_budget_samples(name, ks):
     peak = O.peak_live(tr, flags)
     budgets = [peak * (20 * 255 + 80 * k) // (100 * 255) for k in ks]
     check(tr, budgets, flags, ctx=f"config5 {name}")
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_dtr_dte_random_traces_gpu(seed):
+    """NEXT-1 baselines (R46) through coop_replay_trace: bit-exact with O2 incl. event logs."""
+    rng = np.random.default_rng(900 + seed)
+    for _ in range(6):
+        tr = TR.random_trace(rng, n_params=int(rng.integers(0, 4)), n_fwd=int(rng.integers(3, 12)),
+                             iters=int(rng.integers(1, 3)), inplace_p=0.25)
+        for pol in (coop.F_POLICY_DTR, coop.F_POLICY_DTE):
+            flags = pol | int(rng.choice([0, 1, 2, 3]))
+            peak = O.peak_live(tr, flags & 7)
+            budgets = [max(1, int(peak * f)) for f in (0.4, 0.6, 0.8, 1.0)]
+            check(tr, budgets, flags, log_cap=4000, ctx=f"seed {seed} pol {pol}")
+
+
+@pytest.mark.parametrize("name", ["resnet50", "unet", "swin_t"])
+def test_dtr_dte_dnn_gpu(name):
+    tr = dnn.dnn(name)
+    for pol in (coop.F_POLICY_DTR, coop.F_POLICY_DTE):
+        peak = O.peak_live(tr, 0)
+        budgets = [int(peak * f) for f in (0.5, 0.75, 1.0)]
+        check(tr, budgets, pol, ctx=f"{name} pol {pol}")
