@@ -341,6 +341,22 @@ int coop_pool_stats(coop_pool_t pool, coop_replay_result *out);
 int coop_pool_layout(coop_pool_t pool, uint64_t *addr, uint64_t *size, int64_t *owner,
                      int32_t cap, int32_t *n_blocks);
 
+/*
+ * coop_pool_service -- low-latency mode for the online calls above (
+ * the calls are Alg. 1 per call, whose search the paper times per call,
+ * PAPER.md:264, 299-300).  With idle_timeout_us > 0 one CTA stays resident on the pool's
+ * stream and polls a mailbox in mapped pinned host memory: each call writes its arguments
+ * and a sequence number there and spins until the device acknowledges it -- no kernel
+ * launch and no stream synchronisation per call.  Results are bit-identical to the
+ * launch-per-call mode (same device code).  The resident kernel exits after
+ * idle_timeout_us without a call (so a device-wide synchronisation elsewhere in the
+ * process waits at most that long) and is relaunched transparently by the next call.
+ * idle_timeout_us = 0 stops it and returns to one launch per call (the default).
+ * The resident CTA occupies one SM while active.  COOP_ERR_INVALID_ARG for a timeout
+ * above 10 s, COOP_ERR_CUDA on launch failure.  Not thread-safe (one owner per handle).
+ */
+int coop_pool_service(coop_pool_t pool, uint32_t idle_timeout_us);
+
 #ifdef __cplusplus
 }
 #endif

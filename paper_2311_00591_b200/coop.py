@@ -268,8 +268,9 @@ lib.coop_access.argtypes = [_vp, ctypes.c_int64, ctypes.c_uint64]
 lib.coop_rematerialize.argtypes = [_vp, ctypes.c_int64, _vp, _vp, ctypes.c_int32]
 lib.coop_pool_stats.argtypes = [_vp, _vp]
 lib.coop_pool_layout.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
+lib.coop_pool_service.argtypes = [_vp, ctypes.c_uint32]
 for _f in ("coop_pool_init", "coop_pool_destroy", "coop_alloc", "coop_free", "coop_access",
-           "coop_rematerialize", "coop_pool_stats", "coop_pool_layout"):
+           "coop_rematerialize", "coop_pool_stats", "coop_pool_layout", "coop_pool_service"):
     getattr(lib, _f).restype = ctypes.c_int
 
 
@@ -280,7 +281,7 @@ class Pool:
     status."""
 
     def __init__(self, budget: int, flags: int = F_PARTITION | F_INPLACE, class_threshold: int = 15,
-                 max_tensors: int = 4096, max_edges: int = 16384):
+                 max_tensors: int = 4096, max_edges: int = 16384, service_idle_us: int = 0):
         cfg = PoolConfig(int(budget), int(flags), int(class_threshold), int(max_tensors), int(max_edges))
         h = _vp()
         rc = lib.coop_pool_init(ctypes.byref(cfg), ctypes.byref(h))
@@ -288,6 +289,14 @@ class Pool:
             raise CoopError(rc, "coop_pool_init")
         self.handle = h
         self._ev = np.zeros(8192, np.int64)
+        if service_idle_us:
+            self.service(service_idle_us)
+
+    def service(self, idle_timeout_us: int):
+        """coop_pool_service: resident polling CTA (idle_timeout_us > 0) or one launch per call (0)."""
+        rc = lib.coop_pool_service(self.handle, int(idle_timeout_us))
+        if rc != OK:
+            raise CoopError(rc, "coop_pool_service")
 
     def close(self):
         if self.handle:

@@ -16,6 +16,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <new>
 #include <vector>
 
@@ -69,9 +71,9 @@ struct PArgs {
   int32_t *io_victims;
 };
 
-__global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  Shared &sh = *reinterpret_cast<Shared *>(smem);
+// One online call on the persistent state (the body of both the per-call kernel and the
+// service kernel's loop).  Ends with every thread's state stores fenced system-wide.
+__device__ __forceinline__ void pool_call(const PArgs &pa, Shared &sh) {
   Cell c(pa.k, sh, 0);
   PoolState &P = *pa.ps;
   const GraphMut &g = pa.g;
@@ -249,6 +251,89 @@ __global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
   __threadfence_system();
 }
 
+__global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  pool_call(pa, *reinterpret_cast<Shared *>(smem));
+}
+
+// ---- persistent service (coop_pool_service) ----------------------------
+// One resident CTA per pool polls a mailbox in mapped pinned host memory: the host writes
+// a call's arguments, then bumps `seq`; thread 0 sees the new sequence number (acquire,
+// system scope), the CTA runs pool_call, and thread 0 publishes `done = seq` after a
+// system-scope fence.  A call therefore costs two PCIe crossings instead of a launch and
+// a stream synchronisation.  The kernel exits on PK_STOP, or after `idle_ns` without a
+// call (so a device-wide synchronisation elsewhere never waits longer than that); the
+// host relaunches it on the next call.
+enum : int32_t { PK_STOP = 4 };
+
+struct Mailbox {  // mapped pinned host memory, written by the host (except done)
+  int64_t seq;
+  int32_t kind, t, src, n_parents;
+  uint64_t size, adv;
+  int64_t cost;
+  uint32_t op_flags, pad0;
+  int64_t pad1[2];
+  int64_t done;  // written by the device (own 64-byte line)
+  int64_t pad2[7];
+};
+
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
+  int64_t v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1) pool_service_kernel(const PArgs base, Mailbox *mb,
+                                                                   uint64_t idle_ns) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int64_t s_seq;
+  __shared__ int32_t s_go;
+  __shared__ PArgs s_pa;
+  Shared &sh = *reinterpret_cast<Shared *>(smem);
+  int64_t last = ld_acquire_sys(&mb->done);
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const uint64_t t0 = gtimer();
+      int64_t s;
+      int go;
+      for (;;) {
+        s = ld_acquire_sys(&mb->seq);
+        if (s != last) { go = 1; break; }
+        if (gtimer() - t0 > idle_ns) { go = 0; break; }
+      }
+      s_seq = s;
+      if (go) {
+        PArgs pa = base;
+        pa.kind = *(volatile int32_t *)&mb->kind;
+        pa.t = *(volatile int32_t *)&mb->t;
+        pa.src = *(volatile int32_t *)&mb->src;
+        pa.n_parents = *(volatile int32_t *)&mb->n_parents;
+        pa.size = *(volatile uint64_t *)&mb->size;
+        pa.adv = *(volatile uint64_t *)&mb->adv;
+        pa.cost = *(volatile int64_t *)&mb->cost;
+        pa.op_flags = *(volatile uint32_t *)&mb->op_flags;
+        if (pa.kind == PK_STOP) go = 2;
+        s_pa = pa;
+      }
+      s_go = go;
+    }
+    __syncthreads();
+    const int go = s_go;
+    if (go == 1) pool_call(s_pa, sh);
+    __syncthreads();
+    if (go == 0) break;
+    last = s_seq;
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      st_release_sys(&mb->done, last);
+    }
+    if (go == 2) break;
+  }
+}
+
 }  // namespace
 }  // namespace coop
 
@@ -269,6 +354,12 @@ struct coop_pool_s {
   unsigned char *io_dev = nullptr;
   int32_t n_tensors = 0, n_edges = 0;
   std::vector<uint64_t> sizes;  // host mirror for argument validation
+  // persistent service (coop_pool_service): mailbox in mapped pinned memory
+  Mailbox *mb_host = nullptr, *mb_dev = nullptr;
+  int64_t seq = 0;
+  uint64_t idle_ns = 0;  // 0: one launch per call
+  bool launched = false;  // a service kernel may be resident on `stream`
+  std::chrono::steady_clock::time_point last_call{};
 };
 
 namespace {
@@ -277,7 +368,11 @@ size_t io_bytes(const coop_pool_config &c) {
   return sizeof(HostIO) + (size_t)(c.max_edges + 1) * 4 + (size_t)(kCap + 2) * 4;
 }
 
+void service_stop(coop_pool_s *p);
+
 void pool_release(coop_pool_s *p) {
+  service_stop(p);
+  if (p->mb_host) cudaFreeHost(p->mb_host);
   if (p->stream) cudaStreamDestroy(p->stream);
   if (p->d_ps) cudaFree(p->d_ps);
   if (p->d_graph) cudaFree(p->d_graph);
@@ -286,8 +381,7 @@ void pool_release(coop_pool_s *p) {
   delete p;
 }
 
-int launch_call(coop_pool_s *p, int32_t kind, int32_t t, uint64_t size, int64_t cost,
-                uint32_t op_flags, int32_t src, int32_t n_parents, uint64_t adv) {
+PArgs base_args(coop_pool_s *p) {
   PArgs a{};
   a.k.tr = p->td;
   a.k.flags = p->cfg.flags;
@@ -298,6 +392,82 @@ int launch_call(coop_pool_s *p, int32_t kind, int32_t t, uint64_t size, int64_t 
   a.k.lay = p->lay;
   a.g = p->g;
   a.ps = p->d_ps;
+  a.io = reinterpret_cast<HostIO *>(p->io_dev);
+  a.io_parents = reinterpret_cast<const int32_t *>(p->io_dev + sizeof(HostIO));
+  a.io_victims = reinterpret_cast<int32_t *>(p->io_dev + sizeof(HostIO) + (size_t)(p->cfg.max_edges + 1) * 4);
+  return a;
+}
+
+// Launch the service kernel if none is resident (never launched, or it exited idle).
+int service_ensure(coop_pool_s *p) {
+  if (p->launched) {
+    const cudaError_t q = cudaStreamQuery(p->stream);
+    if (q == cudaErrorNotReady) return COOP_OK;
+    if (q != cudaSuccess) return COOP_ERR_CUDA;
+  }
+  pool_service_kernel<<<1, kThreads, sizeof(Shared), p->stream>>>(base_args(p), p->mb_dev, p->idle_ns);
+  if (cudaGetLastError() != cudaSuccess) return COOP_ERR_CUDA;
+  p->launched = true;
+  return COOP_OK;
+}
+
+// Post one call to the mailbox and spin until the device acknowledges it.  A kernel that
+// went idle between the post and its last poll is detected by cudaStreamQuery and
+// relaunched (it then sees the pending sequence number).
+int service_call(coop_pool_s *p, int32_t kind, int32_t t, uint64_t size, int64_t cost,
+                 uint32_t op_flags, int32_t src, int32_t n_parents, uint64_t adv) {
+  volatile Mailbox *m = p->mb_host;
+  m->kind = kind;
+  m->t = t;
+  m->src = src;
+  m->n_parents = n_parents;
+  m->size = size;
+  m->adv = adv;
+  m->cost = cost;
+  m->op_flags = op_flags;
+  const int64_t s = ++p->seq;
+  std::atomic_thread_fence(std::memory_order_release);
+  m->seq = s;
+  const auto t0 = std::chrono::steady_clock::now();
+  // a kernel idle for about its timeout may have exited: check (and relaunch) up front
+  if (!p->launched || (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t0 - p->last_call).count() >= p->idle_ns / 2)
+    if (service_ensure(p) != COOP_OK) return COOP_ERR_CUDA;
+  for (uint32_t spin = 1; m->done != s; ++spin) {
+    if ((spin & 0x3fffu) == 0) {
+      const cudaError_t q = cudaStreamQuery(p->stream);
+      if (q == cudaSuccess) {  // the kernel exited (idle) before seeing the call
+        if (m->done == s) break;
+        p->launched = false;
+        if (service_ensure(p) != COOP_OK) return COOP_ERR_CUDA;
+      } else if (q != cudaErrorNotReady) {
+        return COOP_ERR_CUDA;
+      }
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) return COOP_ERR_CUDA;
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  p->last_call = std::chrono::steady_clock::now();
+  return COOP_OK;
+}
+
+void service_stop(coop_pool_s *p) {
+  if (!p->launched) return;
+  if (cudaStreamQuery(p->stream) == cudaErrorNotReady) service_call(p, PK_STOP, 0, 0, 0, 0, -1, 0, 0);
+  cudaStreamSynchronize(p->stream);
+  p->launched = false;
+}
+
+int launch_call(coop_pool_s *p, int32_t kind, int32_t t, uint64_t size, int64_t cost,
+                uint32_t op_flags, int32_t src, int32_t n_parents, uint64_t adv) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != p->device) cudaSetDevice(p->device);
+  if (p->idle_ns) {
+    const int rc = service_call(p, kind, t, size, cost, op_flags, src, n_parents, adv);
+    if (prev != p->device) cudaSetDevice(prev);
+    return rc;
+  }
+  PArgs a = base_args(p);
   a.kind = kind;
   a.t = t;
   a.src = src;
@@ -306,12 +476,6 @@ int launch_call(coop_pool_s *p, int32_t kind, int32_t t, uint64_t size, int64_t 
   a.adv = adv;
   a.cost = cost;
   a.op_flags = op_flags;
-  a.io = reinterpret_cast<HostIO *>(p->io_dev);
-  a.io_parents = reinterpret_cast<const int32_t *>(p->io_dev + sizeof(HostIO));
-  a.io_victims = reinterpret_cast<int32_t *>(p->io_dev + sizeof(HostIO) + (size_t)(p->cfg.max_edges + 1) * 4);
-  int prev = 0;
-  cudaGetDevice(&prev);
-  if (prev != p->device) cudaSetDevice(p->device);
   pool_kernel<<<1, kThreads, sizeof(Shared), p->stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
@@ -375,6 +539,17 @@ extern "C" int coop_pool_init(const coop_pool_config *cfg, coop_pool_t *out) {
     rc = COOP_ERR_NOMEM;
   }
   if (rc == COOP_OK && cudaHostGetDevicePointer((void **)&p->io_dev, p->io_host, 0) != cudaSuccess) rc = COOP_ERR_CUDA;
+  if (rc == COOP_OK && cudaHostAlloc((void **)&p->mb_host, sizeof(Mailbox), cudaHostAllocMapped) != cudaSuccess) {
+    p->mb_host = nullptr;
+    rc = COOP_ERR_NOMEM;
+  }
+  if (rc == COOP_OK) {
+    memset(p->mb_host, 0, sizeof(Mailbox));
+    if (cudaHostGetDevicePointer((void **)&p->mb_dev, p->mb_host, 0) != cudaSuccess) rc = COOP_ERR_CUDA;
+  }
+  if (rc == COOP_OK && cudaFuncSetAttribute(pool_service_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)sizeof(Shared)) != cudaSuccess)
+    rc = COOP_ERR_CUDA;
   if (rc == COOP_OK && cudaFuncSetAttribute(pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)sizeof(Shared)) != cudaSuccess)
     rc = COOP_ERR_CUDA;
@@ -535,4 +710,16 @@ extern "C" int coop_pool_layout(coop_pool_t p, uint64_t *addr, uint64_t *size, i
   for (int i = 0; i < n; ++i) owner[i] = ow[(size_t)i];
   *n_blocks = nb;
   return COOP_OK;
+}
+
+extern "C" int coop_pool_service(coop_pool_t p, uint32_t idle_timeout_us) {
+  if (!p || idle_timeout_us > 10000000u) return COOP_ERR_INVALID_ARG;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != p->device) cudaSetDevice(p->device);
+  if (idle_timeout_us == 0) service_stop(p);
+  p->idle_ns = (uint64_t)idle_timeout_us * 1000ull;
+  const int rc = (idle_timeout_us && !p->launched) ? service_ensure(p) : COOP_OK;
+  if (prev != p->device) cudaSetDevice(prev);
+  return rc;
 }

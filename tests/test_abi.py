@@ -93,4 +93,5 @@ def test_pool_argument_checks_without_gpu():
     n = ctypes.c_int32()
     assert lib.coop_pool_layout(None, None, None, None, 0, ctypes.byref(n)) == coop.ERR_INVALID_ARG
     assert lib.coop_pool_destroy(None) == coop.ERR_INVALID_ARG
+    assert lib.coop_pool_service(None, 0) == coop.ERR_INVALID_ARG
     assert coop.ALLOC_RESULT_DTYPE.itemsize == 56

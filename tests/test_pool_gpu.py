@@ -109,3 +109,60 @@ def test_capacity_and_double_free():
     assert p.alloc(10, 1)[0] == coop.ERR_NOMEM
     assert p.free(t1) == coop.OK and p.free(t1) == coop.ERR_BAD_STATE
     assert p.access(t1) == coop.ERR_BAD_STATE
+
+
+@pytest.mark.parametrize("flags", [3, 7, 16])
+def test_service_mode_parity(flags):
+    """coop_pool_service (NEXT-4): the resident polling CTA gives call-by-call the same
+    results as the oracle (and so as the launch-per-call mode)"""
+    coop = _coop()
+    for seed in range(4):
+        budget = 200 + (seed * 71) % 400
+        calls = PM.random_session(9100 + 10 * flags + seed, 150, budget=budget, flags=flags)
+        g = coop.Pool(budget, flags, service_idle_us=200000)
+        o = O.Pool(budget, flags)
+        tg = PM.drive(g, calls)
+        to = PM.drive(o, calls)
+        assert tg == to, (flags, seed)
+        _same_state(g, o)
+        g.close()
+
+
+def test_service_idle_exit_and_relaunch():
+    """the resident kernel exits after its idle timeout (a device-wide synchronize then
+    returns), the next call relaunches it transparently, and switching the service off and
+    on mid-session keeps the results equal to the oracle's"""
+    import time
+
+    import torch
+    coop = _coop()
+
+    class Toggling:
+        def __init__(self, pool):
+            self.p, self.n = pool, 0
+
+        def _tick(self):
+            self.n += 1
+            if self.n % 25 == 0:
+                mode = (self.n // 25) % 3
+                self.p.service((0, 2000, 5000)[mode])
+                t0 = time.time()
+                torch.cuda.synchronize()  # returns once any resident kernel went idle
+                assert time.time() - t0 < 5.0
+                time.sleep(0.01)
+
+        def __getattr__(self, name):
+            f = getattr(self.p, name)
+            if name in ("alloc", "free", "access", "remat"):
+                def g(*a, **k):
+                    self._tick()
+                    return f(*a, **k)
+                return g
+            return f
+
+    calls = PM.random_session(4242, 150, budget=400, flags=3)
+    g = coop.Pool(400, 3, service_idle_us=2000)
+    o = O.Pool(400, 3)
+    assert PM.drive(Toggling(g), calls) == PM.drive(o, calls)
+    _same_state(g, o)
+    g.close()

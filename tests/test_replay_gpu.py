@@ -91,6 +91,16 @@ def test_ablation_flags_dnn():
             check(tr, [int(peak * 0.6), int(peak * 0.85)], flags, ctx=f"{name} flags {flags}")
 
 
+@pytest.mark.parametrize("name", ["resnet50", "unet"])
+def test_ablation_no_sliding_window_dnn(name):
+    """App. B "w/o sliding window": DTE's heuristic loop in place of the
+    window search, with partitioning and recomputable in-place kept (NEXT-2)."""
+    flags = coop.F_POLICY_DTE | coop.F_PARTITION | coop.F_INPLACE
+    tr = dnn.dnn(name)
+    peak = O.peak_live(tr, flags & 7)
+    check(tr, [int(peak * 0.4), int(peak * 0.6), int(peak * 0.85)], flags, ctx=f"{name} no-window")
+
+
 @pytest.mark.parametrize("name,ks", [("bilstm", (48, 100, 180, 255)), ("inception_v3", (0, 40, 120)),
                                      ("spos", (0, 64, 200))])
 def test_config5_budget_samples(name, ks):
