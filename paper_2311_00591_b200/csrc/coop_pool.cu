@@ -71,31 +71,63 @@ struct PArgs {
   int32_t *io_victims;
 };
 
-// One online call on the persistent state (the body of both the per-call kernel and the
-// service kernel's loop).  Ends with every thread's state stores fenced system-wide.
-__device__ __forceinline__ void pool_call(const PArgs &pa, Shared &sh) {
-  Cell c(pa.k, sh, 0);
+// The persistent state moves between global memory and the CTA's shared memory:
+// pool_load before a call (or once, when the service kernel starts), pool_store after it
+// (or when the service kernel flushes / exits).
+__device__ __forceinline__ void pool_load(const PArgs &pa, Shared &sh) {
   PoolState &P = *pa.ps;
-  const GraphMut &g = pa.g;
-  const int tid = threadIdx.x, t = pa.t;
+  const int tid = threadIdx.x;
   const int nb0 = P.nb, nt = P.n_tensors;
   const int nflag = min(nt + 1, pa.k.tr.T);
-  // ---- load the persistent state into the CTA
+  uint8_t *tflags = pa.k.ws + pa.k.lay.tflags;  // CTA slot 0 (Cell's layout)
   for (int b = tid; b < nb0; b += kThreads) {
     sh.addr[0][b] = P.addr[b];
     sh.size[0][b] = P.size[b];
     sh.owner[0][b] = P.owner[b];
   }
-  for (int x = tid; x < nflag; x += kThreads) sh.tfl[x] = c.w.tflags[x];
+  for (int x = tid; x < nflag; x += kThreads) sh.tfl[x] = tflags[x];
   if (tid == 0) {
     sh.cur = 0;
     sh.nb = nb0;
     sh.bytes_free = P.bytes_free;
     sh.clock = P.clock;
+    sh.res = P.res;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void pool_store(const PArgs &pa, Shared &sh) {
+  PoolState &P = *pa.ps;
+  const int tid = threadIdx.x;
+  const int nflag = min(P.n_tensors + 1, pa.k.tr.T);
+  uint8_t *tflags = pa.k.ws + pa.k.lay.tflags;
+  const int nb1 = sh.nb, cur = sh.cur;
+  for (int b = tid; b < nb1; b += kThreads) {
+    P.addr[b] = sh.addr[cur][b];
+    P.size[b] = sh.size[cur][b];
+    P.owner[b] = sh.owner[cur][b];
+  }
+  for (int x = tid; x < nflag; x += kThreads) tflags[x] = sh.tfl[x];
+  if (tid == 0) {
+    P.nb = nb1;
+    P.bytes_free = sh.bytes_free;
+    P.clock = sh.clock;
+    P.res = sh.res;
+  }
+  __syncthreads();
+}
+
+// One online call on the state held in shared memory (loaded by pool_load).  Results go
+// to the mapped HostIO; the caller orders them before its completion signal.
+__device__ __forceinline__ void pool_call(const PArgs &pa, Shared &sh) {
+  Cell c(pa.k, sh, 0);
+  PoolState &P = *pa.ps;
+  const GraphMut &g = pa.g;
+  const int tid = threadIdx.x, t = pa.t;
+  if (tid == 0) {
     sh.status = COOP_OK;
     sh.cur_op = t;
     sh.redpar = 0;
-    sh.res = P.res;
     sh.win_first = sh.win_last = -1;
     sh.nvict = 0;
     sh.win_span = 0;
@@ -233,27 +265,17 @@ __device__ __forceinline__ void pool_call(const PArgs &pa, Shared &sh) {
       io.r = r;
     }
   }
-  // ---- store the state back
-  const int nb1 = sh.nb, cur = sh.cur;
-  for (int b = tid; b < nb1; b += kThreads) {
-    P.addr[b] = sh.addr[cur][b];
-    P.size[b] = sh.size[cur][b];
-    P.owner[b] = sh.owner[cur][b];
-  }
-  for (int x = tid; x < nflag; x += kThreads) c.w.tflags[x] = sh.tfl[x];
-  if (tid == 0) {
-    P.nb = nb1;
-    P.bytes_free = sh.bytes_free;
-    P.clock = sh.clock;
-    P.res = sh.res;
-  }
   c.w.epochs[tid] = c.epoch;
-  __threadfence_system();
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
   extern __shared__ __align__(16) unsigned char smem[];
-  pool_call(pa, *reinterpret_cast<Shared *>(smem));
+  Shared &sh = *reinterpret_cast<Shared *>(smem);
+  pool_load(pa, sh);
+  pool_call(pa, sh);
+  pool_store(pa, sh);
+  __threadfence_system();
 }
 
 // ---- persistent service (coop_pool_service) ----------------------------
@@ -264,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
 // a stream synchronisation.  The kernel exits on PK_STOP, or after `idle_ns` without a
 // call (so a device-wide synchronisation elsewhere never waits longer than that); the
 // host relaunches it on the next call.
-enum : int32_t { PK_STOP = 4 };
+enum : int32_t { PK_STOP = 4, PK_FLUSH = 5 };
 
 struct Mailbox {  // mapped pinned host memory, written by the host (except done)
   int64_t seq;
@@ -294,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) pool_service_kernel(const PArgs b
   __shared__ PArgs s_pa;
   Shared &sh = *reinterpret_cast<Shared *>(smem);
   int64_t last = ld_acquire_sys(&mb->done);
+  pool_load(base, sh);  // the state stays in shared memory while the kernel is resident
   for (;;) {
     if (threadIdx.x == 0) {
       const uint64_t t0 = gtimer();
@@ -322,9 +345,17 @@ __global__ void __launch_bounds__(kThreads, 1) pool_service_kernel(const PArgs b
     }
     __syncthreads();
     const int go = s_go;
-    if (go == 1) pool_call(s_pa, sh);
+    if (go == 1) {
+      if (s_pa.kind == PK_FLUSH) pool_store(base, sh);
+      else pool_call(s_pa, sh);
+    } else {
+      pool_store(base, sh);  // exit (idle or PK_STOP): the state back to global memory
+    }
     __syncthreads();
-    if (go == 0) break;
+    if (go == 0) {
+      __threadfence_system();
+      break;
+    }
     last = s_seq;
     if (threadIdx.x == 0) {
       __threadfence_system();
@@ -688,8 +719,20 @@ extern "C" int coop_rematerialize(coop_pool_t p, int64_t t, coop_alloc_result *o
   return finish(p, out, evicted_ids, evicted_cap);
 }
 
+// With a resident service kernel the live state is in its shared memory: flush it first.
+static int service_flush(coop_pool_t p) {
+  if (!p->idle_ns || !p->launched || cudaStreamQuery(p->stream) != cudaErrorNotReady) return COOP_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != p->device) cudaSetDevice(p->device);
+  const int rc = service_call(p, PK_FLUSH, 0, 0, 0, 0, -1, 0, 0);
+  if (prev != p->device) cudaSetDevice(prev);
+  return rc;
+}
+
 extern "C" int coop_pool_stats(coop_pool_t p, coop_replay_result *out) {
   if (!p || !out) return COOP_ERR_INVALID_ARG;
+  if (service_flush(p) != COOP_OK) return COOP_ERR_CUDA;
   if (cudaMemcpy(out, &p->d_ps->res, sizeof(*out), cudaMemcpyDeviceToHost) != cudaSuccess)
     return COOP_ERR_CUDA;
   out->status = COOP_OK;
@@ -699,6 +742,7 @@ extern "C" int coop_pool_stats(coop_pool_t p, coop_replay_result *out) {
 extern "C" int coop_pool_layout(coop_pool_t p, uint64_t *addr, uint64_t *size, int64_t *owner,
                                 int32_t cap, int32_t *n_blocks) {
   if (!p || !n_blocks || cap < 0 || (cap > 0 && (!addr || !size || !owner))) return COOP_ERR_INVALID_ARG;
+  if (service_flush(p) != COOP_OK) return COOP_ERR_CUDA;
   int32_t nb = 0;
   if (cudaMemcpy(&nb, &p->d_ps->nb, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return COOP_ERR_CUDA;
   const int n = std::min(nb, cap);

@@ -33,7 +33,7 @@ namespace coop {
 
 namespace {
 
-constexpr int kCandCap = 1024;
+constexpr int kCandCap = 512;  // fits two 512-thread CTAs (one stage each) per SM at N = 4096
 constexpr int kMaxWarps = 16;
 constexpr uint64_t kSizeMask = (1ull << 62) - 1ull;
 constexpr uint64_t kSizeLimit = 1ull << 48;
@@ -873,7 +873,7 @@ int launch_window_search(const coop_tables_soa *t, const uint64_t *requests, coo
   const char *two = getenv("COOP_SEARCH_TWO_CTA");  // profiling hook: 2 CTAs/SM, 1 stage
   if (two && two[0] == '1' && a.n <= 4096) return launch_k<16, 256, 2>(a, st);
   if (a.n <= 2048) return launch_k<8, 256, 2>(a, st);  // 2 CTAs per SM
-  if (a.n <= 4096) return launch_k<8, 512, 1>(a, st);  // 1 CTA per SM, 2 stages
+  if (a.n <= 4096) return launch_k<8, 512, 2>(a, st);  // 2 CTAs per SM, 1 stage each
   return launch_k<16, 512, 1>(a, st);
 }
 
