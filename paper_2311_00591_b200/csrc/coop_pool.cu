@@ -13,6 +13,7 @@
 // Readings R38-R44; bit-exact with the oracle O3.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stddef.h>
 #include <string.h>
 
 #include <algorithm>
@@ -142,12 +143,14 @@ __device__ __forceinline__ void pool_call(const PArgs &pa, Shared &sh) {
   if (pa.kind == PK_ALLOC || pa.kind == PK_REMAT) {
     // the op's inputs: the call's parents (alloc) or the recorded ones (remat)
     const int np = pa.kind == PK_ALLOC ? pa.n_parents : g.in_ptr[t + 1] - g.in_ptr[t];
-    const int32_t *par = pa.kind == PK_ALLOC ? pa.io_parents : g.in_idx + g.in_ptr[t];
+    // parents: copied once from mapped host memory (one PCIe round trip, all threads),
+    // then read from the device copy in the graph's edge list
+    const int32_t *par = g.in_idx + g.in_ptr[t];
     bool resident_now = false;
     if (pa.kind == PK_ALLOC) {
+      const int32_t e0 = g.in_ptr[t];
+      for (int j = tid; j < np; j += kThreads) g.in_idx[e0 + j] = pa.io_parents[j];
       if (tid == 0) {  // the new op / tensor t (read below with plain loads only)
-        const int32_t e0 = g.in_ptr[t];
-        for (int j = 0; j < np; ++j) g.in_idx[e0 + j] = par[j];
         g.in_ptr[t + 1] = e0 + np;
         g.size[t] = pa.size;
         g.producer[t] = t;
@@ -288,16 +291,18 @@ __global__ void __launch_bounds__(kThreads, 1) pool_kernel(const PArgs pa) {
 // host relaunches it on the next call.
 enum : int32_t { PK_STOP = 4, PK_FLUSH = 5 };
 
-struct Mailbox {  // mapped pinned host memory, written by the host (except done)
-  int64_t seq;
-  int32_t kind, t, src, n_parents;
+struct alignas(64) Mailbox {  // mapped pinned host memory, written by the host (except done)
+  int32_t kind, t, src, n_parents;  // arguments: bytes [0, 48), read as 3 x 16 bytes
   uint64_t size, adv;
   int64_t cost;
   uint32_t op_flags, pad0;
-  int64_t pad1[2];
+  int64_t seq;   // bumped by the host after the arguments
+  int64_t pad1;
   int64_t done;  // written by the device (own 64-byte line)
   int64_t pad2[7];
 };
+static_assert(offsetof(Mailbox, size) == 16 && offsetof(Mailbox, op_flags) == 40 &&
+              offsetof(Mailbox, seq) == 48 && offsetof(Mailbox, done) == 64, "mailbox layout");
 
 __device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
   int64_t v;
@@ -329,15 +334,23 @@ __global__ void __launch_bounds__(kThreads, 1) pool_service_kernel(const PArgs b
       }
       s_seq = s;
       if (go) {
+        // the 48 bytes of arguments after seq: three independent 16-byte loads in flight
+        // together (one PCIe round trip), ordered after the acquire of seq
+        uint64_t w[6];
+        const uint64_t *f = reinterpret_cast<const uint64_t *>(mb);
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          asm volatile("ld.relaxed.sys.global.v2.b64 {%0, %1}, [%2];"
+                       : "=l"(w[2 * q]), "=l"(w[2 * q + 1]) : "l"(f + 2 * q) : "memory");
         PArgs pa = base;
-        pa.kind = *(volatile int32_t *)&mb->kind;
-        pa.t = *(volatile int32_t *)&mb->t;
-        pa.src = *(volatile int32_t *)&mb->src;
-        pa.n_parents = *(volatile int32_t *)&mb->n_parents;
-        pa.size = *(volatile uint64_t *)&mb->size;
-        pa.adv = *(volatile uint64_t *)&mb->adv;
-        pa.cost = *(volatile int64_t *)&mb->cost;
-        pa.op_flags = *(volatile uint32_t *)&mb->op_flags;
+        pa.kind = (int32_t)(uint32_t)w[0];
+        pa.t = (int32_t)(uint32_t)(w[0] >> 32);
+        pa.src = (int32_t)(uint32_t)w[1];
+        pa.n_parents = (int32_t)(uint32_t)(w[1] >> 32);
+        pa.size = w[2];
+        pa.adv = w[3];
+        pa.cost = (int64_t)w[4];
+        pa.op_flags = (uint32_t)w[5];
         if (pa.kind == PK_STOP) go = 2;
         s_pa = pa;
       }
@@ -357,10 +370,9 @@ __global__ void __launch_bounds__(kThreads, 1) pool_service_kernel(const PArgs b
       break;
     }
     last = s_seq;
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      st_release_sys(&mb->done, last);
-    }
+    // the call's HostIO / victim writes (all threads, ordered by the barrier above) are
+    // published by one release store at system scope
+    if (threadIdx.x == 0) st_release_sys(&mb->done, last);
     if (go == 2) break;
   }
 }

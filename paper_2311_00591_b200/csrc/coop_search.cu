@@ -44,6 +44,7 @@ struct Scratch {
   uint64_t wS[kMaxWarps];
   double wH[kMaxWarps];
   double wU[kMaxWarps];
+  double wP[kMaxWarps];  // chunk-pruning upper bounds
   int32_t wF[kMaxWarps];
   int32_t wZ[kMaxWarps];
   uint64_t part[2][kMaxWarps][3];
@@ -578,13 +579,81 @@ __global__ void __launch_bounds__(MAXT, MINB)
         if (zmin != kInfIdx) {
           if (zi == zmin) write_result(a.out + p, zi, ze - 1, v.S_at(ze) - v.S_at(zi), 0.0, znev, COOP_OK);
         } else {
-        // ---------------- phase B: window ends (merge path), then the fp64 filter ----------
-        v.merge_path(tid, T);
+        // ---------------- phase B1: chunk pruning -------------------------------------------
+        // Thread t's starts i in [k0, kl] have ends e(i) >= e(k0) (monotone) and prefixes
+        // H[i] <= H[kl], so every window cost there is >= H[e(k0)] - H[kl].  e(k0) by one
+        // binary search per thread; the first start's window (when PINNED-free) gives an
+        // upper bound; chunks whose lower bound exceeds the CTA's best upper bound by more
+        // than the filter's margin cannot hold the winner (nor tie it after rounding) and
+        // skip the per-start work.  Bounds: |C^ - C| <= gerr (H^[e] + H^[i]) for any pair.
+        const int kl = min(k0 + K, n) - 1;
+        int e0 = n + 1;
+        double LBt = kInf, Ut = kInf;
+        if (k0 < n && !(barmask & 1u)) {
+          const uint64_t target = S_car + spre[0] + v.R;  // S[k0] + R  (< 2^63)
+          int lo = k0 + 1, hi = n + 1;                    // S[n + 1] = ~0 >= target
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (v.S_at(mid) >= target) hi = mid;
+            else lo = mid + 1;
+          }
+          e0 = lo;
+        } else if (k0 < n) {
+          e0 = -1;  // first start PINNED: no sample; ends of the others found below
+        }
+        if (k0 < n && e0 <= n) {
+          const int nb = barmask ? k0 + __ffs(barmask) - 1 : nb_right;
+          const double Hl = __dadd_rn(H_car, hpre[kl - k0]);
+          if (e0 >= 0) {
+            const double He = v.H_at(e0), Hk = __dadd_rn(H_car, hpre[0]);
+            if (nb >= e0) Ut = (He - Hk) + v.gerr * (He + Hk);
+            LBt = (He - Hl) - v.gerr * (He + Hl);
+          } else {
+            LBt = -kInf;  // no bound without e(k0): keep the chunk
+          }
+        }
+        {
+          const double uw = warp_allreduce(Ut, [](double x, double y) { return fmin(x, y); });
+          if (lane == 0) sc.wP[warp] = uw;
+        }
         __syncthreads();
+        const double Upre = warp_allreduce(lane < W ? sc.wP[lane] : kInf,
+                                           [](double x, double y) { return fmin(x, y); });
+        const bool survive = (k0 < n) && (e0 <= n) && !(LBt > Upre * (1.0 + 0x1p-45));
+        if (survive) {
+          // per-start ends of the chunk: a short walk from the previous end, binary search
+          // once the walk gets long
+          int eprev = e0 >= 0 ? e0 : k0 + 1;
+          for (int q = 0; q < K; ++q) {
+            const int i = k0 + q;
+            if (i >= n) break;
+            int e = eprev > i + 1 ? eprev : i + 1;
+            if (!(q == 0 && e0 >= 0)) {
+              const uint64_t target = S_car + spre[q] + v.R;
+              int steps = 0;
+              while (v.S_at(e) < target) {
+                ++e;
+                if (++steps == 8) {
+                  int lo = e, hi = n + 1;
+                  while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (v.S_at(mid) >= target) hi = mid;
+                    else lo = mid + 1;
+                  }
+                  e = lo;
+                  break;
+                }
+              }
+            }
+            v.E[i] = (uint16_t)e;
+            eprev = e;
+          }
+        }
         LaneBest bl;
         bl.U = kInf; bl.L = kInf; bl.L2 = kInf; bl.li = -1; bl.le = -1;
         bl.xb = ~0ull; bl.xi = kInfIdx; bl.xe = -1;
-        filter_starts<K, 0>(v, k0, barmask, nzmask, nb_right, nz_right, hpre, H_car, 0.0, 0, 0, sc, bl);
+        if (survive)
+          filter_starts<K, 0>(v, k0, barmask, nzmask, nb_right, nz_right, hpre, H_car, 0.0, 0, 0, sc, bl);
         const double Uw = warp_allreduce(bl.U, [](double x, double y) { return fmin(x, y); });
         const uint64_t xw = warp_allreduce(bl.xb, [](uint64_t x, uint64_t y) { return x < y ? x : y; });
         if (lane == 0) {
@@ -646,7 +715,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
               if (tid == 0) sc.ncand = 0;
               __syncthreads();
               const int w_lo = rd * kCandCap, w_hi = w_lo + kCandCap;
-              if (wmulti && k0 < w_hi && k0 + K > w_lo) {
+              if (wmulti && survive && k0 < w_hi && k0 + K > w_lo) {
                 LaneBest dummy = bl;
                 filter_starts<K, 1>(v, k0, barmask, nzmask, nb_right, nz_right, hpre, H_car, thresh, w_lo, w_hi, sc, dummy);
               }
