@@ -54,6 +54,7 @@ struct Scratch {
   int32_t bend[kMaxWarps];
   int32_t bnev[kMaxWarps];
   int32_t ncand;
+  int32_t nsurv;      // surviving chunks in the list (phase B1)
   int32_t xend, xnev;  // end / evictions of the best exactly-costed window
   uint32_t cand[kCandCap];
   unsigned long long mbar[2];
@@ -187,10 +188,10 @@ __device__ __forceinline__ bool better(uint64_t cb, int i, uint64_t bb, int bi) 
 //   region 0: S[k]   exclusive span prefix, k in [0, n]; S[n] = total span, S[n+1] = ~0
 //   region 1: H^[k]  fp64 prefix of h, k in [0, n]
 //   region 2: v[k]   h as binary64; FREE items stored as -0.0, PINNED items as NaN
-//   E[a]             (u16, scratch) window end of start a from the merge path
+//   list[c]          (uint4, scratch) surviving chunks of the pruning pass (phase B1)
 struct PoolView {
   smem_t *sr, *hr, *vr;
-  uint16_t *E;
+  uint4 *list;
   int32_t n;
   uint64_t R, S_total;
   double gerr;
@@ -199,33 +200,6 @@ struct PoolView {
   __device__ __forceinline__ double H_at(int x) const { return sm<double>(hr, swz((uint32_t)x)); }
   __device__ __forceinline__ double v_at(int x) const { return sm<double>(vr, swz((uint32_t)x)); }
 
-  // Window ends of all starts by a merge path of A[a] = S[a] + R (a < n) with B[b] = S[b]
-  // (b <= n): e(a) = #{b : S[b] < A[a]} = min{e : S[e] - S[a] >= R}, or n + 1 when no end
-  // exists.  The 2n + 1 steps are split evenly over the T threads (balanced whatever the
-  // item-size distribution); the sentinels S[n + 1] = ~0 and A[n] = S[n] + R > S[n] make
-  // every step branch-free.
-  __device__ __forceinline__ void merge_path(int t, int T) const {
-    const int L = 2 * n + 1;
-    const int D = (L + T - 1) / T;
-    const int d0 = min(t * D, L), d1 = min(d0 + D, L);
-    if (d0 >= d1) return;
-    int lo = max(0, d0 - (n + 1)), hi = min(d0, n);
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (S_at(mid) + R <= S_at(d0 - mid - 1)) lo = mid + 1;
-      else hi = mid;
-    }
-    int ai = lo, bi = d0 - lo;
-    uint64_t Av = S_at(ai) + R, Bv = S_at(bi);
-    for (int d = d0; d < d1; ++d) {
-      const bool takeA = Av <= Bv;  // start ai is complete: its window is [ai, bi - 1]
-      if (takeA) E[ai] = (uint16_t)bi;
-      const int x = takeA ? ++ai : ++bi;
-      const uint64_t sx = S_at(x);
-      Av = takeA ? sx + R : Av;
-      Bv = takeA ? Bv : sx;
-    }
-  }
 };
 
 // Per-thread running state of the filter.
@@ -236,69 +210,86 @@ struct LaneBest {
   int xi, xe;        //   ... its start (lowest among equal cost) and end
 };
 
-// The owner thread's filter over its K starts, ends from E[].  MODE 0 fills LaneBest;
-// MODE 1 appends the inexact starts in [w_lo, w_hi) whose lower bound is <= thresh.
-template <int K, int MODE>
-__device__ __forceinline__ void filter_starts(const PoolView &v, int k0, uint32_t barmask,
-                                              uint32_t nzmask, int nb_right, int nz_right,
-                                              const double (&hpre)[K], double H_car, double thresh,
-                                              int w_lo, int w_hi, Scratch &sc, LaneBest &b) {
+// A surviving chunk (phase B1): x = k0 | elo << 16 (elo <= e(i) for every start of the
+// chunk), y = PINNED mask | nonzero-h mask << 16 of its K items, z / w = first PINNED /
+// nonzero-h index to the right of the chunk.
+__device__ __forceinline__ uint4 chunk_rec(int k0, int elo, uint32_t barmask, uint32_t nzmask,
+                                           int nb_right, int nz_right) {
+  return make_uint4((uint32_t)k0 | ((uint32_t)elo << 16), barmask | (nzmask << 16),
+                    (uint32_t)nb_right, (uint32_t)nz_right);
+}
+
+// The filter for start i = k0 + q of a surviving chunk, run by any thread: window end by a
+// galloping search from elo, PINNED and zero-cost checks from the chunk masks, exact cost
+// for zero windows and windows of <= 2 items, else the fp64 prefix difference with its
+// bound.  MODE 0 folds the start into LaneBest (lexicographic (cost bits, start) for exact
+// windows, so the order in which a thread visits starts does not matter); MODE 1 appends
+// it to the candidate list when it is inexact, its lower bound is <= thresh and i lies in
+// [w_lo, w_hi).
+template <int MODE>
+__device__ __forceinline__ void eval_start(const PoolView &v, const uint4 rec, int q, double thresh,
+                                           int w_lo, int w_hi, Scratch &sc, LaneBest &b) {
   const int n = v.n;
-  uint16_t E[K];
-#pragma unroll
-  for (int q = 0; q < K; q += 8) {
-    const uint4 w = *reinterpret_cast<const uint4 *>(v.E + k0 + q);
-    E[q + 0] = (uint16_t)(w.x & 0xffffu); E[q + 1] = (uint16_t)(w.x >> 16);
-    E[q + 2] = (uint16_t)(w.y & 0xffffu); E[q + 3] = (uint16_t)(w.y >> 16);
-    E[q + 4] = (uint16_t)(w.z & 0xffffu); E[q + 5] = (uint16_t)(w.z >> 16);
-    E[q + 6] = (uint16_t)(w.w & 0xffffu); E[q + 7] = (uint16_t)(w.w >> 16);
-  }
-#pragma unroll
-  for (int q = 0; q < K; ++q) {
-    const int i = k0 + q;
-    if (i >= n) break;
-    if ((barmask >> q) & 1u) continue;
-    const int e = E[q];
-    if (e > n) break;  // this and every later start: no window covers R
-    const uint32_t mb = barmask >> q, mz = nzmask >> q;
-    const int nb = mb ? i + __ffs(mb) - 1 : nb_right;
-    if (nb < e) continue;  // a PINNED item inside [i, e-1]
-    const int nz = mz ? i + __ffs(mz) - 1 : nz_right;
-    const int len = e - i;
-    // exact cost for zero-cost windows (only h = 0 items) and windows of <= 2 items (one
-    // IEEE add is correctly rounded); otherwise the fp64 prefix difference with its bound
-    const bool zero = nz >= e;
-    const bool exact = zero || len <= 2;
-    const double h0 = fabs(v.v_at(i));
-    const double h1 = len >= 2 ? fabs(v.v_at(i + 1)) : 0.0;
-    const double He = v.H_at(e), Hi = __dadd_rn(H_car, hpre[q]);
-    const double Cx = zero ? 0.0 : __dadd_rn(h0, h1);
-    const double C = exact ? Cx : He - Hi;
-    const double err = exact ? 0.0 : v.gerr * (He + Hi);
-    const double Lb = C - err;
-    if (MODE == 0) {
-      if (exact) {
-        const uint64_t cb = (uint64_t)__double_as_longlong(C);
-        if (cb < b.xb) {  // starts ascend: ties keep the lower start
-          b.xb = cb;
-          b.xi = i;
-          b.xe = e;
-        }
-      } else {
-        b.U = fmin(b.U, C + err);
-        if (Lb < b.L) {
-          b.L2 = b.L;
-          b.L = Lb;
-          b.li = i;
-          b.le = e;
-        } else {
-          b.L2 = fmin(b.L2, Lb);
-        }
-      }
-    } else if (!exact && Lb <= thresh && i >= w_lo && i < w_hi) {
-      const int slot = atomicAdd(&sc.ncand, 1);
-      if (slot < kCandCap) sc.cand[slot] = ((uint32_t)i << 16) | (uint32_t)(e - i);  // n <= 8192
+  const int k0 = (int)(rec.x & 0xffffu), elo = (int)(rec.x >> 16);
+  const uint32_t barmask = rec.y & 0xffffu, nzmask = rec.y >> 16;
+  const int i = k0 + q;
+  if (i >= n || ((barmask >> q) & 1u)) return;
+  const uint64_t target = v.S_at(i) + v.R;  // < 2^63
+  int lo = max(elo, i + 1), e;
+  if (v.S_at(lo) >= target) {
+    e = lo;
+  } else {  // S[lo] < target <= S[n + 1] = ~0: gallop, then bisect (lo, hi]
+    int step = 1, hi = min(lo + 1, n + 1);
+    while (v.S_at(hi) < target) {
+      lo = hi;
+      step <<= 1;
+      hi = min(lo + step, n + 1);
     }
+    ++lo;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (v.S_at(mid) >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    e = hi;
+  }
+  if (e > n) return;  // no window covers R from i (nor from any later start)
+  const uint32_t mb = barmask >> q, mz = nzmask >> q;
+  const int nb = mb ? i + __ffs(mb) - 1 : (int)rec.z;
+  if (nb < e) return;  // a PINNED item inside [i, e-1]
+  const int nz = mz ? i + __ffs(mz) - 1 : (int)rec.w;
+  const int len = e - i;
+  const bool zero = nz >= e;
+  const bool exact = zero || len <= 2;
+  const double h0 = fabs(v.v_at(i));
+  const double h1 = len >= 2 ? fabs(v.v_at(i + 1)) : 0.0;
+  const double He = v.H_at(e), Hi = v.H_at(i);
+  const double Cx = zero ? 0.0 : __dadd_rn(h0, h1);
+  const double C = exact ? Cx : He - Hi;
+  const double err = exact ? 0.0 : v.gerr * (He + Hi);
+  const double Lb = C - err;
+  if (MODE == 0) {
+    if (exact) {
+      const uint64_t cb = (uint64_t)__double_as_longlong(C);
+      if (better(cb, i, b.xb, b.xi)) {
+        b.xb = cb;
+        b.xi = i;
+        b.xe = e;
+      }
+    } else {
+      b.U = fmin(b.U, C + err);
+      if (Lb < b.L) {
+        b.L2 = b.L;
+        b.L = Lb;
+        b.li = i;
+        b.le = e;
+      } else {
+        b.L2 = fmin(b.L2, Lb);
+      }
+    }
+  } else if (!exact && Lb <= thresh && i >= w_lo && i < w_hi) {
+    const int slot = atomicAdd(&sc.ncand, 1);
+    if (slot < kCandCap) sc.cand[slot] = ((uint32_t)i << 16) | (uint32_t)(e - i);  // n <= 8192
   }
 }
 
@@ -373,7 +364,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
   const uint32_t base = (raw + 1023u) & ~1023u;
   smem_t *base_ptr = smem_raw + (base - raw);
   Scratch &sc = *reinterpret_cast<Scratch *>(base_ptr + (size_t)a.stages * a.stage_bytes);
-  uint16_t *Ebuf = reinterpret_cast<uint16_t *>(base_ptr + (size_t)a.stages * a.stage_bytes +
+  uint4 *Ebuf = reinterpret_cast<uint4 *>(base_ptr + (size_t)a.stages * a.stage_bytes +
                                                  (sizeof(Scratch) + 15) / 16 * 16);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -410,7 +401,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
     v.sr = stage;
     v.hr = stage + a.region_bytes;
     v.vr = stage + 2u * a.region_bytes;
-    v.E = Ebuf;
+    v.list = Ebuf;
     v.n = n;
     v.R = Rraw < kRClamp ? Rraw : kRClamp;
     v.gerr = a.gerr;
@@ -603,7 +594,11 @@ __global__ void __launch_bounds__(MAXT, MINB)
         }
         if (k0 < n && e0 <= n) {
           const int nb = barmask ? k0 + __ffs(barmask) - 1 : nb_right;
-          const double Hl = __dadd_rn(H_car, hpre[kl - k0]);
+          double hl = hpre[0];  // hpre[kl - k0] with constant indices (stays in registers)
+#pragma unroll
+          for (int q = 1; q < K; ++q)
+            if (k0 + q <= kl) hl = hpre[q];
+          const double Hl = __dadd_rn(H_car, hl);
           if (e0 >= 0) {
             const double He = v.H_at(e0), Hk = __dadd_rn(H_car, hpre[0]);
             if (nb >= e0) Ut = (He - Hk) + v.gerr * (He + Hk);
@@ -615,45 +610,29 @@ __global__ void __launch_bounds__(MAXT, MINB)
         {
           const double uw = warp_allreduce(Ut, [](double x, double y) { return fmin(x, y); });
           if (lane == 0) sc.wP[warp] = uw;
+          if (tid == 0) sc.nsurv = 0;
         }
         __syncthreads();
         const double Upre = warp_allreduce(lane < W ? sc.wP[lane] : kInf,
                                            [](double x, double y) { return fmin(x, y); });
         const bool survive = (k0 < n) && (e0 <= n) && !(LBt > Upre * (1.0 + 0x1p-45));
-        if (survive) {
-          // per-start ends of the chunk: a short walk from the previous end, binary search
-          // once the walk gets long
-          int eprev = e0 >= 0 ? e0 : k0 + 1;
-          for (int q = 0; q < K; ++q) {
-            const int i = k0 + q;
-            if (i >= n) break;
-            int e = eprev > i + 1 ? eprev : i + 1;
-            if (!(q == 0 && e0 >= 0)) {
-              const uint64_t target = S_car + spre[q] + v.R;
-              int steps = 0;
-              while (v.S_at(e) < target) {
-                ++e;
-                if (++steps == 8) {
-                  int lo = e, hi = n + 1;
-                  while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (v.S_at(mid) >= target) hi = mid;
-                    else lo = mid + 1;
-                  }
-                  e = lo;
-                  break;
-                }
-              }
-            }
-            v.E[i] = (uint16_t)e;
-            eprev = e;
-          }
+        {  // compact the surviving chunks (one shared atomic per warp)
+          const uint32_t bal = __ballot_sync(0xffffffffu, survive);
+          int wbase = 0;
+          if (lane == 0 && bal) wbase = atomicAdd(&sc.nsurv, __popc(bal));
+          wbase = __shfl_sync(0xffffffffu, wbase, 0);
+          if (survive)
+            v.list[wbase + __popc(bal & ((1u << lane) - 1u))] =
+                chunk_rec(k0, e0 >= 0 ? e0 : k0 + 1, barmask, nzmask, nb_right, nz_right);
         }
+        __syncthreads();
+        // every start of the surviving chunks, spread evenly over the CTA's threads
+        const int nslots = sc.nsurv * K;
         LaneBest bl;
         bl.U = kInf; bl.L = kInf; bl.L2 = kInf; bl.li = -1; bl.le = -1;
         bl.xb = ~0ull; bl.xi = kInfIdx; bl.xe = -1;
-        if (survive)
-          filter_starts<K, 0>(v, k0, barmask, nzmask, nb_right, nz_right, hpre, H_car, 0.0, 0, 0, sc, bl);
+        for (int sl = tid; sl < nslots; sl += T)
+          eval_start<0>(v, v.list[sl / K], sl % K, 0.0, 0, 0, sc, bl);
         const double Uw = warp_allreduce(bl.U, [](double x, double y) { return fmin(x, y); });
         const uint64_t xw = warp_allreduce(bl.xb, [](uint64_t x, uint64_t y) { return x < y ? x : y; });
         if (lane == 0) {
@@ -715,9 +694,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
               if (tid == 0) sc.ncand = 0;
               __syncthreads();
               const int w_lo = rd * kCandCap, w_hi = w_lo + kCandCap;
-              if (wmulti && survive && k0 < w_hi && k0 + K > w_lo) {
+              if (wmulti) {
                 LaneBest dummy = bl;
-                filter_starts<K, 1>(v, k0, barmask, nzmask, nb_right, nz_right, hpre, H_car, thresh, w_lo, w_hi, sc, dummy);
+                for (int sl = tid; sl < nslots; sl += T)
+                  eval_start<1>(v, v.list[sl / K], sl % K, thresh, w_lo, w_hi, sc, dummy);
               }
               __syncthreads();
             }
@@ -879,7 +859,7 @@ int launch_k(const Args &a0, cudaStream_t st) {
   int max_smem = 0, sms = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t fixed = (sizeof(Scratch) + 15) / 16 * 16 + ((size_t)threads * K + 16) * 2 + 1024;  // + E[]
+  const size_t fixed = (sizeof(Scratch) + 15) / 16 * 16 + (size_t)threads * 16 + 1024;  // + chunk list
   // MINB CTAs per SM share the SM's shared memory (228 KiB less 1 KiB per CTA reserved);
   // each CTA double-buffers only if that still fits
   size_t per_cta = (size_t)max_smem;
