@@ -114,8 +114,10 @@ int coop_window_search_batched(const coop_tables_soa *t, const uint64_t *request
  * library streams chunks of pools host->device, searches them and copies the results
  * back, overlapping the copies with the kernel on two internal streams.  Host arrays
  * should be pinned (cudaHostAlloc / torch pin_memory) for full copy bandwidth.
- * Allocates (and frees before returning) device staging of at most chunk_pools pools
- * x 2 buffers; chunk_pools <= 0 selects a default.  Synchronous.
+ * Uses a per-device staging workspace of chunk_pools pools x 2 buffers, allocated on
+ * first use (or grown for a larger chunk) and kept for later calls, so steady-state calls
+ * make no device allocation; chunk_pools <= 0 selects a default (16384).  Synchronous;
+ * calls are serialised process-wide.
  * Returns as coop_window_search_batched, or COOP_ERR_NOMEM.
  */
 int coop_window_search_batched_host(const coop_tables_soa *host_tables,

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "coop.h"
 #include "coop_internal.h"
 
@@ -63,19 +65,53 @@ extern "C" int coop_window_search_batched_host(const coop_tables_soa *ht,
   if (chunk_pools > P) chunk_pools = P;
 
   const size_t arr_bytes = (size_t)chunk_pools * dstride * 8;
-  void *buf[2][5] = {{nullptr}};
-  cudaStream_t st[2] = {nullptr, nullptr};
+  // staging workspace: per device, grown on demand and reused by later calls (no device
+  // allocation on the steady-state path); one caller at a time per process
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  struct Staging {
+    void *buf[2][5] = {{nullptr}};
+    cudaStream_t st[2] = {nullptr, nullptr};
+    size_t arr_bytes = 0, pools = 0;
+  };
+  static Staging ws[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return COOP_ERR_CUDA;
+  Staging &W = ws[dev];
   int status = COOP_OK;
-  for (int b = 0; b < 2 && status == COOP_OK; ++b) {
-    if (cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking) != cudaSuccess) status = COOP_ERR_CUDA;
-    for (int a = 0; a < 3 && status == COOP_OK; ++a)
-      if (cudaMalloc(&buf[b][a], arr_bytes) != cudaSuccess) status = COOP_ERR_NOMEM;
-    if (status == COOP_OK && cudaMalloc(&buf[b][3], (size_t)chunk_pools * 8) != cudaSuccess)
-      status = COOP_ERR_NOMEM;
-    if (status == COOP_OK &&
-        cudaMalloc(&buf[b][4], (size_t)chunk_pools * sizeof(coop_window)) != cudaSuccess)
-      status = COOP_ERR_NOMEM;
+  if (W.arr_bytes < arr_bytes || W.pools < (size_t)chunk_pools) {
+    for (int b = 0; b < 2; ++b)
+      for (int a = 0; a < 5; ++a)
+        if (W.buf[b][a]) {
+          cudaFree(W.buf[b][a]);
+          W.buf[b][a] = nullptr;
+        }
+    W.arr_bytes = W.pools = 0;
+    for (int b = 0; b < 2 && status == COOP_OK; ++b) {
+      if (!W.st[b] && cudaStreamCreateWithFlags(&W.st[b], cudaStreamNonBlocking) != cudaSuccess)
+        status = COOP_ERR_CUDA;
+      for (int a = 0; a < 3 && status == COOP_OK; ++a)
+        if (cudaMalloc(&W.buf[b][a], arr_bytes) != cudaSuccess) status = COOP_ERR_NOMEM;
+      if (status == COOP_OK && cudaMalloc(&W.buf[b][3], (size_t)chunk_pools * 8) != cudaSuccess)
+        status = COOP_ERR_NOMEM;
+      if (status == COOP_OK &&
+          cudaMalloc(&W.buf[b][4], (size_t)chunk_pools * sizeof(coop_window)) != cudaSuccess)
+        status = COOP_ERR_NOMEM;
+    }
+    if (status != COOP_OK) {
+      for (int b = 0; b < 2; ++b)
+        for (int a = 0; a < 5; ++a)
+          if (W.buf[b][a]) {
+            cudaFree(W.buf[b][a]);
+            W.buf[b][a] = nullptr;
+          }
+      return status;
+    }
+    W.arr_bytes = arr_bytes;
+    W.pools = (size_t)chunk_pools;
   }
+  void *(&buf)[2][5] = W.buf;
+  cudaStream_t *st = W.st;
   const void *src[3] = {ht->size_state, ht->cost, ht->stale};
   for (int64_t c0 = 0, ci = 0; c0 < P && status == COOP_OK; c0 += chunk_pools, ++ci) {
     const int b = (int)(ci & 1);
@@ -106,14 +142,8 @@ extern "C" int coop_window_search_batched_host(const coop_tables_soa *ht,
                         cudaMemcpyDeviceToHost, st[b]) != cudaSuccess)
       status = COOP_ERR_CUDA;
   }
-  for (int b = 0; b < 2; ++b) {
-    if (st[b]) {
-      if (cudaStreamSynchronize(st[b]) != cudaSuccess && status == COOP_OK) status = COOP_ERR_CUDA;
-      cudaStreamDestroy(st[b]);
-    }
-    for (int a = 0; a < 5; ++a)
-      if (buf[b][a]) cudaFree(buf[b][a]);
-  }
+  for (int b = 0; b < 2; ++b)
+    if (cudaStreamSynchronize(st[b]) != cudaSuccess && status == COOP_OK) status = COOP_ERR_CUDA;
   return status;
 }
 
