@@ -33,6 +33,11 @@ namespace coop {
 
 namespace {
 
+#ifdef COOP_SEARCH_PHASE_HOOKS
+constexpr bool kPhaseHooks = true;  // COOP_SEARCH_DBG = 3..6 (profiling builds only)
+#else
+constexpr bool kPhaseHooks = false;
+#endif
 constexpr int kCandCap = 512;  // fits two 512-thread CTAs (one stage each) per SM at N = 4096
 constexpr int kMaxWarps = 16;
 constexpr uint64_t kSizeMask = (1ull << 62) - 1ull;
@@ -75,8 +80,9 @@ struct Args {
   uint32_t stage_bytes;
   int32_t stages;
   int32_t use_tma;
-  int32_t dbg;  // profiling hook (COOP_SEARCH_DBG): stop each pool after 1 = load, 2/3 = phase A +
-                // scan + write-back, 4 = zero pass, 5 = pruning + compaction, 6 = filter + reductions
+  int32_t dbg;  // profiling hook (COOP_SEARCH_DBG): stop each pool after 1 = load, 2 = phase A +
+                // scan + write-back; with -DCOOP_SEARCH_PHASE_HOOKS also 3 = write-back,
+                // 4 = zero pass, 5 = pruning + compaction, 6 = filter + reductions
   double gerr;  // filter error coefficient: |C^ - C| <= gerr * (H^[e] + H^[i])
 };
 
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
       if (bad_any || a.dbg == 2) {
         if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_ERR_INVALID_ARG);
       } else {
-        if (a.dbg == 3) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
+        if (kPhaseHooks && a.dbg == 3) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
         // ---------------- phase B0: zero-cost windows -------------------------------------
         // A run of consecutive h = 0 items (FREE, or EVICTABLE with c = 0) is a zero-cost
         // window iff its span covers R; the lowest such run head is the answer (exact cost
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
         if (lane == 0) sc.wZ[warp] = zw;
         __syncthreads();
         const int zmin = warp_allreduce(lane < W ? sc.wZ[lane] : kInfIdx, [](int x, int y) { return min(x, y); });
-        if (a.dbg == 4) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
+        if (kPhaseHooks && a.dbg == 4) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
         if (zmin != kInfIdx) {
           if (zi == zmin) write_result(a.out + p, zi, ze - 1, v.S_at(ze) - v.S_at(zi), 0.0, znev, COOP_OK);
         } else {
@@ -629,7 +635,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
                 chunk_rec(k0, e0 >= 0 ? e0 : k0 + 1, barmask, nzmask, nb_right, nz_right);
         }
         __syncthreads();
-        if (a.dbg == 5) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
+        if (kPhaseHooks && a.dbg == 5) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
         // every start of the surviving chunks, spread evenly over the CTA's threads
         const int nslots = sc.nsurv * K;
         LaneBest bl;
@@ -650,7 +656,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
         const uint64_t xbest = warp_allreduce(lane < W ? sc.bcost[lane] : ~0ull,
                                               [](uint64_t x, uint64_t y) { return x < y ? x : y; });
         const double thresh = fmin(Umin, __longlong_as_double((long long)xbest)) * (1.0 + 0x1p-45);
-        if (a.dbg == 6) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
+        if (kPhaseHooks && a.dbg == 6) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
         // a lane with exactly one start under the threshold appends it; two or more re-walk
         const bool multi = (bl.L2 <= thresh);
         if (bl.L <= thresh && !multi) {
