@@ -434,7 +434,7 @@ def main():
             "frac": achieved / peak, "peak_source": peak_src,
             "traffic": (tr["dram_bytes_per_pool"] * P) if tr else None,
             "algorithmic_bytes_per_launch": P * ALGO_BYTES_PER_POOL,
-            "kernel": "coop::search_kernel<8>", "kernel_ms_mean": kmean,
+            "kernel": "coop::search_kernel<8,512,2>", "kernel_ms_mean": kmean,
             "frac_of_8TBps": achieved / 8000.0}
     replay = None
     if not args.no_replay:

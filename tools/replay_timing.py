@@ -21,3 +21,7 @@ for name in (sys.argv[2].split(",") if len(sys.argv) > 2 else dnn.DNNS):
     print(f"{name:13s} cells {len(budgets)} ops {tr.n_ops} wall {dt*1e3:9.1f} ms  ok {(r['status']==0).sum()} "
           f"remat {r['remat'].sum()} evict {r['evictions'].sum()} press {r['pressure'].sum()} "
           f"ops/s {len(budgets)*tr.n_ops/dt:.3g}", flush=True)
+    top = np.argsort(-r["search_ns_total"])[:4]
+    print("   slowest cells (k, budget frac, search s, pressure, remat, status):",
+          [(int(k * (256 // nb)), round(budgets[k] / peak, 3), round(r["search_ns_total"][k] / 1e9, 2),
+            int(r["pressure"][k]), int(r["remat"][k]), int(r["status"][k])) for k in top], flush=True)
