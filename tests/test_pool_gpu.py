@@ -166,3 +166,17 @@ def test_service_idle_exit_and_relaunch():
     assert PM.drive(Toggling(g), calls) == PM.drive(o, calls)
     _same_state(g, o)
     g.close()
+
+
+def test_service_invalid_timeout_and_stats_flush():
+    """coop_pool_service argument check; stats / layout read the live state of a resident
+    service kernel (flush) and agree with the oracle mid-session"""
+    coop = _coop()
+    g = coop.Pool(300, 3)
+    assert coop.lib.coop_pool_service(g.handle, 10000001) == coop.ERR_INVALID_ARG
+    g.service(50000)
+    o = O.Pool(300, 3)
+    calls = PM.random_session(31337, 60, budget=300, flags=3)
+    assert PM.drive(g, calls) == PM.drive(o, calls)
+    _same_state(g, o)  # while the kernel is resident
+    g.close()
