@@ -1,0 +1,4 @@
+timeout 900 ncu --section SourceCounters --section WarpStateStats --section SchedulerStats --clock-control none --import-source on -k regex:replay_kernel -c 1 -o gpurun_out/replay_bilstm -f python tools/replay_one.py bilstm 0.351 > gpurun_out/ncu_bilstm.out 2>&1
+tail -3 gpurun_out/ncu_bilstm.out
+ncu -i gpurun_out/replay_bilstm.ncu-rep --page source --csv --print-source sass > gpurun_out/replay_bilstm_sass.csv 2>/dev/null
+ls -la gpurun_out/replay_bilstm*
