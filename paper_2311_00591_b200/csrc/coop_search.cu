@@ -537,27 +537,32 @@ __global__ void __launch_bounds__(MAXT, MINB)
           const uint32_t valid = cnt >= K ? (K == 32 ? ~0u : ((1u << K) - 1u)) : (cnt > 0 ? (1u << cnt) - 1u : 0u);
           const uint32_t zm = valid & ~barmask & ~nzmask;
           const uint32_t heads = zm & ~(zm << 1);
-          int zstop = n;
+          // items that alone cover R (sizes from the prefix registers; the chunk's last
+          // item is left to the span test below)
+          uint32_t cov = 0;
 #pragma unroll
-          for (int q = 0; q < K; ++q) {
-            if (zi != kInfIdx || !((heads >> q) & 1u)) continue;
-            if (q + 1 < K && !((zm >> (q + 1)) & 1u)) {
-              // a one-item run inside the chunk (the common case: FREE items are isolated):
-              // its span is the item's size, from the thread's own prefix registers
-              if (spre[q + 1 < K ? q + 1 : q] - spre[q] >= v.R) {
-                zi = k0 + q;
-                zstop = k0 + q + 1;
-              }
-              continue;
-            }
+          for (int q = 0; q + 1 < K; ++q) cov |= (uint32_t)(spre[q + 1] - spre[q] >= v.R) << q;
+          const uint32_t one = heads & cov;  // zero windows [q, q]
+          const uint32_t lower = one ? (1u << (__ffs(one) - 1)) - 1u : ~0u;
+          // heads below the first of them whose run may be longer than one item
+          uint32_t multi = heads & ~one & lower & ((zm >> 1) | (1u << (K - 1)));
+          int zstop = n;
+          while (multi) {
+            const int q = __ffs(multi) - 1;
+            multi &= multi - 1u;
             const uint32_t mb = barmask >> q, mz = nzmask >> q;
             const int nb = mb ? k0 + q + __ffs(mb) - 1 : nb_right;
             const int nz = mz ? k0 + q + __ffs(mz) - 1 : nz_right;
             const int stop = min(min(nb, nz), n);
-            if (v.S_at(stop) - (S_car + spre[q]) >= v.R) {
+            if (v.S_at(stop) - v.S_at(k0 + q) >= v.R) {
               zi = k0 + q;
               zstop = stop;
+              break;
             }
+          }
+          if (zi == kInfIdx && one) {
+            zi = k0 + __ffs(one) - 1;
+            zstop = zi + 1;
           }
           if (zi != kInfIdx) {
             const uint64_t target = v.S_at(zi) + v.R;
