@@ -356,6 +356,13 @@ struct Cell {
     const uint8_t f = sh.tfl[d];
     return (f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD);
   }
+  // push-time filter: only nodes that can pass the pop-time test are pushed (and marked);
+  // the pop-time test stays, so the visited set and the sums are unchanged (resident
+  // neighbours such as parameters were pushed, popped and rejected before)
+  __device__ __forceinline__ bool dfs_elig(int y, int stage) const {
+    const uint8_t f = sh.tfl[y];
+    return stage == 0 ? !(f & TF_RES) : ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD));
+  }
   static __device__ __forceinline__ int64_t rec_cost(const int4 r) {
     return (int64_t)(((uint64_t)(uint32_t)r.y << 32) | (uint32_t)r.x);
   }
@@ -375,7 +382,7 @@ struct Cell {
           stage = 1;
           for (int e = __ldg(&tr.cons_head[t]); e >= 0; e = __ldg(&tr.cons_next[e])) {
             const int y = __ldg(&tr.cons_out[e]);
-            if (mk[y] != ep) {
+            if (dfs_elig(y, 1) && mk[y] != ep) {
               mk[y] = ep;
               stk[sp++] = y;
             }
@@ -411,7 +418,7 @@ struct Cell {
         stage = 0;
         for (int j = r.z; j < r.w; ++j) {
           const int y = __ldg(&tr.in_idx[j]);
-          if (mk[y] != ep) {
+          if (dfs_elig(y, 0) && mk[y] != ep) {
             mk[y] = ep;
             stk[sp++] = y;
           }
@@ -435,7 +442,7 @@ struct Cell {
 #pragma unroll
           for (int k = 0; k < 4; ++k) y[k] = j0 + k < r.w ? __ldg(&tr.in_idx[j0 + k]) : -1;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) m[k] = y[k] >= 0 ? mk[y[k]] : ep;
+          for (int k = 0; k < 4; ++k) m[k] = (y[k] >= 0 && dfs_elig(y[k], 0)) ? mk[y[k]] : ep;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             bool fresh = m[k] != ep;
@@ -450,7 +457,7 @@ struct Cell {
       } else {
         for (int e = __ldg(&tr.cons_head[x]); e >= 0; e = __ldg(&tr.cons_next[e])) {
           const int y = __ldg(&tr.cons_out[e]);
-          if (mk[y] != ep) {
+          if (dfs_elig(y, 1) && mk[y] != ep) {
             mk[y] = ep;
             stk[sp++] = y;
           }
