@@ -351,7 +351,7 @@ struct Cell {
   // stay busy whatever the closure sizes), switches a candidate from its ancestors to its
   // descendants, or pops one DFS node.  No nested data-dependent loops, so the lanes of a
   // warp stay converged while their closures differ in size.  Visited marks: per-thread
-  // epoch words in global memory (one epoch per candidate).
+  // epoch bytes in global memory (one epoch per candidate, cleared every 255).
   __device__ __forceinline__ bool down_ok(int d) const {  // evicted and live
     const uint8_t f = sh.tfl[d];
     return (f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD);
@@ -371,11 +371,13 @@ struct Cell {
   // A node is marked when pushed, so every node enters a candidate's stack at most once:
   // the per-thread stack (global workspace, T entries) cannot overflow.
   __device__ void projected_costs(const int32_t *cand, int ncand, int pol = 0) {
-    uint32_t *mk = w.marks + (size_t)threadIdx.x * tr.T;
+    // visited marks: one byte per tensor and thread (epoch & 255; cleared on wrap), four
+    // times denser than word epochs so a walking thread's marks stay in L1
+    uint8_t *mk = reinterpret_cast<uint8_t *>(w.marks) + (size_t)threadIdx.x * tr.T;
     int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
     int sp = 0, ci = -1, t = -1, stage = 0;
     int64_t acc = 0;
-    uint32_t ep = 0;
+    uint8_t ep = 0;
     while (true) {
       if (sp == 0) {
         if (ci >= 0 && stage == 0) {  // ancestors done: the descendants' roots
@@ -409,10 +411,10 @@ struct Cell {
         t = O()[cand[ci]];
         const int4 r = __ldg(&tr.rec[t]);
         acc = rec_cost(r);
-        ep = ++epoch;
-        if (ep == 0) {  // epoch wrap: clear this thread's marks (never in practice)
+        ep = (uint8_t)++epoch;
+        if (ep == 0) {  // epoch wrap (every 255 candidates): clear this thread's marks
           for (int x = 0; x < tr.T; ++x) mk[x] = 0u;
-          ep = epoch = 1;
+          ep = (uint8_t)++epoch;
         }
         mk[t] = ep;
         stage = 0;
@@ -438,7 +440,7 @@ struct Cell {
         // (duplicates inside a batch are skipped explicitly: their marks were read early)
         for (int j0 = r.z; j0 < r.w; j0 += 4) {
           int y[4];
-          uint32_t m[4];
+          uint8_t m[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) y[k] = j0 + k < r.w ? __ldg(&tr.in_idx[j0 + k]) : -1;
 #pragma unroll
@@ -1008,7 +1010,7 @@ WsLayout make_layout(int T) {
   L.last_access = take((size_t)T * 8);
   L.taddr = take((size_t)T * 8);
   L.epochs = take((size_t)kThreads * 4);
-  L.marks = take((size_t)kThreads * T * 4);
+  L.marks = take((size_t)kThreads * T);  // one byte per tensor and thread
   L.stack = take((size_t)kThreads * T * 4);
   L.isz = take((size_t)(kCap + 1) * 8);
   L.ih = take((size_t)(kCap + 1) * 8);
