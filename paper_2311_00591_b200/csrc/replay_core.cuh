@@ -55,7 +55,7 @@ struct TraceDev {
 };
 
 struct WsLayout {  // byte offsets inside one cell's workspace
-  size_t tflags, pins, last_access, taddr, epochs, marks, stack, isz, ih, ist, S, H, B, trans, victims, cand;
+  size_t tflags, pins, last_access, taddr, epochs, marks, stack, isz, ih, ist, S, H, B, trans, victims, cand, pacc;
   size_t bytes;
 };
 
@@ -74,6 +74,7 @@ struct CellPtrs {
   int32_t *B;
   int32_t *trans, *victims;
   int32_t *cand;
+  int64_t *pacc;  // per (candidate, half) closure sums of the current pressure event
 };
 
 struct KArgs {
@@ -203,6 +204,7 @@ struct Cell {
     w.trans = (int32_t *)(base + a.lay.trans);
     w.victims = (int32_t *)(base + a.lay.victims);
     w.cand = (int32_t *)(base + a.lay.cand);
+    w.pacc = (int64_t *)(base + a.lay.pacc);
     log = a.log ? a.log + (size_t)cell * a.log_cap : nullptr;
   }
 
@@ -368,61 +370,52 @@ struct Cell {
   }
 
   // cand[0..ncand): block indices of EVICTABLE items; writes w.ih[b] = RN(c(t) / s(t)).
-  // A node is marked when pushed, so every node enters a candidate's stack at most once:
-  // the per-thread stack (global workspace, T entries) cannot overflow.
+  // The work items are (candidate, half): half 0 sums Anc(t), half 1 sums Desc(t) -- in a
+  // DAG the two sets are disjoint, so they are independent walks that different threads
+  // take up (finer items balance long chains better); the integer sums meet in w.pacc and
+  // one pass after a barrier forms c(t) and h.  A node is marked when pushed, so every
+  // node enters a walk's stack at most once: the per-thread stack (T entries) cannot
+  // overflow.
   __device__ void projected_costs(const int32_t *cand, int ncand, int pol = 0) {
     // visited marks: one byte per tensor and thread (epoch & 255; cleared on wrap), four
     // times denser than word epochs so a walking thread's marks stay in L1
-    uint8_t *mk = reinterpret_cast<uint8_t *>(w.marks) + (size_t)threadIdx.x * tr.T;
+    const int Tp = (tr.T + 15) & ~15;  // per-thread stride, 16-byte aligned (uint4 clears)
+    uint8_t *mk = reinterpret_cast<uint8_t *>(w.marks) + (size_t)threadIdx.x * Tp;
     int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
-    int sp = 0, ci = -1, t = -1, stage = 0;
+    const int nitems = 2 * ncand;
+    int sp = 0, it = -1, stage = 0;
     int64_t acc = 0;
     uint8_t ep = 0;
     while (true) {
       if (sp == 0) {
-        if (ci >= 0 && stage == 0) {  // ancestors done: the descendants' roots
-          stage = 1;
+        if (it >= 0) w.pacc[it] = acc;
+        it = atomicAdd(&sh.cand_next, 1);
+        if (it >= nitems) break;
+        const int t = O()[cand[it >> 1]];
+        stage = it & 1;
+        acc = 0;
+        ep = (uint8_t)++epoch;
+        if (ep == 0) {  // epoch wrap (every 255 walks): clear this thread's marks
+          for (int x = 0; x < Tp; x += 16) *reinterpret_cast<uint4 *>(mk + x) = make_uint4(0, 0, 0, 0);
+          ep = (uint8_t)++epoch;
+        }
+        mk[t] = ep;
+        if (stage == 0) {  // the ancestors' roots: t's producer's inputs
+          const int4 r = __ldg(&tr.rec[t]);
+          for (int j = r.z; j < r.w; ++j) {
+            const int y = __ldg(&tr.in_idx[j]);
+            if (dfs_elig(y, 0) && mk[y] != ep) {
+              mk[y] = ep;
+              stk[sp++] = y;
+            }
+          }
+        } else {  // the descendants' roots: the outputs of t's consumers
           for (int e = __ldg(&tr.cons_head[t]); e >= 0; e = __ldg(&tr.cons_next[e])) {
             const int y = __ldg(&tr.cons_out[e]);
             if (dfs_elig(y, 1) && mk[y] != ep) {
               mk[y] = ep;
               stk[sp++] = y;
             }
-          }
-          if (sp > 0) continue;
-        }
-        if (ci >= 0) {
-          const int b = cand[ci];
-          int64_t s = sh.clock - w.last_access[t];  // staleness (R17)
-          if (s < 1) s = 1;
-          double den = (double)s;  // Coop: h = c/s (R1)
-          if (pol) {               // DTR: c / (m s); DTE: m + the adjacent free bytes (R46)
-            uint64_t m = Z()[b];
-            if (pol == 2) {
-              if (b > 0 && O()[b - 1] == kFree) m += Z()[b - 1];
-              if (b + 1 < sh.nb && O()[b + 1] == kFree) m += Z()[b + 1];
-            }
-            den = __dmul_rn((double)m, (double)s);
-          }
-          w.ih[b] = __ddiv_rn((double)acc, den);
-        }
-        ci = atomicAdd(&sh.cand_next, 1);
-        if (ci >= ncand) break;
-        t = O()[cand[ci]];
-        const int4 r = __ldg(&tr.rec[t]);
-        acc = rec_cost(r);
-        ep = (uint8_t)++epoch;
-        if (ep == 0) {  // epoch wrap (every 255 candidates): clear this thread's marks
-          for (int x = 0; x < tr.T; ++x) mk[x] = 0u;
-          ep = (uint8_t)++epoch;
-        }
-        mk[t] = ep;
-        stage = 0;
-        for (int j = r.z; j < r.w; ++j) {
-          const int y = __ldg(&tr.in_idx[j]);
-          if (dfs_elig(y, 0) && mk[y] != ep) {
-            mk[y] = ep;
-            stk[sp++] = y;
           }
         }
         continue;
@@ -465,6 +458,26 @@ struct Cell {
           }
         }
       }
+    }
+    __syncthreads();
+    // c(t) = producer cost + the two sums; h = c / s (Coop), c / (m s) (DTR), c / ((m +
+    // adjacent free bytes) s) (DTE)
+    for (int ci = threadIdx.x; ci < ncand; ci += kThreads) {
+      const int b = cand[ci];
+      const int t = O()[b];
+      const int64_t c = rec_cost(__ldg(&tr.rec[t])) + w.pacc[2 * ci] + w.pacc[2 * ci + 1];
+      int64_t s = sh.clock - w.last_access[t];  // staleness (R17)
+      if (s < 1) s = 1;
+      double den = (double)s;  // Coop: h = c/s (R1)
+      if (pol) {               // DTR: c / (m s); DTE: m + the adjacent free bytes (R46)
+        uint64_t m = Z()[b];
+        if (pol == 2) {
+          if (b > 0 && O()[b - 1] == kFree) m += Z()[b - 1];
+          if (b + 1 < sh.nb && O()[b + 1] == kFree) m += Z()[b + 1];
+        }
+        den = __dmul_rn((double)m, (double)s);
+      }
+      w.ih[b] = __ddiv_rn((double)c, den);
     }
   }
 
@@ -1010,7 +1023,7 @@ WsLayout make_layout(int T) {
   L.last_access = take((size_t)T * 8);
   L.taddr = take((size_t)T * 8);
   L.epochs = take((size_t)kThreads * 4);
-  L.marks = take((size_t)kThreads * T);  // one byte per tensor and thread
+  L.marks = take((size_t)kThreads * ((T + 15) & ~15));  // one byte per tensor and thread
   L.stack = take((size_t)kThreads * T * 4);
   L.isz = take((size_t)(kCap + 1) * 8);
   L.ih = take((size_t)(kCap + 1) * 8);
@@ -1021,6 +1034,7 @@ WsLayout make_layout(int T) {
   L.trans = take((size_t)T * 4 * 4);
   L.victims = take((size_t)kCap * 4);
   L.cand = take((size_t)(kCap + 2) * 4);
+  L.pacc = take((size_t)(kCap + 2) * 2 * 8);
   L.bytes = o;
   return L;
 }
