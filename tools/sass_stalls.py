@@ -1,6 +1,5 @@
 """Per-source-line executed-instruction and stall-sample shares of one kernel, sorted by stall share (ncu --page source --csv --print-source sass input).
 usage: sass_stalls.py <ncu_sass.csv> <lib.so> <kernel-substring> [top]"""
-usage: sass_lines.py <ncu_sass.csv> <lib.so> <kernel-substring> [top]"""
 import collections, csv, os, re, subprocess, sys, tempfile
 
 csv_path, lib, ksub = sys.argv[1:4]
