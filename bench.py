@@ -17,6 +17,12 @@ kernel time vs MEASURED_PEAKS.json; `cpu_baseline` = the CPU oracle (oracle/) ti
 box's host cores on a bounded sample; `e2e` = the same metric through the host-buffer C-ABI
 entry point (coop_window_search_batched_host) with H2D/D2H copies inside the timed region.
 `--impl reference` times the oracle itself (rank 0 only) on bounded samples per step.
+
+Also reported (untimed for `value`): the replay sweeps of BASELINE configs 2, 3 and 5 with
+the O2 oracle timed beside them on the host cores and every GPU cell record compared with
+the oracle's (rank 0 at N = 1); the config-1 single-query latency; at N > 1 the gather of
+every rank's result records to all ranks (the path's only collective, timed separately) and
+a digest of the whole job's records.
 """
 from __future__ import annotations
 
@@ -137,8 +143,8 @@ def _oracle_worker(args):
     ss, c, s, r = G.bench_pools_host(G.MODE_BENCH, SEED, p0, n_pools, N_BLOCKS)
     barrier.wait()
     t = time.perf_counter()
-    O.search_many(ss, c, s, r, n_pools, N_BLOCKS, N_BLOCKS)
-    return n_pools, time.perf_counter() - t
+    w = O.search_many(ss, c, s, r, n_pools, N_BLOCKS, N_BLOCKS)
+    return n_pools, time.perf_counter() - t, p0, w.tobytes()
 
 
 def cpu_baseline(cpu_seconds: float, sample_offset: int = 0):
@@ -154,10 +160,11 @@ def cpu_baseline(cpu_seconds: float, sample_offset: int = 0):
                                             for w in range(cores)])
     total = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
+    windows = b"".join(r[3] for r in sorted(res, key=lambda r: r[2]))
     return {"value": total / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{total} pools x {N_BLOCKS} blocks (global pools "
                       f"[{sample_offset}, {sample_offset + total})), one process per core, "
-                      f"C oracle O(N*L) per pool, wall {wall:.2f} s"}
+                      f"C oracle O(N*L) per pool, wall {wall:.2f} s"}, windows
 
 
 # ------------------------------------------------------------------------ reference arm
@@ -197,10 +204,38 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------- replay sweeps
-def replay_bench(world: int, rank: int, steps: int, with_config5: bool):
-    """BASELINE configs 3 and 5 on this rank's cells (config 5 cells cyclic over ranks):
-    trace ops/s = trace ops (not counting recomputes) replayed per second, summed over
-    cells; device time per sweep with CUDA events; one stream per trace."""
+REPLAY_FIELDS = ["status", "fail_op", "base_us", "total_us", "evictions", "remat", "pressure",
+                 "frag_fail", "inplace_reuse", "heuristic_evals", "sum_free_bytes_after",
+                 "sum_free_blocks_after", "digest", "max_depth", "max_blocks", "budget", "n_events"]
+
+
+def replay_sweeps(peaks_by_name, with_config5: bool):
+    """BASELINE configs 2, 3 and 5 as lists of (trace name, budget, k) cells."""
+    from gen import dnn
+    sw = {
+        # config 2: ResNet-50 at 50 % of peak, one cell
+        "config2": [("resnet50", peaks_by_name["resnet50"] // 2, 0)],
+        # config 3: GPT-3-style 2.7B, 64 budgets 25 %..100 % of peak, one CTA per budget
+        "config3": [("gpt3_2.7b", peaks_by_name["gpt3_2.7b"] * (1575 + 75 * k) // 6300, k)
+                    for k in range(64)],
+        # config 5: eight DNN shapes x 256 budgets 20 %..100 % of peak
+        "config5": [(name, peaks_by_name[name] * (20 * 255 + 80 * k) // (100 * 255), k)
+                    for name in dnn.DNNS for k in range(256)],
+    }
+    if not with_config5:
+        del sw["config5"]
+    return sw
+
+
+def replay_bench(world: int, rank: int, steps: int, with_config5: bool, with_oracle: bool):
+    """BASELINE configs 2, 3 and 5 on this rank's cells (cells cyclic over ranks): trace
+    ops/s = trace ops (not counting recomputes) replayed per second, summed over cells;
+    device time per sweep with CUDA events (max over ranks); one stream per trace.  Every
+    rank's 136-byte cell records are gathered to all ranks (dist.gather_cells) and, at
+    N = 1 on rank 0, compared field by field with the O2 oracle run on the host cores
+    (one process per core), whose wall time gives the oracle's ops/s."""
+    import hashlib
+
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -214,28 +249,18 @@ def replay_bench(world: int, rank: int, steps: int, with_config5: bool):
     traces = {name: dnn.dnn(name) for name in dnn.DNNS}
     handles = {name: coop.Trace(tr) for name, tr in traces.items()}
     peaks = {name: handles[name].peak_live(flags) for name in traces}
-    sweeps = {
-        # config 2: ResNet-50 at 50 % of peak, one cell
-        "config2": [("resnet50", [peaks["resnet50"] // 2])],
-        # config 3: GPT-3-style 2.7B, 64 budgets 25 %..100 % of peak, one CTA per budget
-        "config3": [("gpt3_2.7b", [peaks["gpt3_2.7b"] * (1575 + 75 * k) // 6300 for k in range(64)])],
-        # config 5: eight DNN shapes x 256 budgets 20 %..100 % of peak
-        "config5": [(name, [peaks[name] * (20 * 255 + 80 * k) // (100 * 255) for k in range(256)])
-                    for name in dnn.DNNS],
-    }
-    if not with_config5:
-        del sweeps["config5"]
+    sweeps = replay_sweeps(peaks, with_config5)
     streams = {name: torch.cuda.Stream() for name in traces}
     main_s = torch.cuda.current_stream()
-    for key, sweep in sweeps.items():
-        # shard: global cell index over the sweep, cyclic over ranks (config 3 too)
-        cells = [(name, j, b) for name, bs in sweep for j, b in enumerate(bs)]
+    rec_bytes = coop.REPLAY_RESULT_DTYPE.itemsize
+    launches = 0
+    for key, cells in sweeps.items():
         mine = [cells[c] for c in D.cyclic_cells(len(cells), rank, world)]
         per = {}
-        for name, j, b in mine:
+        for name, b, _ in mine:
             per.setdefault(name, []).append(b)
-        bufs = {name: torch.empty(len(bs) * coop.REPLAY_RESULT_DTYPE.itemsize, dtype=torch.uint8,
-                                  device="cuda") for name, bs in per.items()}
+        bufs = {name: torch.empty(len(bs) * rec_bytes, dtype=torch.uint8, device="cuda")
+                for name, bs in per.items()}
         ops = sum(traces[name].n_ops * len(bs) for name, bs in per.items())
 
         def sweep_once(warm=False):
@@ -259,44 +284,69 @@ def replay_bench(world: int, rank: int, steps: int, with_config5: bool):
             dist.barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
-        nsteps = 1 if key == "config5" else steps  # config 5: one sweep takes minutes
+        nsteps = 1 if key == "config5" else steps  # config 5: one sweep is the long one
         t0.record(main_s)
         for _ in range(nsteps):
             sweep_once()
         t1.record(main_s)
         torch.cuda.synchronize()
+        launches += nsteps * len(per)
         ms = t0.elapsed_time(t1) / nsteps
         if world > 1:
             t = torch.tensor([ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t[0])
-            tops = torch.tensor([ops], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tops)
-            ops_all = float(tops[0])
-        else:
-            ops_all = float(ops)
-        res = np.concatenate([bufs[n].cpu().numpy().view(coop.REPLAY_RESULT_DTYPE) for n in per]) \
-            if per else np.zeros(0, coop.REPLAY_RESULT_DTYPE)
+        # this rank's records in its cyclic cell order, then the gather to global order
+        local = torch.empty(len(mine) * rec_bytes, dtype=torch.uint8, device="cuda")
+        off = {name: 0 for name in per}
+        for j, (name, b, _) in enumerate(mine):
+            local[j * rec_bytes:(j + 1) * rec_bytes] = bufs[name][off[name] * rec_bytes:(off[name] + 1) * rec_bytes]
+            off[name] += 1
+        g0 = time.perf_counter()
+        allrec = D.gather_cells(local, len(cells), rec_bytes, world)
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - g0) * 1e3
+        res = allrec.cpu().numpy().reshape(-1).view(coop.REPLAY_RESULT_DTYPE)
+        ops_all = float(sum(traces[name].n_ops for name, _, _ in cells))
         ok = res["status"] == 0
         frag = (res["sum_free_bytes_after"][ok] / np.maximum(1, res["pressure"][ok]) /
                 res["budget"][ok].astype(np.float64))
         ovh = (res["total_us"][ok] - res["base_us"][ok]) / np.maximum(1, res["base_us"][ok])
         lat = res["search_ns_total"][ok] / np.maximum(1, res["pressure"][ok])
-        out[key] = {
+        exact = np.stack([res[f].astype(np.int64) if res[f].dtype != np.uint64 else res[f].view(np.int64)
+                          for f in REPLAY_FIELDS], 1)
+        entry = {
             "workload": {"config2": "ResNet-50 at 50 % of peak, 1 budget",
                          "config3": "GPT-3-style 2.7B x 64 budgets (25-100 % of peak)",
                          "config5": "8 DNN shapes x 256 budgets (20-100 % of peak)"}[key],
             "flags": "partition+recomputable-inplace", "cells": len(cells),
             "cells_this_rank": len(mine), "ms_per_sweep": ms, "timed_sweeps": nsteps,
             "trace_ops_per_s": ops_all / (ms / 1e3),
-            "events_per_s_incl_recompute": (ops_all + float(res["remat"].sum()) * world) / (ms / 1e3),
-            "completed_cells_rank0": int(ok.sum()),
-            "mean_frag_rate_rank0": float(frag.mean()) if ok.any() else None,
-            "mean_overhead_rank0": float(ovh.mean()) if ok.any() else None,
-            "search_latency_us_mean_rank0": float(lat.mean() / 1e3) if ok.any() else None,
-            "search_latency_us_max_rank0": float(res["search_ns_max"][ok].max() / 1e3) if ok.any() else None,
+            "events_per_s_incl_recompute": (ops_all + float(res["remat"].sum())) / (ms / 1e3),
+            "completed_cells": int(ok.sum()),
+            "mean_frag_rate": float(frag.mean()) if ok.any() else None,
+            "mean_overhead": float(ovh.mean()) if ok.any() else None,
+            "search_latency_us_mean": float(lat.mean() / 1e3) if ok.any() else None,
+            "search_latency_us_max": float(res["search_ns_max"][ok].max() / 1e3) if ok.any() else None,
             "gpu_launches_per_sweep": len(per),
+            "records_sha256": hashlib.sha256(exact.tobytes()).hexdigest()[:16],
+            "gather_ms": gather_ms if world > 1 else None,
         }
+        if with_oracle and rank == 0:
+            from oracle import parallel as OP
+            want, wall, secs, procs = OP.replay_cells(cells, flags)
+            bad = [i for i in range(len(cells))
+                   if any(int(res[i][f]) != int(want[i][f]) for f in REPLAY_FIELDS)]
+            entry["cpu_baseline"] = {
+                "value": ops_all / wall, "unit": "trace ops/s", "cores": procs, "kind": "oracle",
+                "sample": f"all {len(cells)} cells, O2 (oracle/oracle_replay.c) one process per "
+                          f"core, wall {wall:.2f} s, slowest cell {secs.max():.2f} s"}
+            entry["oracle_ms_per_sweep"] = wall * 1e3
+            entry["gpu_vs_oracle"] = wall * 1e3 / ms
+            entry["parity"] = {"cells_compared": len(cells), "mismatches": len(bad),
+                               "fields": "all integer counters, status, fail_op, digest (R29)",
+                               "first_mismatch": cells[bad[0]][:2] if bad else None}
+        out[key] = entry
     # NEXT-3: minimum / cutoff budgets (R45) of the config-2 and config-3 traces, rank 0 only
     if rank == 0:
         for name in ("resnet50", "gpt3_2.7b"):
@@ -309,10 +359,62 @@ def replay_bench(world: int, rank: int, steps: int, with_config5: bool):
                 "min_budget_frac": (int(b["min_budget"]) / pk) if b["min_status"] == 0 else None,
                 "cutoff_budget_frac": (int(b["cutoff_budget"]) / pk) if b["cutoff_status"] == 0 else None,
                 "replays": int(b["replays"]), "wall_ms": dt * 1e3,
-                "grid": "64 coarse x 64 fine budgets (DESIGN.md R45)"}
+                "grid": "64 coarse x 64 fine budgets on brackets (0,P], (P,2P], ... (DESIGN.md R45)"}
     for h in handles.values():
         h.close()
-    return out
+    return out, launches
+
+
+def config1_latency(dev, calls: int = 2000):
+    """BASELINE config 1: one 32-block query per call (launch + stream sync, host wall
+    clock), and the same launch captured in a CUDA graph; the paper's < 0.4 us
+     is a host-side search inside OneFlow on A100 -- context only."""
+    import numpy as np
+    import torch
+
+    from gen import pools as G
+    from paper_2311_00591_b200 import coop
+    ss, c, s, r = G.bench_pools_host(G.MODE_SMALL, 5, 0, 1, 32)
+    d = [torch.from_numpy(ss.view(np.int64)).to(dev), torch.from_numpy(c).to(dev),
+         torch.from_numpy(s).to(dev), torch.from_numpy(r.view(np.int64)).to(dev)]
+    out = torch.empty(4, dtype=torch.int64, device=dev)
+    st = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(st):
+        for _ in range(20):
+            coop.window_search_batched(*d, out, 1, 32, 32, st)
+        st.synchronize()
+        ts = []
+        for _ in range(calls):
+            t = time.perf_counter()
+            coop.window_search_batched(*d, out, 1, 32, 32, st)
+            st.synchronize()
+            ts.append(time.perf_counter() - t)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            coop.window_search_batched(*d, out, 1, 32, 32, st)
+        for _ in range(20):
+            g.replay()
+        st.synchronize()
+        tg = []
+        for _ in range(calls):
+            t = time.perf_counter()
+            g.replay()
+            st.synchronize()
+            tg.append(time.perf_counter() - t)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(calls):
+            coop.window_search_batched(*d, out, 1, 32, 32, st)
+        e1.record(st)
+        st.synchronize()
+    ts.sort()
+    tg.sort()
+    return {"workload": "config1: one query on a 32-block pool (MODE_SMALL, seed 5)",
+            "launch_sync_us_median": 1e6 * ts[len(ts) // 2], "launch_sync_us_p99": 1e6 * ts[int(len(ts) * 0.99)],
+            "graph_replay_sync_us_median": 1e6 * tg[len(tg) // 2],
+            "device_us_per_query_back_to_back": 1e3 * e0.elapsed_time(e1) / calls,
+            "paper_context": "< 0.4 us host-side search (OneFlow, A100 host; PAPER.md:299-300)"}
 
 
 # ---------------------------------------------------------------------------- GPU arm
@@ -321,12 +423,15 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    import hashlib
+
     import numpy as np
     import torch
     import torch.distributed as dist
 
     from gen import pools as G
     from paper_2311_00591_b200 import coop
+    from paper_2311_00591_b200 import dist as D
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -338,7 +443,7 @@ def main():
     torch.cuda.set_device(dev)
 
     P, n = args.pools, N_BLOCKS
-    p0 = rank * P
+    p0 = D.pool_range(P, rank)[0]
     ss = torch.empty(P * n, dtype=torch.int64, device=dev)
     c = torch.empty(P * n, dtype=torch.float64, device=dev)
     s = torch.empty(P * n, dtype=torch.float64, device=dev)
@@ -386,15 +491,27 @@ def main():
     else:
         kmean = statistics.mean(kernel_ms)
 
-    # results summary (untimed): status histogram; gather per-rank digests to rank 0
-    res = coop.windows_from_device(out)
-    digest = int(np.bitwise_xor.reduce(res.view(np.uint64)))
-    stat = {str(k): int(v) for k, v in zip(*np.unique(res["status"], return_counts=True))}
+    # the path's only collective: every rank's 32-byte window records to every rank
+    # (NCCL all-gather over NVLink), timed on the device separately from `value`
+    gather_ms = None
     if world > 1:
-        # the path's only collective: gather of per-shard results (here: shard digests)
-        d = torch.tensor([digest & 0x7FFFFFFFFFFFFFFF], dtype=torch.int64, device=dev)
-        gathered = [torch.zeros_like(d) for _ in range(world)]
-        dist.all_gather(gathered, d)
+        dist.barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        allw = D.gather_bytes(out.view(torch.uint8), world)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gt = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gather_ms = float(gt[0])
+        res_all = allw.cpu().numpy().reshape(-1).view(coop.WINDOW_DTYPE)
+        del allw
+    else:
+        res_all = coop.windows_from_device(out)
+    res = res_all[rank * P:(rank + 1) * P]
+    stat = {str(k): int(v) for k, v in zip(*np.unique(res_all["status"], return_counts=True))}
+    job_sha = hashlib.sha256(res_all.tobytes()).hexdigest()[:16]
 
     # e2e through the host-buffer C-ABI entry (rank-local; pinned host copies, untimed fill)
     e2e = None
@@ -422,9 +539,13 @@ def main():
         e2e = {"value": world * Pe / te, "unit": UNIT,
                "h2d_bytes_per_step": Pe * n * 24 + Pe * 8, "d2h_bytes_per_step": Pe * 32,
                "pools_per_gpu": Pe, "matches_device_results": same,
+               "bound": "PCIe: 24 B per block crosses the host link (%.1f GB/s achieved)"
+                        % (Pe * ALGO_BYTES_PER_POOL / te / 1e9),
                "api": "coop_window_search_batched_host (pinned host buffers, chunked "
                       "H2D/kernel/D2H overlap on 2 streams)"}
         del h_ss, h_c, h_s, h_r
+    del ss, c, s
+    torch.cuda.empty_cache()
 
     value = world * P * args.steps / (elapsed_ms / 1e3)
     peak, peak_src = peaks()
@@ -434,14 +555,24 @@ def main():
             "frac": achieved / peak, "peak_source": peak_src,
             "traffic": (tr["dram_bytes_per_pool"] * P) if tr else None,
             "algorithmic_bytes_per_launch": P * ALGO_BYTES_PER_POOL,
-            "kernel": "coop::search_kernel<8,512,2>", "kernel_ms_mean": kmean,
-            "frac_of_8TBps": achieved / 8000.0}
-    replay = None
+            "kernel": "coop::search_kernel", "kernel_ms_mean": kmean,
+            "kernel_ms_min": min(kernel_ms), "frac_of_8TBps": achieved / 8000.0}
+    lat1 = config1_latency(dev) if rank == 0 else None
+    replay, replay_launches = None, 0
+    with_oracle = (rank == 0 and world == 1 and not args.no_cpu_baseline)
     if not args.no_replay:
-        replay = replay_bench(world, rank, args.replay_steps, not args.no_config5)
+        replay, replay_launches = replay_bench(world, rank, args.replay_steps, not args.no_config5,
+                                               with_oracle)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.cpu_seconds)
+    if with_oracle:
+        cpu, windows = cpu_baseline(args.cpu_seconds)
+        ow = np.frombuffer(windows, dtype=coop.WINDOW_DTYPE)
+        g = res[:len(ow)]
+        mism = int(sum((g[f] != ow[f]).sum() for f in ("status", "first", "last", "span", "n_evict"))
+                   + (g["cost"].view(np.uint64) != ow["cost"].view(np.uint64)).sum())
+        cpu["parity_self_check"] = {"pools_compared": int(len(ow)), "field_mismatches": mism,
+                                    "what": "the oracle's windows for its sample vs the timed "
+                                            "GPU run's records of the same pools"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -451,8 +582,12 @@ def main():
                 "config": dict(ARM_CONFIG, pools_per_gpu=P,
                                parallelism=f"dp{world} (pool shards, weak scaling)"),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": args.steps, "clocks": clk, "replay": replay,
-                "results": {"status_counts": stat, "xor_digest": f"{digest:016x}"}}
+                "gpu_launches": args.steps, "clocks": clk,
+                "config1_latency": lat1, "replay": replay,
+                "results": {"status_counts": stat, "records_sha256": job_sha,
+                            "gather_ms": gather_ms, "records": int(len(res_all)),
+                            "gather": "NCCL all_gather_into_tensor of the 32-byte windows"
+                                      if world > 1 else "single rank"}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -109,6 +109,53 @@ def fig2_trace(mib: int = MiB) -> Trace:
     return b.build()
 
 
+def fig2_dtr_trace(mib: int = MiB) -> Trace:
+    """Fig. 2 as the DTR half of PAPER.md:202 tells it: the same chain, but the first conv
+    is the more expensive one (twice the FLOPs of the second: 3560 us vs 1780 us at Table 1's
+    35.6 us/MB).  With equal conv costs the DTR heuristics of x1 and x2 tie exactly after
+    x0's eviction ((1780 + 195) / 1975 = 195 / 195), which is not the paper's scenario.
+    Here x0 is the stalest and cheapest tensor (c = 195, s = 2170), its eviction raises
+    h(x1) to (3560 + 195) / 1975 > h(x2) = 195 / 195, so DTR (h = c / (m s), R46) evicts x0,
+    then x2, finds the two freed 50 MB chunks non-contiguous, and evicts x1 as well; Coop's
+    window search evicts one contiguous run of two tensors."""
+    b = Builder("fig2_dtr")
+    x0 = b.op([], 50 * mib, 195)
+    x1 = b.op([x0], 50 * mib, 3560)
+    x2 = b.op([x1], 50 * mib, 195)
+    x3 = b.op([x2], 50 * mib, 1780)
+    x4 = b.op([x3], 50 * mib, 195)
+    x5 = b.op([x4], 100 * mib, 3560)
+    g = b.op([x5], 1 * mib, 10, BWD)
+    for x in (x4, x3, x2, x1, x0):
+        g = b.op([g, x], 1 * mib, 10, BWD)
+    return b.build()
+
+
+def dead_diamond_trace(n: int = 8, unit: int = 1) -> Trace:
+    """A chain of n diamonds whose tensors are all dead when the chain's tip must be
+    recomputed (pins DESIGN.md R22 against SURVEY N22):
+        x0 = src(); a_k = g(x_{k-1}); b_k = h(x_{k-1}); x_k = f(a_k, b_k)   (k = 1..n)
+        y = f(x_n)                              -- every x, a, b dies in the forward pass
+        z = src() (size Z)                      -- with budget Z + 1, y (2 units) is evicted
+        u = f(z); w = f(y, u)                   -- y is needed again: recompute the chain
+    Under R22 each dead tensor recomputed for y stays resident until the end of the op, so
+    the chain is recomputed once (3n + 2 recomputes).  Freeing a dead tensor right after the
+    recompute that consumed it (N22) makes b_k recompute x_{k-1} again after a_k did:
+    T(x_k) = 3 + 2 T(x_{k-1}), exponential in n."""
+    b = Builder("dead_diamond")
+    x = b.op([], unit, 3)
+    for _ in range(n):
+        a = b.op([x], unit, 5)
+        c = b.op([x], unit, 5)
+        x = b.op([a, c], unit, 7)
+    y = b.op([x], 2 * unit, 11)
+    big = (3 * n + 4) * unit
+    z = b.op([], big, 13)
+    u = b.op([z], unit, 1)
+    b.op([y, u], unit, 1)
+    return b.build()
+
+
 def random_trace(rng: np.random.Generator, n_params=3, n_fwd=12, max_in=3, inplace_p=0.15,
                  size_choices=(1, 2, 3, 4, 6, 8), unit=1, iters=1) -> Trace:
     """Random small training-like DAG: forward chain-ish ops reading recent tensors and

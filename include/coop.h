@@ -207,7 +207,11 @@ typedef struct {
  * out: DEVICE array [n_budgets]; log: DEVICE array [n_budgets * log_cap_per_budget] or
  * NULL.  class_threshold: us per MiB separating C1/C2 (0 -> 15, R14); max_depth:
  * rematerialization bound (0 -> 512, R23).  The trace's device workspace grows on demand
- * (first call with a larger n_budgets allocates).  Asynchronous.
+ * (first call with a larger n_budgets allocates).  Asynchronous.  Calls on one trace
+ * handle serialise on the device: each call's stream first waits for the previous call's
+ * kernel (an event recorded after every launch), because they share the handle's
+ * workspace; run independent sweeps concurrently on distinct handles.  The launch goes to
+ * the device the trace was first uploaded to.
  */
 int coop_replay_trace(coop_trace_t trace, const uint64_t *budgets, int32_t n_budgets,
                       uint32_t flags, uint32_t class_threshold, int32_t max_depth,
@@ -220,12 +224,15 @@ int coop_replay_trace(coop_trace_t trace, const uint64_t *budgets, int32_t n_bud
  * for one trace, by waves of coop_replay_trace (one CTA per budget):
  *   min budget    = the smallest budget at which the replay completes (status COOP_OK),
  *   cutoff budget = the smallest budget at which it completes with zero evictions.
- * Grid (R45): P = peak_live(flags) (R25); coarse budgets B_k = max(1, floor(P * k / Kc)),
- * k = 1..Kc; for each metric, k* = the smallest k whose replay satisfies it; then the fine
- * budgets B_{k*-1} + floor((B_{k*} - B_{k*-1}) * j / Kf), j = 1..Kf (B_0 = 0, budgets
- * clamped to >= 1), and the result is the smallest fine budget that satisfies it.  A metric
- * that no coarse budget satisfies gets status COOP_INFEASIBLE and budget 0.  Synchronous;
- * allocates (and frees) device result buffers.  Kc, Kf in [1, 4096].
+ * Grid (R45): P = peak_live(flags) (R25), Z = the bytes of all tensors of the trace (a pool
+ * of Z bytes never evicts).  Brackets (lo, hi] = (0, P], (P, 2P], (2P, 4P], ...: coarse
+ * budgets B_k = max(1, lo + floor((hi - lo) * k / Kc)), k = 1..Kc; for each metric the
+ * first bracket with a satisfying B_k gives k* = its smallest such k (later brackets are
+ * tried only while some metric has none and hi < Z); then the fine budgets B_{k*-1} +
+ * floor((B_{k*} - B_{k*-1}) * j / Kf), j = 1..Kf (B_0 = lo), and the result is the smallest
+ * fine budget that satisfies it (else B_{k*}).  A metric that no bracket satisfies gets
+ * status COOP_INFEASIBLE and budget 0.  Synchronous (legacy default stream); the device
+ * result buffer is cached in the trace handle.  Kc, Kf in [1, 4096].
  */
 typedef struct {
   uint64_t peak;           /* P */

@@ -26,11 +26,8 @@ def lib():
     global _lib
     if _lib is None:
         if not os.path.exists(LIB_PATH):
-            here = os.path.dirname(_HERE)
-            import sys
-            sys.path.insert(0, here)
-            from paper_2311_00591_b200 import _build  # builds only; does not load libcoop
-            _build.build_oracle()
+            from oracle import build as _ob  # the oracle's own gcc build (no product code)
+            _ob.build_oracle()
         L = ctypes.CDLL(LIB_PATH)
         L.orc_window_search.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]

@@ -955,6 +955,11 @@ int orc_budget_search(const orc_trace *tr, uint32_t flags, uint32_t class_thresh
   memset(out, 0, sizeof(*out));
   uint64_t peak = orc_peak_live(tr, flags);
   out->peak = peak;
+  /* Z = the bytes of every tensor of the trace: a pool that large never evicts, so the
+   * brackets below stop there (R45) */
+  uint64_t zsum = 0;
+  for (int i = 0; i < tr->n_tensors; ++i) zsum += tr->size[i];
+  if (zsum < peak) zsum = peak;
   orc_cfg cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.flags = flags;
@@ -963,21 +968,28 @@ int orc_budget_search(const orc_trace *tr, uint32_t flags, uint32_t class_thresh
   for (int m = 0; m < 2; ++m) {
     uint64_t *dst = m == 0 ? &out->min_budget : &out->cutoff_budget;
     int32_t *st = m == 0 ? &out->min_status : &out->cutoff_status;
-    /* coarse grid: the smallest k whose replay satisfies the metric */
+    /* coarse grid on the brackets (0, P], (P, 2P], (2P, 4P], ... until the bracket's upper
+     * end reaches Z: the smallest k of the first bracket that has one */
     int kstar = -1;
+    uint64_t blo = 0, bhi = peak > 0 ? peak : 1;
     orc_replay_result r;
-    for (int k = 1; k <= kc && kstar < 0; ++k) {
-      cfg.budget = o4_grid(0, peak, k, kc);
-      orc_replay(tr, &cfg, &r, NULL, 0);
-      if (o4_meets(&r, m)) kstar = k;
+    for (;;) {
+      for (int k = 1; k <= kc && kstar < 0; ++k) {
+        cfg.budget = o4_grid(blo, bhi, k, kc);
+        orc_replay(tr, &cfg, &r, NULL, 0);
+        if (o4_meets(&r, m)) kstar = k;
+      }
+      if (kstar >= 0 || bhi >= zsum) break;
+      blo = bhi;
+      bhi = bhi > (UINT64_MAX >> 1) ? UINT64_MAX : 2 * bhi;
     }
     if (kstar < 0) {
       *st = ORC_INFEASIBLE;
       *dst = 0;
       continue;
     }
-    /* fine grid inside (B_{k*-1}, B_{k*}] */
-    uint64_t lo = kstar > 1 ? o4_grid(0, peak, kstar - 1, kc) : 0, hi = o4_grid(0, peak, kstar, kc);
+    /* fine grid inside (B_{k*-1}, B_{k*}] of that bracket */
+    uint64_t lo = kstar > 1 ? o4_grid(blo, bhi, kstar - 1, kc) : blo, hi = o4_grid(blo, bhi, kstar, kc);
     *st = ORC_OK;
     *dst = hi;
     for (int j = 1; j <= kf; ++j) {

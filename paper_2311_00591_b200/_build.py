@@ -2,8 +2,8 @@
 
   paper_2311_00591_b200/libcoop.so  -- the product: CUDA kernels + C ABI (include/coop.h)
   gen/libcoopgen.so                 -- seeded input generators (host + device)
-  oracle/liboracle.so               -- TEST INFRASTRUCTURE: the CPU oracle (built, never
-                                       linked into or called by the product path)
+
+The CPU oracle (test infrastructure) has its own build next to it (oracle/build.py).
 """
 from __future__ import annotations
 
@@ -21,7 +21,6 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-shared"
 
 LIBCOOP = os.path.join(PKG, "libcoop.so")
 LIBGEN = os.path.join(ROOT, "gen", "libcoopgen.so")
-LIBORACLE = os.path.join(ROOT, "oracle", "liboracle.so")
 
 
 def _stale(target: str, sources: list[str]) -> bool:
@@ -54,22 +53,12 @@ def build_libgen(force: bool = False) -> str:
     return LIBGEN
 
 
-def build_oracle(force: bool = False) -> str:
-    srcs = sorted(glob.glob(os.path.join(ROOT, "oracle", "*.c")))
-    deps = srcs + glob.glob(os.path.join(ROOT, "oracle", "*.h"))
-    if force or _stale(LIBORACLE, deps):
-        _run(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-              "-shared", "-Wall", "-o", LIBORACLE, *srcs, "-lm"])
-    return LIBORACLE
-
-
 def build_all(force: bool = False) -> None:
     build_libcoop(force)
     build_libgen(force)
-    build_oracle(force)
 
 
 if __name__ == "__main__":
     import sys
     build_all(force="--force" in sys.argv)
-    print("built", LIBCOOP, LIBGEN, LIBORACLE)
+    print("built", LIBCOOP, LIBGEN)

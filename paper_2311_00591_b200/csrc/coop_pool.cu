@@ -121,7 +121,7 @@ __device__ __forceinline__ void pool_store(const PArgs &pa, Shared &sh) {
 // One online call on the state held in shared memory (loaded by pool_load).  Results go
 // to the mapped HostIO; the caller orders them before its completion signal.
 __device__ __forceinline__ void pool_call(const PArgs &pa, Shared &sh) {
-  Cell c(pa.k, sh, 0);
+  CellT<false> c(pa.k, sh, 0);  // coherent loads: the graph grows between calls
   PoolState &P = *pa.ps;
   const GraphMut &g = pa.g;
   const int tid = threadIdx.x, t = pa.t;
@@ -650,10 +650,13 @@ extern "C" int coop_pool_init(const coop_pool_config *cfg, coop_pool_t *out) {
   h->res.digest = 0x9E3779B97F4A7C15ull;
   h->res.budget = cfg->budget;
   h->res.max_blocks = 1;
-  bool ok = cudaMemcpy(p->d_ps, h, sizeof(PoolState), cudaMemcpyHostToDevice) == cudaSuccess &&
-            cudaMemset(p->d_graph, 0, off) == cudaSuccess &&
-            cudaMemset(g.cons_head, 0xff, (size_t)T * 4) == cudaSuccess &&
-            cudaMemset(p->ws, 0, p->lay.bytes) == cudaSuccess;
+  // every initialisation is ordered on the pool's (non-blocking) stream, on which all of
+  // its kernels run, and completed before the handle is returned
+  bool ok = cudaMemcpyAsync(p->d_ps, h, sizeof(PoolState), cudaMemcpyHostToDevice, p->stream) == cudaSuccess &&
+            cudaMemsetAsync(p->d_graph, 0, off, p->stream) == cudaSuccess &&
+            cudaMemsetAsync(g.cons_head, 0xff, (size_t)T * 4, p->stream) == cudaSuccess &&
+            cudaMemsetAsync(p->ws, 0, p->lay.bytes, p->stream) == cudaSuccess &&
+            cudaStreamSynchronize(p->stream) == cudaSuccess;
   delete h;
   if (!ok) {
     pool_release(p);

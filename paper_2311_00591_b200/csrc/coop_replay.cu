@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kThreads, 1) replay_kernel(const KArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   Shared &sh = *reinterpret_cast<Shared *>(smem);
   for (int cell = blockIdx.x; cell < a.n_cells; cell += gridDim.x) {
-    Cell c(a, sh, cell);
+    CellT<true> c(a, sh, cell);
     c.run(a.budgets[cell]);
     if (threadIdx.x == 0) a.out[cell] = sh.res;
     __syncthreads();
@@ -63,6 +63,12 @@ struct coop_trace_s {
   WsLayout lay{};
   uint64_t *d_budgets = nullptr;
   size_t budgets_cap = 0;
+  coop_replay_result *d_wave = nullptr;  // coop_budget_search's result buffer (grows on demand)
+  size_t wave_cap = 0;
+  // completion of the last replay launched on this handle: the next call's stream waits on
+  // it before reusing the workspace and the budget buffer (calls on one handle serialise,
+  // whatever streams they are issued on)
+  cudaEvent_t done = nullptr;
   int device = 0;
 };
 
@@ -288,9 +294,18 @@ extern "C" int coop_trace_create(const coop_trace_desc *d, coop_trace_t *out) {
 
 extern "C" int coop_trace_destroy(coop_trace_t t) {
   if (!t) return COOP_ERR_INVALID_ARG;
-  if (t->dev) cudaFree(t->dev);
-  if (t->ws) cudaFree(t->ws);
-  if (t->d_budgets) cudaFree(t->d_budgets);
+  if (t->dev) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != t->device) cudaSetDevice(t->device);
+    if (t->done) cudaEventSynchronize(t->done);
+    cudaFree(t->dev);
+    if (t->ws) cudaFree(t->ws);
+    if (t->d_budgets) cudaFree(t->d_budgets);
+    if (t->d_wave) cudaFree(t->d_wave);
+    if (t->done) cudaEventDestroy(t->done);
+    if (prev != t->device) cudaSetDevice(prev);
+  }
   delete t;
   return COOP_OK;
 }
@@ -317,6 +332,10 @@ extern "C" int coop_trace_peak_live(coop_trace_t t, uint32_t flags, uint64_t *ou
   return COOP_OK;
 }
 
+static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_budgets, uint32_t flags,
+                            uint32_t class_threshold, int32_t max_depth, coop_replay_result *out,
+                            coop_event *log, int64_t log_cap, cudaStream_t st);
+
 extern "C" int coop_replay_trace(coop_trace_t t, const uint64_t *budgets, int32_t n_budgets,
                                  uint32_t flags, uint32_t class_threshold, int32_t max_depth,
                                  coop_replay_result *out, coop_event *log, int64_t log_cap,
@@ -329,9 +348,23 @@ extern "C" int coop_replay_trace(coop_trace_t t, const uint64_t *budgets, int32_
     if (budgets[i] < 1) return COOP_ERR_INVALID_ARG;
   if (!is_device_ptr(out) || (log && !is_device_ptr(log))) return COOP_ERR_INVALID_ARG;
   if (t->T > kMaxT) return COOP_ERR_NOMEM;  // per-tensor flags / pins live in shared memory
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (t->dev && prev != t->device) cudaSetDevice(t->device);  // launch where the mirror lives
+  const int rc = replay_on_device(t, budgets, n_budgets, flags, class_threshold, max_depth, out, log,
+                                  log_cap, (cudaStream_t)stream);
+  if (prev != t->device) cudaSetDevice(prev);
+  return rc;
+}
+
+static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_budgets, uint32_t flags,
+                            uint32_t class_threshold, int32_t max_depth, coop_replay_result *out,
+                            coop_event *log, int64_t log_cap, cudaStream_t st) {
   const int up = upload_trace(t);
   if (up != COOP_OK) return up;
-  cudaStream_t st = (cudaStream_t)stream;
+  if (!t->done && cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming) != cudaSuccess) return COOP_ERR_CUDA;
+  // the previous call on this handle (possibly on another stream) still owns ws / d_budgets
+  if (cudaStreamWaitEvent(st, t->done, 0) != cudaSuccess) return COOP_ERR_CUDA;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
   const size_t smem = sizeof(Shared);
@@ -347,7 +380,8 @@ extern "C" int coop_replay_trace(coop_trace_t t, const uint64_t *budgets, int32_
     t->ws = nullptr;
     t->ws_cells = 0;
     if (cudaMalloc(&t->ws, cells * t->lay.bytes) != cudaSuccess) return COOP_ERR_NOMEM;
-    cudaMemset(t->ws, 0, cells * t->lay.bytes);  // DFS epochs start at 0
+    // DFS epochs start at 0; ordered before the kernel on the launch stream
+    if (cudaMemsetAsync(t->ws, 0, cells * t->lay.bytes, st) != cudaSuccess) return COOP_ERR_CUDA;
     t->ws_cells = cells;
   }
   if ((size_t)n_budgets > t->budgets_cap) {
@@ -371,7 +405,8 @@ extern "C" int coop_replay_trace(coop_trace_t t, const uint64_t *budgets, int32_
   // each CTA owns a workspace slot: cells are assigned cyclically, CTA b takes cells
   // b, b + grid, ... and always uses slot b
   replay_kernel<<<(unsigned)cells, kThreads, smem, st>>>(a);
-  return cudaGetLastError() == cudaSuccess ? COOP_OK : COOP_ERR_CUDA;
+  if (cudaGetLastError() != cudaSuccess) return COOP_ERR_CUDA;
+  return cudaEventRecord(t->done, st) == cudaSuccess ? COOP_OK : COOP_ERR_CUDA;
 }
 
 // ------------------------------------------------------------------ budget searches (R45)
@@ -388,13 +423,19 @@ int run_wave(coop_trace_t t, const std::vector<uint64_t> &budgets, uint32_t flag
              int32_t depth, std::vector<coop_replay_result> &res) {
   res.assign(budgets.size(), coop_replay_result{});
   if (budgets.empty()) return COOP_OK;
-  coop_replay_result *d = nullptr;
-  if (cudaMalloc(&d, budgets.size() * sizeof(coop_replay_result)) != cudaSuccess) return COOP_ERR_NOMEM;
-  int rc = coop_replay_trace(t, budgets.data(), (int32_t)budgets.size(), flags, thr, depth, d, nullptr, 0, nullptr);
+  if (budgets.size() > t->wave_cap) {  // grows once per handle, not per wave
+    if (t->d_wave) cudaFree(t->d_wave);
+    t->d_wave = nullptr;
+    t->wave_cap = 0;
+    if (cudaMalloc(&t->d_wave, budgets.size() * sizeof(coop_replay_result)) != cudaSuccess) return COOP_ERR_NOMEM;
+    t->wave_cap = budgets.size();
+  }
+  int rc = coop_replay_trace(t, budgets.data(), (int32_t)budgets.size(), flags, thr, depth, t->d_wave, nullptr, 0,
+                             nullptr);
   if (rc == COOP_OK &&
-      cudaMemcpy(res.data(), d, budgets.size() * sizeof(coop_replay_result), cudaMemcpyDeviceToHost) != cudaSuccess)
+      cudaMemcpy(res.data(), t->d_wave, budgets.size() * sizeof(coop_replay_result), cudaMemcpyDeviceToHost) !=
+          cudaSuccess)
     rc = COOP_ERR_CUDA;
-  cudaFree(d);
   return rc;
 }
 
@@ -413,22 +454,43 @@ extern "C" int coop_budget_search(coop_trace_t t, uint32_t flags, uint32_t thr, 
   if (rc != COOP_OK) return rc;
   coop_budget_result r{};
   r.peak = peak;
-  std::vector<uint64_t> coarse((size_t)kc);
-  for (int k = 1; k <= kc; ++k) coarse[(size_t)k - 1] = grid_budget(0, peak, k, kc);
-  std::vector<coop_replay_result> cres;
-  rc = run_wave(t, coarse, flags, thr, depth, cres);
-  if (rc != COOP_OK) return rc;
-  r.replays = kc;
+  // Z = the bytes of every tensor: a pool that large never evicts (R45)
+  uint64_t zsum = 0;
+  for (int i = 0; i < t->T; ++i) zsum += t->size[i];
+  if (zsum < peak) zsum = peak;
+  // coarse waves on the brackets (0, P], (P, 2P], ... until every metric has a satisfying
+  // grid point or the bracket reaches Z; both metrics share a bracket's wave
+  uint64_t blo = 0, bhi = peak > 0 ? peak : 1;
+  uint64_t mlo[2] = {0, 0}, mhi[2] = {0, 0};
   int kstar[2] = {-1, -1};
-  for (int m = 0; m < 2; ++m)
-    for (int k = 0; k < kc && kstar[m] < 0; ++k)
-      if (meets(cres[(size_t)k], m)) kstar[m] = k;
-  // both metrics' fine grids in one wave
+  std::vector<uint64_t> coarse((size_t)kc);
+  std::vector<coop_replay_result> cres;
+  for (;;) {
+    for (int k = 1; k <= kc; ++k) coarse[(size_t)k - 1] = grid_budget(blo, bhi, k, kc);
+    rc = run_wave(t, coarse, flags, thr, depth, cres);
+    if (rc != COOP_OK) return rc;
+    r.replays += kc;
+    for (int m = 0; m < 2; ++m) {
+      if (kstar[m] >= 0) continue;
+      for (int k = 0; k < kc && kstar[m] < 0; ++k)
+        if (meets(cres[(size_t)k], m)) {
+          kstar[m] = k + 1;
+          mlo[m] = blo;
+          mhi[m] = bhi;
+        }
+    }
+    if ((kstar[0] >= 0 && kstar[1] >= 0) || bhi >= zsum) break;
+    blo = bhi;
+    bhi = bhi > (UINT64_MAX >> 1) ? UINT64_MAX : 2 * bhi;
+  }
+  // both metrics' fine grids inside (B_{k*-1}, B_{k*}] of their brackets, in one wave
   std::vector<uint64_t> fine;
+  uint64_t flo[2] = {0, 0}, fhi[2] = {0, 0};
   for (int m = 0; m < 2; ++m) {
     if (kstar[m] < 0) continue;
-    const uint64_t lo = kstar[m] > 0 ? coarse[(size_t)kstar[m] - 1] : 0, hi = coarse[(size_t)kstar[m]];
-    for (int j = 1; j <= kf; ++j) fine.push_back(grid_budget(lo, hi, j, kf));
+    flo[m] = kstar[m] > 1 ? grid_budget(mlo[m], mhi[m], kstar[m] - 1, kc) : mlo[m];
+    fhi[m] = grid_budget(mlo[m], mhi[m], kstar[m], kc);
+    for (int j = 1; j <= kf; ++j) fine.push_back(grid_budget(flo[m], fhi[m], j, kf));
   }
   std::vector<coop_replay_result> fres;
   rc = run_wave(t, fine, flags, thr, depth, fres);
@@ -444,7 +506,7 @@ extern "C" int coop_budget_search(coop_trace_t t, uint32_t flags, uint32_t thr, 
       continue;
     }
     *st = COOP_OK;
-    *dst = coarse[(size_t)kstar[m]];
+    *dst = fhi[m];
     for (int j = 0; j < kf; ++j)
       if (meets(fres[base + (size_t)j], m)) {
         *dst = fine[base + (size_t)j];

@@ -810,6 +810,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
       }
     }
   pool_done:
+    // every thread orders its generic-proxy writes into the stage (S / H^ / h write-back)
+    // before the async-proxy (TMA) refill that the barrier releases
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();  // stage s fully consumed
     if (a.use_tma && tid == 0) {
       const int64_t pn = p + (int64_t)a.stages * gridDim.x;

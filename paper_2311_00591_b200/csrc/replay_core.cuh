@@ -176,8 +176,19 @@ __device__ __forceinline__ uint64_t cta_min_u64(Shared &sh, uint64_t v) {
   return r;
 }
 
+// Loads of the trace graph: the read-only path (__ldg, ld.global.nc) for the trace replay,
+// whose graph is immutable for the kernel's lifetime; plain coherent loads for the online
+// pool, whose graph arrays are appended to by earlier calls of the same resident kernel.
+template <bool RO, class T>
+__device__ __forceinline__ T ldg_if(const T *p) {
+  if constexpr (RO) return __ldg(p);
+  else return *p;
+}
+
 // ------------------------------------------------------------------ the replay cell
-struct Cell {
+// kRO: the trace graph is read-only while the kernel runs (replay) or not (online pool).
+template <bool kRO>
+struct CellT {
   const KArgs &a;
   const TraceDev &tr;
   Shared &sh;
@@ -186,7 +197,7 @@ struct Cell {
   uint32_t epoch;  // per-thread DFS epoch
   coop_event *log;
 
-  __device__ Cell(const KArgs &a_, Shared &sh_, int cell_) : a(a_), tr(a_.tr), sh(sh_), cell(cell_) {
+  __device__ CellT(const KArgs &a_, Shared &sh_, int cell_) : a(a_), tr(a_.tr), sh(sh_), cell(cell_) {
     unsigned char *base = a.ws + (size_t)blockIdx.x * a.lay.bytes;  // this CTA's slot
     w.tflags = (uint8_t *)(base + a.lay.tflags);
     w.pins = (int32_t *)(base + a.lay.pins);
@@ -401,17 +412,17 @@ struct Cell {
         }
         mk[t] = ep;
         if (stage == 0) {  // the ancestors' roots: t's producer's inputs
-          const int4 r = __ldg(&tr.rec[t]);
+          const int4 r = ldg_if<kRO>(&tr.rec[t]);
           for (int j = r.z; j < r.w; ++j) {
-            const int y = __ldg(&tr.in_idx[j]);
+            const int y = ldg_if<kRO>(&tr.in_idx[j]);
             if (dfs_elig(y, 0) && mk[y] != ep) {
               mk[y] = ep;
               stk[sp++] = y;
             }
           }
         } else {  // the descendants' roots: the outputs of t's consumers
-          for (int e = __ldg(&tr.cons_head[t]); e >= 0; e = __ldg(&tr.cons_next[e])) {
-            const int y = __ldg(&tr.cons_out[e]);
+          for (int e = ldg_if<kRO>(&tr.cons_head[t]); e >= 0; e = ldg_if<kRO>(&tr.cons_next[e])) {
+            const int y = ldg_if<kRO>(&tr.cons_out[e]);
             if (dfs_elig(y, 1) && mk[y] != ep) {
               mk[y] = ep;
               stk[sp++] = y;
@@ -422,7 +433,7 @@ struct Cell {
       }
       const int x = stk[--sp];
       const uint8_t f = sh.tfl[x];
-      const int4 r = __ldg(&tr.rec[x]);
+      const int4 r = ldg_if<kRO>(&tr.rec[x]);
       // ancestors: non-resident and recomputable; descendants: evicted and live
       const bool ok = stage == 0 ? (!(f & TF_RES) && r.z >= 0)
                                  : ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD));
@@ -435,7 +446,7 @@ struct Cell {
           int y[4];
           uint8_t m[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) y[k] = j0 + k < r.w ? __ldg(&tr.in_idx[j0 + k]) : -1;
+          for (int k = 0; k < 4; ++k) y[k] = j0 + k < r.w ? ldg_if<kRO>(&tr.in_idx[j0 + k]) : -1;
 #pragma unroll
           for (int k = 0; k < 4; ++k) m[k] = (y[k] >= 0 && dfs_elig(y[k], 0)) ? mk[y[k]] : ep;
 #pragma unroll
@@ -450,8 +461,8 @@ struct Cell {
           }
         }
       } else {
-        for (int e = __ldg(&tr.cons_head[x]); e >= 0; e = __ldg(&tr.cons_next[e])) {
-          const int y = __ldg(&tr.cons_out[e]);
+        for (int e = ldg_if<kRO>(&tr.cons_head[x]); e >= 0; e = ldg_if<kRO>(&tr.cons_next[e])) {
+          const int y = ldg_if<kRO>(&tr.cons_out[e]);
           if (dfs_elig(y, 1) && mk[y] != ep) {
             mk[y] = ep;
             stk[sp++] = y;
@@ -465,7 +476,7 @@ struct Cell {
     for (int ci = threadIdx.x; ci < ncand; ci += kThreads) {
       const int b = cand[ci];
       const int t = O()[b];
-      const int64_t c = rec_cost(__ldg(&tr.rec[t])) + w.pacc[2 * ci] + w.pacc[2 * ci + 1];
+      const int64_t c = rec_cost(ldg_if<kRO>(&tr.rec[t])) + w.pacc[2 * ci] + w.pacc[2 * ci + 1];
       int64_t s = sh.clock - w.last_access[t];  // staleness (R17)
       if (s < 1) s = 1;
       double den = (double)s;  // Coop: h = c/s (R1)
@@ -507,7 +518,7 @@ struct Cell {
       __syncthreads();
       for (int b = threadIdx.x; b < sh.nb; b += kThreads) {
         const int o = O()[b];
-        if (o != kFree && !__ldg(&tr.unevict[o]) && w.pins[o] == 0 && !(sh.tfl[o] & TF_LOCK))
+        if (o != kFree && !ldg_if<kRO>(&tr.unevict[o]) && w.pins[o] == 0 && !(sh.tfl[o] & TF_LOCK))
           w.cand[atomicAdd(&sh.ncand, 1)] = b;
       }
       __syncthreads();
@@ -578,7 +589,7 @@ struct Cell {
       int st;
       if (o == kFree) {
         st = COOP_FREE;
-      } else if (__ldg(&tr.unevict[o]) || w.pins[o] > 0 || (sh.tfl[o] & TF_LOCK)) {
+      } else if (ldg_if<kRO>(&tr.unevict[o]) || w.pins[o] > 0 || (sh.tfl[o] & TF_LOCK)) {
         st = COOP_PINNED;
       } else {
         st = COOP_EVICTABLE;

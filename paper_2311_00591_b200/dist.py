@@ -7,6 +7,7 @@ over NVLink on B200; gloo in the CPU tests), done outside the timed region.
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -34,6 +35,19 @@ def gather_bytes(local: torch.Tensor, world: int, group=None) -> torch.Tensor:
     return out
 
 
+def assemble_cyclic(per_rank, n_cells: int, world: int):
+    """Records of rank r's cyclic cells (rank-major, [len(cyclic_cells(n, r, world)), ...]
+    each, extra padding rows ignored) -> all records in global cell order."""
+    first = per_rank[0]
+    shape = (n_cells,) + tuple(first.shape[1:])
+    out = first.new_empty(shape) if isinstance(first, torch.Tensor) else np.empty(shape, first.dtype)
+    for r in range(world):
+        cells = cyclic_cells(n_cells, r, world)
+        if cells:
+            out[cells] = per_rank[r][:len(cells)]
+    return out
+
+
 def gather_cells(local: torch.Tensor, n_cells: int, rec_bytes: int, world: int, group=None) -> torch.Tensor:
     """Gather per-rank cyclic cell records (padded to ceil(n_cells / world) records per
     rank) and return them in global cell order as [n_cells, rec_bytes] uint8."""
@@ -41,9 +55,4 @@ def gather_cells(local: torch.Tensor, n_cells: int, rec_bytes: int, world: int, 
     buf = torch.zeros(per * rec_bytes, dtype=torch.uint8, device=local.device)
     buf[:local.numel()] = local.view(-1)
     allr = gather_bytes(buf, world, group).view(world, per, rec_bytes)
-    out = torch.empty((n_cells, rec_bytes), dtype=torch.uint8, device=local.device)
-    for r in range(world):
-        cells = cyclic_cells(n_cells, r, world)
-        if cells:
-            out[cells] = allr[r, :len(cells)]
-    return out
+    return assemble_cyclic([allr[r] for r in range(world)], n_cells, world)

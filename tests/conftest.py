@@ -18,6 +18,8 @@ def _built():
     """Build the in-tree libraries once per session (no-op when up to date)."""
     from paper_2311_00591_b200 import _build
     _build.build_all()
+    from oracle import build as oracle_build
+    oracle_build.build_oracle()
     yield
 
 

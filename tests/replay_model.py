@@ -32,7 +32,12 @@ class Thrash(Exception):
 
 
 class Model:
-    def __init__(self, tr, budget, flags, threshold=15, max_depth=512):
+    def __init__(self, tr, budget, flags, threshold=15, max_depth=512, n22=False):
+        # n22: the alternative reading SURVEY N22 (a dead tensor recomputed for another
+        # recompute is freed right after the recompute that consumed it, once unpinned)
+        # instead of DESIGN.md R22 (kept resident until the end of the trace op); used only
+        # to show that the two readings differ (tests/test_oracle_replay.py)
+        self.n22 = n22
         self.tr = tr
         self.flags = flags
         self.thr = threshold
@@ -272,6 +277,11 @@ class Model:
         self.last_access[t] = self.clock
         for u in self.ins[op]:
             self.pins[u] -= 1
+        if self.n22:
+            for u in self.ins[op]:
+                if self.dead[u] and self.resident[u] and self.pins[u] == 0 and not self.unev[u]:
+                    a = self.clear(u)
+                    self.events.append((4, self.cur_op, u, a))
 
     def run(self):
         tr = self.tr

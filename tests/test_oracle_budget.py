@@ -26,15 +26,22 @@ def model_meets(tr, budget, flags, metric):
 
 
 def model_search(tr, flags, kc, kf):
+    """R45 with brackets (0, P], (P, 2P], ... up to Z = the bytes of all tensors"""
     peak = O.peak_live(tr, flags)
+    z = max(peak, int(sum(int(x) for x in tr.size)))
     out = []
     for metric in (0, 1):
-        ks = [k for k in range(1, kc + 1) if model_meets(tr, grid(0, peak, k, kc), flags, metric)]
+        blo, bhi = 0, max(peak, 1)
+        while True:
+            ks = [k for k in range(1, kc + 1) if model_meets(tr, grid(blo, bhi, k, kc), flags, metric)]
+            if ks or bhi >= z:
+                break
+            blo, bhi = bhi, 2 * bhi
         if not ks:
             out.append((1, 0))
             continue
         k = ks[0]
-        lo, hi = (grid(0, peak, k - 1, kc) if k > 1 else 0), grid(0, peak, k, kc)
+        lo, hi = (grid(blo, bhi, k - 1, kc) if k > 1 else blo), grid(blo, bhi, k, kc)
         b = hi
         for j in range(1, kf + 1):
             if model_meets(tr, grid(lo, hi, j, kf), flags, metric):
@@ -79,3 +86,22 @@ def test_budget_properties_fig2():
             assert not (r["status"] == 0 and (metric == 0 or r["evictions"] == 0))
     # the largest tensor plus the unevictable bytes bound the minimum budget from below
     assert mb >= int(max(tr.size))
+
+
+def test_cutoff_above_peak_bracket():
+    """Fragmentation can force evictions at the peak itself (R25 is a resident-bytes peak,
+    not an address high-water mark); the cutoff is then found in the bracket (P, 2P]
+    (R45): zero evictions at the result, evictions at P."""
+    rng = np.random.default_rng(0)
+    tr = TR.random_trace(rng, n_fwd=6, iters=1)
+    o = O.budget_search(tr, 0, coarse=8, fine=6)
+    peak, cb = int(o["peak"]), int(o["cutoff_budget"])
+    assert o["cutoff_status"] == 0 and peak < cb <= 2 * peak
+    r, _ = O.replay(tr, peak, 0)
+    assert r["status"] == 0 and r["evictions"] > 0
+    r, _ = O.replay(tr, cb, 0)
+    assert r["status"] == 0 and r["evictions"] == 0
+    # a pool of all tensors' bytes never evicts (the bracket bound Z)
+    z = int(sum(int(x) for x in tr.size))
+    r, _ = O.replay(tr, z, 0)
+    assert r["status"] == 0 and r["evictions"] == 0

@@ -211,3 +211,71 @@ def test_dtr_dte_baselines_vs_model(seed):
             want = dict(m.c, status=status, fail_op=fail_op)
             assert got == {k: int(want[k]) for k in RESULT_FIELDS}, (f, budget)
             assert ev_tuples(log) == m.events
+
+
+def test_fig2_dtr_half():
+    """The DTR half of Fig. 2 (NEXT-1, R46) on fig2_dtr_trace: at op 5 DTR
+    evicts x0 (stalest and cheapest: h = 195 / (m 2170)), then x2 (x0's eviction raised
+    h(x1) to (3560 + 195) / (m 1975) > h(x2) = 195 / (m 195)), finds the freed 50 MB
+    chunks [0, 50) and [100, 150) non-contiguous and evicts x1 too: three evictions before
+    x5 fits at 0.  Coop's window search on the same state evicts the contiguous pair
+    {x0, x1} (h sum 195/2170 + 3560/1975, the cheapest two-tensor window)."""
+    tr = TR.fig2_dtr_trace()
+    _, log = O.replay(tr, 250 * MiB, O.F_DTR, log_cap=200)
+    op5 = [(k, t, a) for k, op, t, a in ev_tuples(log) if op == 5 and k in (O.EV_EVICT, O.EV_ALLOC)]
+    assert op5 == [(O.EV_EVICT, 0, 0), (O.EV_EVICT, 2, 100 * MiB), (O.EV_EVICT, 1, 50 * MiB),
+                   (O.EV_ALLOC, 5, 0)]
+    _, log = O.replay(tr, 250 * MiB, 0, log_cap=200)
+    op5 = [(k, t, a) for k, op, t, a in ev_tuples(log) if op == 5 and k in (O.EV_EVICT, O.EV_ALLOC)]
+    assert op5 == [(O.EV_EVICT, 0, 0), (O.EV_EVICT, 1, 50 * MiB), (O.EV_ALLOC, 5, 0)]
+    # the independent byte-map model agrees on the whole run (byte units: sizes 50 B)
+    small = TR.fig2_dtr_trace(mib=1)
+    for f in (O.F_DTR, 0, O.F_DTE, O.F_PARTITION | O.F_INPLACE):
+        r, log = O.replay(small, 250, f, log_cap=1000)
+        m = Model(small, 250, f)
+        status, fail_op = m.run()
+        got = {k: int(r[k]) for k in RESULT_FIELDS}
+        want = dict(m.c, status=status, fail_op=fail_op)
+        assert got == {k: int(want[k]) for k in RESULT_FIELDS}, f
+        assert ev_tuples(log) == m.events, f
+
+
+@pytest.mark.parametrize("n", [4, 6, 8])
+def test_r22_dead_recomputes_kept_until_end_of_op(n):
+    """DESIGN.md R22 vs SURVEY N22 on a chain of dead diamonds (gen/traces.py
+    dead_diamond_trace): under R22 (the oracle) the dead chain recomputed for y stays
+    resident until the end of the op, so every tensor of it is recomputed once (3n + 2
+    recomputes: x0, n x (a, b, x), y); freeing each dead input right after the recompute
+    that consumed it (N22, modelled by the independent Python model with n22=True) makes the
+    sibling b_k recompute x_{k-1} again, T(x_k) = 3 + 2 T(x_{k-1}): exponential.  The model
+    without n22 agrees with the oracle on every counter and event."""
+    tr = TR.dead_diamond_trace(n)
+    budget = (3 * n + 4) + 1
+    r, log = O.replay(tr, budget, 0, log_cap=100000)
+    assert int(r["status"]) == O.OK and int(r["evictions"]) == 1
+    assert int(r["remat"]) == 3 * n + 2
+    m = Model(tr, budget, 0)
+    status, fail_op = m.run()
+    assert (status, m.c["remat"]) == (0, 3 * n + 2)
+    assert ev_tuples(log) == m.events
+    m22 = Model(tr, budget, 0, n22=True)
+    status22, _ = m22.run()
+    t = 1  # T(x0)
+    for _ in range(n):
+        t = 3 + 2 * t
+    assert status22 == 0 and m22.c["remat"] == t + 1  # + y
+    assert m22.c["remat"] >= 2 ** n
+
+
+def test_r34_input_batch_is_recomputable():
+    """DESIGN.md R34 (vs SURVEY N34): an input batch is the output of a source op (no
+    inputs; re-running it reloads the batch), so it is evictable and rematerializable like
+    any activation.  In Fig. 2's chain x0 is such a source output: at 250 MiB Coop evicts
+    it at op 5 and the backward pass recomputes it by re-running op 0 (a remat event of op
+    0).  Under N34 x0 would be a barrier while live and the op-5 window could not use it."""
+    tr = TR.fig2_trace()
+    r, log = O.replay(tr, 250 * MiB, O.F_INPLACE, log_cap=200)
+    ev = ev_tuples(log)
+    assert (O.EV_EVICT, 5, 0, 0) in ev
+    assert any(k == O.EV_REXEC and op == 0 and t == 0 for k, op, t, _ in ev)
+    assert int(r["status"]) == O.OK

@@ -135,3 +135,24 @@ def test_dtr_dte_dnn_gpu(name):
         peak = O.peak_live(tr, 0)
         budgets = [int(peak * f) for f in (0.5, 0.75, 1.0)]
         check(tr, budgets, pol, ctx=f"{name} pol {pol}")
+
+
+def test_fig2_dtr_half_gpu():
+    """The DTR half of Fig. 2 through coop_replay_trace: x0, x2, then x1."""
+    tr = TR.fig2_dtr_trace()
+    for flags in (coop.F_POLICY_DTR, coop.F_POLICY_DTE, 0, 3):
+        check(tr, [250 << 20, 200 << 20, 300 << 20], flags, log_cap=200, ctx="fig2_dtr")
+    t = coop.Trace(tr)
+    _, ev = t.replay([250 << 20], coop.F_POLICY_DTR, log_cap=200)
+    e = ev[0]
+    op5 = [(int(k), int(x), int(a) >> 20) for k, o, x, a in zip(e["kind"], e["op"], e["tensor"], e["addr"])
+           if o == 5 and k in (O.EV_EVICT, O.EV_ALLOC)]
+    assert op5 == [(O.EV_EVICT, 0, 0), (O.EV_EVICT, 2, 100), (O.EV_EVICT, 1, 50), (O.EV_ALLOC, 5, 0)]
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_dead_diamond_gpu(n):
+    """R22 on the GPU: the dead chain is recomputed once (3n + 2 recomputes)."""
+    tr = TR.dead_diamond_trace(n)
+    res = check(tr, [3 * n + 5, 3 * n + 8], 0, log_cap=1000, ctx="dead_diamond")
+    assert int(res[0]["remat"]) == 3 * n + 2
