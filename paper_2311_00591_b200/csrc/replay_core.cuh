@@ -28,7 +28,11 @@ inline bool bad_flags(uint32_t f) {
 }
 constexpr int kMaxT = 16384;     // tensors per trace whose flags live in shared memory
 
-enum : uint8_t { TF_RES = 1, TF_BORN = 2, TF_DEAD = 4, TF_LOCK = 8 };
+enum : uint8_t { TF_RES = 1, TF_BORN = 2, TF_DEAD = 4, TF_LOCK = 8,
+                 // replay only: the cached projected-cost closure of the tensor may be stale
+                 // (TF_DIRTY); the tensor's residency / liveness changed since the last
+                 // pressure event and it is on the changed list (TF_CHG)
+                 TF_DIRTY = 16, TF_CHG = 32 };
 
 struct TraceDev {
   int32_t T, M, n_params;
@@ -55,7 +59,8 @@ struct TraceDev {
 };
 
 struct WsLayout {  // byte offsets inside one cell's workspace
-  size_t tflags, pins, last_access, taddr, epochs, marks, stack, isz, ih, ist, S, H, B, trans, victims, cand, pacc;
+  size_t tflags, pins, last_access, taddr, epochs, marks, stack, isz, ih, ist, S, H, B, trans, victims, cand, pacc,
+      cc, chg, dl;
   size_t bytes;
 };
 
@@ -75,6 +80,9 @@ struct CellPtrs {
   int32_t *trans, *victims;
   int32_t *cand;
   int64_t *pacc;  // per (candidate, half) closure sums of the current pressure event
+  int64_t *cc;    // per tensor: cached |Anc| + |Desc| cost sums (valid unless TF_DIRTY)
+  int32_t *chg;   // tensors whose residency / liveness changed since the last event
+  int32_t *dl;    // candidate indices whose closure is recomputed at this event
 };
 
 struct KArgs {
@@ -117,6 +125,8 @@ struct Shared {
   U192 red192[kWarps];
   int32_t redpar;
   int32_t ncand, cand_next;  // projected-cost work list of the current pressure event
+  int32_t nchg, chg_next;    // changed list (replay) and its invalidation work counter
+  int32_t ndirty;            // candidates whose closure is recomputed at this event
   // the last evicted window (read by the online calls): items, span, cost bits, victims
   int32_t win_first, win_last, nvict;
   uint64_t win_span, win_cost;
@@ -216,6 +226,9 @@ struct CellT {
     w.victims = (int32_t *)(base + a.lay.victims);
     w.cand = (int32_t *)(base + a.lay.cand);
     w.pacc = (int64_t *)(base + a.lay.pacc);
+    w.cc = (int64_t *)(base + a.lay.cc);
+    w.chg = (int32_t *)(base + a.lay.chg);
+    w.dl = (int32_t *)(base + a.lay.dl);
     log = a.log ? a.log + (size_t)cell * a.log_cap : nullptr;
   }
 
@@ -236,6 +249,17 @@ struct CellT {
       e.pad = 0;
       e.addr = addr;
       log[i] = e;
+    }
+  }
+
+  // Thread 0 only: tensor t's residency / liveness changed (R18's closures may change for
+  // the resident tensors next to it); recorded once per event for the replay's closure cache.
+  __device__ __forceinline__ void changed(int t) {
+    if constexpr (kRO) {
+      if (!(sh.tfl[t] & TF_CHG)) {
+        sh.tfl[t] |= TF_CHG;
+        w.chg[sh.nchg++] = t;
+      }
     }
   }
 
@@ -337,6 +361,7 @@ struct CellT {
     release(b);
     if (threadIdx.x == 0) {
       sh.tfl[t] &= (uint8_t)~TF_RES;
+      changed(t);
       log_ev(4, sh.cur_op, t, ad);
     }
     __syncthreads();
@@ -387,29 +412,109 @@ struct CellT {
   // one pass after a barrier forms c(t) and h.  A node is marked when pushed, so every
   // node enters a walk's stack at most once: the per-thread stack (T entries) cannot
   // overflow.
+  // next visited-mark epoch of this thread (one byte per tensor and thread, epoch & 255;
+  // the marks are cleared when the epoch wraps, every 255 walks)
+  __device__ __forceinline__ uint8_t next_epoch(uint8_t *mk, int Tp) {
+    uint8_t ep = (uint8_t)++epoch;
+    if (ep == 0) {
+      for (int x = 0; x < Tp; x += 16) *reinterpret_cast<uint4 *>(mk + x) = make_uint4(0, 0, 0, 0);
+      ep = (uint8_t)++epoch;
+    }
+    return ep;
+  }
+
+  // Replay closure cache: which resident tensors' closures may differ from the cached ones.
+  // Anc(t) / Desc(t) depend only on the residency / liveness flags of the tensors they
+  // reach (or stop at).  For a candidate t whose closure (old or new) touches a changed
+  // tensor, take the first changed tensor x on that path: the path's other tensors are
+  // unchanged, so they are as eligible now as before, and the reverse walk from x finds t:
+  //   down from x through born, non-resident tensors (the reverse of the Anc walk) to the
+  //   resident tensors reached (x is in, or bounds, their Anc);
+  //   up from x through evicted live tensors (the reverse of the Desc walk) to the resident
+  //   tensors reached.
+  // Those and the changed tensors themselves get TF_DIRTY; every other resident tensor's
+  // cached sums are exact.  Two work items per changed tensor, same flat loop as below.
+  __device__ void invalidate(uint8_t *mk, int32_t *stk, int Tp) {
+    const int nchg = sh.nchg;
+    if (threadIdx.x == 0) sh.chg_next = 0;
+    __syncthreads();
+    int sp = 0, stage = 0;
+    uint8_t ep = 0;
+    auto visit = [&](int y) {
+      const uint8_t f = sh.tfl[y];
+      if (f & TF_RES) {
+        if (!(f & TF_DIRTY)) sh.tfl[y] = f | TF_DIRTY;  // only TF_DIRTY is set in this phase
+        return;
+      }
+      const bool go = stage == 0 ? (f & TF_BORN) : ((f & TF_BORN) && !(f & TF_DEAD));
+      if (go && mk[y] != ep) {
+        mk[y] = ep;
+        stk[sp++] = y;
+      }
+    };
+    auto expand = [&](int x) {
+      if (stage == 0) {
+        for (int e = ldg_if<kRO>(&tr.cons_head[x]); e >= 0; e = ldg_if<kRO>(&tr.cons_next[e]))
+          visit(ldg_if<kRO>(&tr.cons_out[e]));
+      } else {
+        const int4 r = ldg_if<kRO>(&tr.rec[x]);
+        for (int j = r.z; j < r.w; ++j) visit(ldg_if<kRO>(&tr.in_idx[j]));
+      }
+    };
+    while (true) {
+      if (sp == 0) {
+        const int it = atomicAdd(&sh.chg_next, 1);
+        if (it >= 2 * nchg) break;
+        const int x = w.chg[it >> 1];
+        stage = it & 1;
+        ep = next_epoch(mk, Tp);
+        mk[x] = ep;
+        if (stage == 0) sh.tfl[x] |= TF_DIRTY;
+        expand(x);
+        continue;
+      }
+      expand(stk[--sp]);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nchg; i += kThreads) sh.tfl[w.chg[i]] &= (uint8_t)~TF_CHG;
+    __syncthreads();
+    if (threadIdx.x == 0) sh.nchg = 0;
+  }
+
   __device__ void projected_costs(const int32_t *cand, int ncand, int pol = 0) {
     // visited marks: one byte per tensor and thread (epoch & 255; cleared on wrap), four
     // times denser than word epochs so a walking thread's marks stay in L1
     const int Tp = (tr.T + 15) & ~15;  // per-thread stride, 16-byte aligned (uint4 clears)
     uint8_t *mk = reinterpret_cast<uint8_t *>(w.marks) + (size_t)threadIdx.x * Tp;
     int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
-    const int nitems = 2 * ncand;
-    int sp = 0, it = -1, stage = 0;
+    // replay: walk only the candidates whose cached closure may be stale
+    int nwork = ncand;
+    const int32_t *wl = nullptr;
+    if constexpr (kRO) {
+      invalidate(mk, stk, Tp);
+      if (threadIdx.x == 0) sh.ndirty = 0;
+      __syncthreads();
+      for (int ci = threadIdx.x; ci < ncand; ci += kThreads)
+        if (sh.tfl[O()[cand[ci]]] & TF_DIRTY) w.dl[atomicAdd(&sh.ndirty, 1)] = ci;
+      __syncthreads();
+      nwork = sh.ndirty;
+      wl = w.dl;
+    }
+    const int nitems = 2 * nwork;
+    int sp = 0, it = -1, stage = 0, slot = 0;
     int64_t acc = 0;
     uint8_t ep = 0;
     while (true) {
       if (sp == 0) {
-        if (it >= 0) w.pacc[it] = acc;
+        if (it >= 0) w.pacc[slot] = acc;
         it = atomicAdd(&sh.cand_next, 1);
         if (it >= nitems) break;
-        const int t = O()[cand[it >> 1]];
+        const int ci = wl ? wl[it >> 1] : (it >> 1);
+        const int t = O()[cand[ci]];
         stage = it & 1;
+        slot = 2 * ci + stage;
         acc = 0;
-        ep = (uint8_t)++epoch;
-        if (ep == 0) {  // epoch wrap (every 255 walks): clear this thread's marks
-          for (int x = 0; x < Tp; x += 16) *reinterpret_cast<uint4 *>(mk + x) = make_uint4(0, 0, 0, 0);
-          ep = (uint8_t)++epoch;
-        }
+        ep = next_epoch(mk, Tp);
         mk[t] = ep;
         if (stage == 0) {  // the ancestors' roots: t's producer's inputs
           const int4 r = ldg_if<kRO>(&tr.rec[t]);
@@ -476,7 +581,20 @@ struct CellT {
     for (int ci = threadIdx.x; ci < ncand; ci += kThreads) {
       const int b = cand[ci];
       const int t = O()[b];
-      const int64_t c = rec_cost(ldg_if<kRO>(&tr.rec[t])) + w.pacc[2 * ci] + w.pacc[2 * ci + 1];
+      int64_t closure;
+      if constexpr (kRO) {
+        const uint8_t f = sh.tfl[t];
+        if (f & TF_DIRTY) {  // walked at this event: refresh the cache
+          closure = w.pacc[2 * ci] + w.pacc[2 * ci + 1];
+          w.cc[t] = closure;
+          sh.tfl[t] = f & (uint8_t)~TF_DIRTY;
+        } else {
+          closure = w.cc[t];
+        }
+      } else {
+        closure = w.pacc[2 * ci] + w.pacc[2 * ci + 1];
+      }
+      const int64_t c = rec_cost(ldg_if<kRO>(&tr.rec[t])) + closure;
       int64_t s = sh.clock - w.last_access[t];  // staleness (R17)
       if (s < 1) s = 1;
       double den = (double)s;  // Coop: h = c/s (R1)
@@ -546,6 +664,7 @@ struct CellT {
         const int o = O()[bmin];
         const uint64_t ad = A()[bmin];
         sh.tfl[o] &= (uint8_t)~TF_RES;
+        changed(o);
         sh.res.evictions++;
         log_ev(3, sh.cur_op, o, ad);
         uint64_t d = sh.res.digest;  // R29
@@ -721,6 +840,7 @@ struct CellT {
         w.victims[sh.nvict++] = o;
         const uint64_t ad = A()[b];
         sh.tfl[o] &= (uint8_t)~TF_RES;
+        changed(o);
         sh.res.evictions++;
         log_ev(3, sh.cur_op, o, ad);
         d = splitmix64(d ^ (((uint64_t)(uint32_t)sh.cur_op << 32) | (uint32_t)o));  // R29
@@ -753,6 +873,8 @@ struct CellT {
         w.taddr[t] = ad;
         sh.tfl[src] &= (uint8_t)~TF_RES;
         sh.tfl[t] |= TF_RES;
+        changed(src);
+        changed(t);
         sh.res.inplace_reuse++;
         log_ev(2, op, t, ad);
       }
@@ -792,6 +914,7 @@ struct CellT {
     if (threadIdx.x == 0) {
       w.taddr[t] = at;
       sh.tfl[t] |= TF_RES;
+      changed(t);
       log_ev(kind, op, t, at);
     }
     __syncthreads();
@@ -910,6 +1033,7 @@ struct CellT {
       sh.res.digest = 0x9E3779B97F4A7C15ull;
       sh.res.budget = budget;
       sh.res.max_blocks = 1;
+      sh.nchg = 0;
     }
     epoch = w.epochs[threadIdx.x];
     __syncthreads();
@@ -932,6 +1056,7 @@ struct CellT {
         if (threadIdx.x == 0) {
           w.taddr[t] = at;
           sh.tfl[t] = TF_RES | TF_BORN;
+          changed(t);
           log_ev(0, -1, t, at);
         }
         __syncthreads();
@@ -980,7 +1105,10 @@ struct CellT {
       __syncthreads();
       // deaths after op k (R20) merged with transient dead recomputes (R22), ascending id
       if (threadIdx.x == 0) {
-        for (int j = tr.die_ptr[k]; j < tr.die_ptr[k + 1]; ++j) sh.tfl[tr.die_idx[j]] |= TF_DEAD;
+        for (int j = tr.die_ptr[k]; j < tr.die_ptr[k + 1]; ++j) {
+          sh.tfl[tr.die_idx[j]] |= TF_DEAD;
+          changed(tr.die_idx[j]);
+        }
         // insertion-sort the transient list (small) and merge with the (sorted) die list
         int *tl = w.trans;
         const int nt = sh.ntrans;
@@ -1046,6 +1174,9 @@ WsLayout make_layout(int T) {
   L.victims = take((size_t)kCap * 4);
   L.cand = take((size_t)(kCap + 2) * 4);
   L.pacc = take((size_t)(kCap + 2) * 2 * 8);
+  L.cc = take((size_t)T * 8);
+  L.chg = take((size_t)T * 4);
+  L.dl = take((size_t)(kCap + 2) * 4);
   L.bytes = o;
   return L;
 }
