@@ -60,7 +60,7 @@ struct TraceDev {
 
 struct WsLayout {  // byte offsets inside one cell's workspace
   size_t tflags, pins, last_access, taddr, epochs, marks, stack, isz, ih, ist, S, H, B, trans, victims, cand, pacc,
-      cc, chg, dl;
+      cc, chg, dl, vis;
   size_t bytes;
 };
 
@@ -83,6 +83,7 @@ struct CellPtrs {
   int64_t *cc;    // per tensor: cached |Anc| + |Desc| cost sums (valid unless TF_DIRTY)
   int32_t *chg;   // tensors whose residency / liveness changed since the last event
   int32_t *dl;    // candidate indices whose closure is recomputed at this event
+  uint32_t *vis;  // per (tensor, half): bitmap of the tensors its last closure walk examined
 };
 
 struct KArgs {
@@ -229,6 +230,7 @@ struct CellT {
     w.cc = (int64_t *)(base + a.lay.cc);
     w.chg = (int32_t *)(base + a.lay.chg);
     w.dl = (int32_t *)(base + a.lay.dl);
+    w.vis = (uint32_t *)(base + a.lay.vis);
     log = a.log ? a.log + (size_t)cell * a.log_cap : nullptr;
   }
 
@@ -257,7 +259,7 @@ struct CellT {
   __device__ __forceinline__ void changed(int t) {
     if constexpr (kRO) {
       if (!(sh.tfl[t] & TF_CHG)) {
-        sh.tfl[t] |= TF_CHG;
+        sh.tfl[t] |= TF_CHG | TF_DIRTY;
         w.chg[sh.nchg++] = t;
       }
     }
@@ -423,62 +425,15 @@ struct CellT {
     return ep;
   }
 
-  // Replay closure cache: which resident tensors' closures may differ from the cached ones.
-  // Anc(t) / Desc(t) depend only on the residency / liveness flags of the tensors they
-  // reach (or stop at).  For a candidate t whose closure (old or new) touches a changed
-  // tensor, take the first changed tensor x on that path: the path's other tensors are
-  // unchanged, so they are as eligible now as before, and the reverse walk from x finds t:
-  //   down from x through born, non-resident tensors (the reverse of the Anc walk) to the
-  //   resident tensors reached (x is in, or bounds, their Anc);
-  //   up from x through evicted live tensors (the reverse of the Desc walk) to the resident
-  //   tensors reached.
-  // Those and the changed tensors themselves get TF_DIRTY; every other resident tensor's
-  // cached sums are exact.  Two work items per changed tensor, same flat loop as below.
-  __device__ void invalidate(uint8_t *mk, int32_t *stk, int Tp) {
-    const int nchg = sh.nchg;
-    if (threadIdx.x == 0) sh.chg_next = 0;
-    __syncthreads();
-    int sp = 0, stage = 0;
-    uint8_t ep = 0;
-    auto visit = [&](int y) {
-      const uint8_t f = sh.tfl[y];
-      if (f & TF_RES) {
-        if (!(f & TF_DIRTY)) sh.tfl[y] = f | TF_DIRTY;  // only TF_DIRTY is set in this phase
-        return;
-      }
-      const bool go = stage == 0 ? (f & TF_BORN) : ((f & TF_BORN) && !(f & TF_DEAD));
-      if (go && mk[y] != ep) {
-        mk[y] = ep;
-        stk[sp++] = y;
-      }
-    };
-    auto expand = [&](int x) {
-      if (stage == 0) {
-        for (int e = ldg_if<kRO>(&tr.cons_head[x]); e >= 0; e = ldg_if<kRO>(&tr.cons_next[e]))
-          visit(ldg_if<kRO>(&tr.cons_out[e]));
-      } else {
-        const int4 r = ldg_if<kRO>(&tr.rec[x]);
-        for (int j = r.z; j < r.w; ++j) visit(ldg_if<kRO>(&tr.in_idx[j]));
-      }
-    };
-    while (true) {
-      if (sp == 0) {
-        const int it = atomicAdd(&sh.chg_next, 1);
-        if (it >= 2 * nchg) break;
-        const int x = w.chg[it >> 1];
-        stage = it & 1;
-        ep = next_epoch(mk, Tp);
-        mk[x] = ep;
-        if (stage == 0) sh.tfl[x] |= TF_DIRTY;
-        expand(x);
-        continue;
-      }
-      expand(stk[--sp]);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < nchg; i += kThreads) sh.tfl[w.chg[i]] &= (uint8_t)~TF_CHG;
-    __syncthreads();
-    if (threadIdx.x == 0) sh.nchg = 0;
+  // Replay closure cache.  Anc(t) / Desc(t) (and so the cached sums) depend only on the
+  // flags of the tensors their walks EXAMINE: the nodes summed and every neighbour tested
+  // for eligibility.  Each walk records that examined set in a per-(tensor, half) bitmap
+  // (w.vis); if no examined node changed its residency / liveness since the walk, a new
+  // walk would take exactly the same steps, so the cached sums are exact.  A candidate is
+  // re-walked iff its cache is invalid (TF_DIRTY: it became resident, or was not a
+  // candidate at the last event) or its bitmaps hold a tensor of the changed list.
+  __device__ __forceinline__ uint32_t *vis_of(int t, int half) const {
+    return w.vis + ((size_t)2 * t + half) * (size_t)((tr.T + 127) / 128 * 4);
   }
 
   __device__ void projected_costs(const int32_t *cand, int ncand, int pol = 0) {
@@ -490,16 +445,37 @@ struct CellT {
     // replay: walk only the candidates whose cached closure may be stale
     int nwork = ncand;
     const int32_t *wl = nullptr;
+    const int VW = (tr.T + 127) / 128 * 4;  // bitmap words per (tensor, half), uint4-aligned
     if constexpr (kRO) {
-      invalidate(mk, stk, Tp);
+      const int nchg = sh.nchg;
       if (threadIdx.x == 0) sh.ndirty = 0;
       __syncthreads();
-      for (int ci = threadIdx.x; ci < ncand; ci += kThreads)
-        if (sh.tfl[O()[cand[ci]]] & TF_DIRTY) w.dl[atomicAdd(&sh.ndirty, 1)] = ci;
+      for (int ci = threadIdx.x; ci < ncand; ci += kThreads) {
+        const int t = O()[cand[ci]];
+        bool d = (sh.tfl[t] & TF_DIRTY) || nchg > 64;
+        if (!d) {
+          const uint32_t *v0 = vis_of(t, 0), *v1 = vis_of(t, 1);
+          for (int k = 0; k < nchg && !d; ++k) {
+            const int x = w.chg[k];
+            d = ((v0[x >> 5] | v1[x >> 5]) >> (x & 31)) & 1u;
+          }
+        }
+        if (d) {
+          sh.tfl[t] |= TF_DIRTY;  // distinct candidates: distinct bytes
+          w.dl[atomicAdd(&sh.ndirty, 1)] = ci;
+        }
+      }
       __syncthreads();
+      for (int k = threadIdx.x; k < nchg; k += kThreads) sh.tfl[w.chg[k]] &= (uint8_t)~TF_CHG;
+      __syncthreads();
+      if (threadIdx.x == 0) sh.nchg = 0;
       nwork = sh.ndirty;
       wl = w.dl;
     }
+    uint32_t *bm = nullptr;  // the current walk's examined-set bitmap (replay)
+    auto note = [&](int y) {
+      if constexpr (kRO) atomicOr(&bm[y >> 5], 1u << (y & 31));  // fire-and-forget (RED)
+    };
     const int nitems = 2 * nwork;
     int sp = 0, it = -1, stage = 0, slot = 0;
     int64_t acc = 0;
@@ -516,10 +492,15 @@ struct CellT {
         acc = 0;
         ep = next_epoch(mk, Tp);
         mk[t] = ep;
+        if constexpr (kRO) {
+          bm = vis_of(t, stage);
+          for (int q = 0; q < VW; q += 4) *reinterpret_cast<uint4 *>(bm + q) = make_uint4(0, 0, 0, 0);
+        }
         if (stage == 0) {  // the ancestors' roots: t's producer's inputs
           const int4 r = ldg_if<kRO>(&tr.rec[t]);
           for (int j = r.z; j < r.w; ++j) {
             const int y = ldg_if<kRO>(&tr.in_idx[j]);
+            note(y);
             if (dfs_elig(y, 0) && mk[y] != ep) {
               mk[y] = ep;
               stk[sp++] = y;
@@ -528,6 +509,7 @@ struct CellT {
         } else {  // the descendants' roots: the outputs of t's consumers
           for (int e = ldg_if<kRO>(&tr.cons_head[t]); e >= 0; e = ldg_if<kRO>(&tr.cons_next[e])) {
             const int y = ldg_if<kRO>(&tr.cons_out[e]);
+            note(y);
             if (dfs_elig(y, 1) && mk[y] != ep) {
               mk[y] = ep;
               stk[sp++] = y;
@@ -553,6 +535,9 @@ struct CellT {
 #pragma unroll
           for (int k = 0; k < 4; ++k) y[k] = j0 + k < r.w ? ldg_if<kRO>(&tr.in_idx[j0 + k]) : -1;
 #pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (y[k] >= 0) note(y[k]);
+#pragma unroll
           for (int k = 0; k < 4; ++k) m[k] = (y[k] >= 0 && dfs_elig(y[k], 0)) ? mk[y[k]] : ep;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -568,6 +553,7 @@ struct CellT {
       } else {
         for (int e = ldg_if<kRO>(&tr.cons_head[x]); e >= 0; e = ldg_if<kRO>(&tr.cons_next[e])) {
           const int y = ldg_if<kRO>(&tr.cons_out[e]);
+          note(y);
           if (dfs_elig(y, 1) && mk[y] != ep) {
             mk[y] = ep;
             stk[sp++] = y;
@@ -638,6 +624,8 @@ struct CellT {
         const int o = O()[b];
         if (o != kFree && !ldg_if<kRO>(&tr.unevict[o]) && w.pins[o] == 0 && !(sh.tfl[o] & TF_LOCK))
           w.cand[atomicAdd(&sh.ncand, 1)] = b;
+        else if (kRO && o != kFree)
+          sh.tfl[o] |= TF_DIRTY;  // not a candidate: its cache is not kept up to date
       }
       __syncthreads();
       const int nc = sh.ncand;
@@ -710,6 +698,8 @@ struct CellT {
         st = COOP_FREE;
       } else if (ldg_if<kRO>(&tr.unevict[o]) || w.pins[o] > 0 || (sh.tfl[o] & TF_LOCK)) {
         st = COOP_PINNED;
+        // not a candidate: this event's changes are not checked against its cache
+        if constexpr (kRO) sh.tfl[o] |= TF_DIRTY;
       } else {
         st = COOP_EVICTABLE;
         w.cand[atomicAdd(&sh.ncand, 1)] = b;
@@ -1177,6 +1167,7 @@ WsLayout make_layout(int T) {
   L.cc = take((size_t)T * 8);
   L.chg = take((size_t)T * 4);
   L.dl = take((size_t)(kCap + 2) * 4);
+  L.vis = take((size_t)2 * T * ((T + 127) / 128 * 4) * 4);
   L.bytes = o;
   return L;
 }
