@@ -63,6 +63,8 @@ struct Scratch {
   int32_t xend, xnev;  // end / evictions of the best exactly-costed window
   uint32_t cand[kCandCap];
   unsigned long long mbar[2];
+  int32_t nplist;                      // pending mode: pools of the chunk to finish
+  int16_t plist[kMaxWarps * 32];
 };
 
 struct Args {
@@ -80,6 +82,7 @@ struct Args {
   uint32_t stage_bytes;
   int32_t stages;
   int32_t use_tma;
+  int32_t pending;  // finish only the pools the streaming kernel marked COOP_PENDING_
   int32_t dbg;  // profiling hook (COOP_SEARCH_DBG): stop each pool after 1 = load, 2 = phase A +
                 // scan + write-back; with -DCOOP_SEARCH_PHASE_HOOKS also 3 = write-back,
                 // 4 = zero pass, 5 = pruning + compaction, 6 = filter + reductions
@@ -362,6 +365,421 @@ __device__ __forceinline__ void phase_a(const PoolView &v, int k0, int n, bool &
   }
 }
 
+// One pool of the CTA-per-pool search on its staged stage (called by every thread).
+template <int K>
+__device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *Ebuf, smem_t *stage,
+                                            int64_t p, uint64_t Rraw) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = blockDim.x, W = T >> 5;
+  const int n = a.n;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  PoolView v;
+  v.sr = stage;
+  v.hr = stage + a.region_bytes;
+  v.vr = stage + 2u * a.region_bytes;
+  v.list = Ebuf;
+  v.n = n;
+  v.R = Rraw < kRClamp ? Rraw : kRClamp;
+  v.gerr = a.gerr;
+  const int k0 = tid * K;
+
+  if (a.dbg == 1) {
+    if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK);
+    return;
+  }
+  {
+    // ---------------- phase A: decode, validate, h = c/s, local prefixes -------------
+    bool bad = (Rraw == 0);
+    uint32_t barmask = 0, nzmask = 0;
+    uint64_t spre[K];
+    double hpre[K];
+    uint64_t sacc = 0;
+    double hacc = 0.0;
+    if (k0 + K <= n)  // warp-uniform except in the last warp
+      phase_a<K, true>(v, k0, n, bad, barmask, nzmask, spre, hpre, sacc, hacc);
+    else
+      phase_a<K, false>(v, k0, n, bad, barmask, nzmask, spre, hpre, sacc, hacc);
+
+    // ---------------- block scan: S (u64), H^ (fp64), next PINNED / next nonzero-h ------
+    uint64_t sinc = sacc;
+    double hinc = hacc;
+    int32_t fb = barmask ? k0 + __ffs(barmask) - 1 : kInfIdx;
+    int32_t fz = nzmask ? k0 + __ffs(nzmask) - 1 : kInfIdx;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t so = __shfl_up_sync(0xffffffffu, sinc, d);
+      const double ho = __shfl_up_sync(0xffffffffu, hinc, d);
+      const int32_t bo = __shfl_down_sync(0xffffffffu, fb, d);
+      const int32_t zo = __shfl_down_sync(0xffffffffu, fz, d);
+      if (lane >= d) {
+        sinc += so;
+        hinc = __dadd_rn(ho, hinc);
+      }
+      if (lane + d < 32) {
+        fb = min(fb, bo);
+        fz = min(fz, zo);
+      }
+    }
+    uint64_t sexc = __shfl_up_sync(0xffffffffu, sinc, 1);
+    double hexc = __shfl_up_sync(0xffffffffu, hinc, 1);
+    int32_t bexc = __shfl_down_sync(0xffffffffu, fb, 1);
+    int32_t zexc = __shfl_down_sync(0xffffffffu, fz, 1);
+    if (lane == 0) {
+      sexc = 0;
+      hexc = 0.0;
+    }
+    if (lane == 31) {
+      bexc = kInfIdx;
+      zexc = kInfIdx;
+      sc.wS[warp] = sinc;
+      sc.wH[warp] = hinc;
+    }
+    if (lane == 0) {
+      sc.wF[warp] = fb;
+      sc.wZ[warp] = fz;
+    }
+    const int bad_any = __syncthreads_or(bad);
+    uint64_t S_car, S_total;
+    double H_car;
+    int32_t nb_right, nz_right;
+    {
+      // cross-warp: lane l < W holds warp l's totals; shuffle scan over the (<= 16) warps
+      uint64_t ws = lane < W ? sc.wS[lane] : 0ull;
+      double wh = lane < W ? sc.wH[lane] : 0.0;
+      int32_t wb = lane < W ? sc.wF[lane] : kInfIdx;
+      int32_t wz = lane < W ? sc.wZ[lane] : kInfIdx;
+#pragma unroll
+      for (int d = 1; d < kMaxWarps; d <<= 1) {
+        const uint64_t so = __shfl_up_sync(0xffffffffu, ws, d);
+        const double ho = __shfl_up_sync(0xffffffffu, wh, d);
+        const int32_t bo = __shfl_down_sync(0xffffffffu, wb, d);
+        const int32_t zo = __shfl_down_sync(0xffffffffu, wz, d);
+        if (lane >= d) {
+          ws += so;
+          wh = __dadd_rn(ho, wh);
+        }
+        if (lane + d < 32) {
+          wb = min(wb, bo);
+          wz = min(wz, zo);
+        }
+      }
+      const uint64_t sprev = __shfl_sync(0xffffffffu, ws, warp ? warp - 1 : 0);
+      const double hprev = __shfl_sync(0xffffffffu, wh, warp ? warp - 1 : 0);
+      const int32_t bnext = __shfl_sync(0xffffffffu, wb, min(warp + 1, 31));
+      const int32_t znext = __shfl_sync(0xffffffffu, wz, min(warp + 1, 31));
+      S_car = (warp ? sprev : 0ull) + sexc;
+      H_car = __dadd_rn(warp ? hprev : 0.0, hexc);
+      nb_right = min(bexc, warp + 1 < W ? bnext : kInfIdx);
+      nz_right = min(zexc, warp + 1 < W ? znext : kInfIdx);
+      S_total = __shfl_sync(0xffffffffu, ws, W - 1);
+    }
+    v.S_total = S_total;
+    if (!bad_any) {
+#pragma unroll
+      for (int q = 0; q < K; q += 2) {
+        const int k = k0 + q;
+        if (k < n) {
+          const uint32_t o = swz((uint32_t)k);
+          sm<ulonglong2>(v.sr, o) = make_ulonglong2(S_car + spre[q], S_car + spre[q + 1]);
+          sm<double2>(v.hr, o) = make_double2(__dadd_rn(H_car, hpre[q]), __dadd_rn(H_car, hpre[q + 1]));
+        }
+      }
+      if (k0 <= n - 1 && n - 1 < k0 + K) {  // sentinels at slots n, n + 1
+        sm<uint64_t>(v.sr, swz((uint32_t)n)) = S_total;
+        sm<uint64_t>(v.sr, swz((uint32_t)n + 1u)) = ~0ull;
+        sm<double>(v.hr, swz((uint32_t)n)) = __dadd_rn(H_car, hacc);
+      }
+    }
+    __syncthreads();
+
+    if (bad_any || a.dbg == 2) {
+      if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_ERR_INVALID_ARG);
+    } else {
+      if (kPhaseHooks && a.dbg == 3) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
+      // ---------------- phase B0: zero-cost windows -------------------------------------
+      // A run of consecutive h = 0 items (FREE, or EVICTABLE with c = 0) is a zero-cost
+      // window iff its span covers R; the lowest such run head is the answer (exact cost
+      // 0 is the global minimum, R4).  Each thread checks the run heads of its chunk.
+      int zi = kInfIdx, ze = -1, znev = 0;
+      {
+        const int cnt = n - k0;
+        const uint32_t valid = cnt >= K ? (K == 32 ? ~0u : ((1u << K) - 1u)) : (cnt > 0 ? (1u << cnt) - 1u : 0u);
+        const uint32_t zm = valid & ~barmask & ~nzmask;
+        const uint32_t heads = zm & ~(zm << 1);
+        // items that alone cover R (sizes from the prefix registers; the chunk's last
+        // item is left to the span test below)
+        uint32_t cov = 0;
+#pragma unroll
+        for (int q = 0; q + 1 < K; ++q) cov |= (uint32_t)(spre[q + 1] - spre[q] >= v.R) << q;
+        const uint32_t one = heads & cov;  // zero windows [q, q]
+        const uint32_t lower = one ? (1u << (__ffs(one) - 1)) - 1u : ~0u;
+        // heads below the first of them whose run may be longer than one item
+        uint32_t multi = heads & ~one & lower & ((zm >> 1) | (1u << (K - 1)));
+        int zstop = n;
+        while (multi) {
+          const int q = __ffs(multi) - 1;
+          multi &= multi - 1u;
+          const uint32_t mb = barmask >> q, mz = nzmask >> q;
+          const int nb = mb ? k0 + q + __ffs(mb) - 1 : nb_right;
+          const int nz = mz ? k0 + q + __ffs(mz) - 1 : nz_right;
+          const int stop = min(min(nb, nz), n);
+          if (v.S_at(stop) - v.S_at(k0 + q) >= v.R) {
+            zi = k0 + q;
+            zstop = stop;
+            break;
+          }
+        }
+        if (zi == kInfIdx && one) {
+          zi = k0 + __ffs(one) - 1;
+          zstop = zi + 1;
+        }
+        if (zi != kInfIdx) {
+          const uint64_t target = v.S_at(zi) + v.R;
+          int lo = zi + 1, hi = zstop;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (v.S_at(mid) >= target) hi = mid;
+            else lo = mid + 1;
+          }
+          ze = lo;
+          for (int k = zi; k < ze; ++k) znev += (__double_as_longlong(v.v_at(k)) >= 0);
+        }
+      }
+      const int zw = warp_allreduce(zi, [](int x, int y) { return min(x, y); });
+      if (lane == 0) sc.wZ[warp] = zw;
+      __syncthreads();
+      const int zmin = warp_allreduce(lane < W ? sc.wZ[lane] : kInfIdx, [](int x, int y) { return min(x, y); });
+      if (kPhaseHooks && a.dbg == 4) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
+      if (zmin != kInfIdx) {
+        if (zi == zmin) write_result(a.out + p, zi, ze - 1, v.S_at(ze) - v.S_at(zi), 0.0, znev, COOP_OK);
+      } else {
+      // ---------------- phase B1: chunk pruning -------------------------------------------
+      // Thread t's starts i in [k0, kl] have ends e(i) >= e(k0) (monotone) and prefixes
+      // H[i] <= H[kl], so every window cost there is >= H[e(k0)] - H[kl].  e(k0) by one
+      // binary search per thread; the first start's window (when PINNED-free) gives an
+      // upper bound; chunks whose lower bound exceeds the CTA's best upper bound by more
+      // than the filter's margin cannot hold the winner (nor tie it after rounding) and
+      // skip the per-start work.  Bounds: |C^ - C| <= gerr (H^[e] + H^[i]) for any pair.
+      const int kl = min(k0 + K, n) - 1;
+      int e0 = n + 1;
+      double LBt = kInf, Ut = kInf;
+      if (k0 < n && !(barmask & 1u)) {
+        const uint64_t target = S_car + spre[0] + v.R;  // S[k0] + R  (< 2^63)
+        int lo = k0 + 1, hi = n + 1;                    // S[n + 1] = ~0 >= target
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (v.S_at(mid) >= target) hi = mid;
+          else lo = mid + 1;
+        }
+        e0 = lo;
+      } else if (k0 < n) {
+        e0 = -1;  // first start PINNED: no sample; ends of the others found below
+      }
+      if (k0 < n && e0 <= n) {
+        const int nb = barmask ? k0 + __ffs(barmask) - 1 : nb_right;
+        double hl = hpre[0];  // hpre[kl - k0] with constant indices (stays in registers)
+#pragma unroll
+        for (int q = 1; q < K; ++q)
+          if (k0 + q <= kl) hl = hpre[q];
+        const double Hl = __dadd_rn(H_car, hl);
+        if (e0 >= 0) {
+          const double He = v.H_at(e0), Hk = __dadd_rn(H_car, hpre[0]);
+          if (nb >= e0) Ut = (He - Hk) + v.gerr * (He + Hk);
+          LBt = (He - Hl) - v.gerr * (He + Hl);
+        } else {
+          LBt = -kInf;  // no bound without e(k0): keep the chunk
+        }
+      }
+      {
+        const double uw = warp_allreduce(Ut, [](double x, double y) { return fmin(x, y); });
+        if (lane == 0) sc.wP[warp] = uw;
+        if (tid == 0) sc.nsurv = 0;
+      }
+      __syncthreads();
+      const double Upre = warp_allreduce(lane < W ? sc.wP[lane] : kInf,
+                                         [](double x, double y) { return fmin(x, y); });
+      const bool survive = (k0 < n) && (e0 <= n) && !(LBt > Upre * (1.0 + 0x1p-45));
+      {  // compact the surviving chunks (one shared atomic per warp)
+        const uint32_t bal = __ballot_sync(0xffffffffu, survive);
+        int wbase = 0;
+        if (lane == 0 && bal) wbase = atomicAdd(&sc.nsurv, __popc(bal));
+        wbase = __shfl_sync(0xffffffffu, wbase, 0);
+        if (survive)
+          v.list[wbase + __popc(bal & ((1u << lane) - 1u))] =
+              chunk_rec(k0, e0 >= 0 ? e0 : k0 + 1, barmask, nzmask, nb_right, nz_right);
+      }
+      __syncthreads();
+      if (kPhaseHooks && a.dbg == 5) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
+      // every start of the surviving chunks, spread evenly over the CTA's threads
+      const int nslots = sc.nsurv * K;
+      LaneBest bl;
+      bl.U = kInf; bl.L = kInf; bl.L2 = kInf; bl.li = -1; bl.le = -1;
+      bl.xb = ~0ull; bl.xi = kInfIdx; bl.xe = -1;
+      for (int sl = tid; sl < nslots; sl += T)
+        eval_start<0>(v, v.list[sl / K], sl % K, 0.0, 0, 0, sc, bl);
+      const double Uw = warp_allreduce(bl.U, [](double x, double y) { return fmin(x, y); });
+      const uint64_t xw = warp_allreduce(bl.xb, [](uint64_t x, uint64_t y) { return x < y ? x : y; });
+      if (lane == 0) {
+        sc.wU[warp] = Uw;
+        sc.bcost[warp] = xw;
+      }
+      if (tid == 0) sc.ncand = 0;
+      __syncthreads();
+      const double Umin = warp_allreduce(lane < W ? sc.wU[lane] : kInf,
+                                         [](double x, double y) { return fmin(x, y); });
+      const uint64_t xbest = warp_allreduce(lane < W ? sc.bcost[lane] : ~0ull,
+                                            [](uint64_t x, uint64_t y) { return x < y ? x : y; });
+      const double thresh = fmin(Umin, __longlong_as_double((long long)xbest)) * (1.0 + 0x1p-45);
+      if (kPhaseHooks && a.dbg == 6) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
+      // a lane with exactly one start under the threshold appends it; two or more re-walk
+      const bool multi = (bl.L2 <= thresh);
+      if (bl.L <= thresh && !multi) {
+        const int slot = atomicAdd(&sc.ncand, 1);
+        if (slot < kCandCap) sc.cand[slot] = ((uint32_t)bl.li << 16) | (uint32_t)(bl.le - bl.li);
+      }
+      const int xiw = warp_allreduce(bl.xb == xbest ? bl.xi : kInfIdx, [](int x, int y) { return min(x, y); });
+      const int mw = __any_sync(0xffffffffu, multi) ? 1 : 0;
+      if (lane == 0) {
+        sc.bfirst[warp] = xiw;
+        sc.bnev[warp] = mw;
+      }
+      __syncthreads();
+      const int xfirst = warp_allreduce(lane < W ? sc.bfirst[lane] : kInfIdx, [](int x, int y) { return min(x, y); });
+      const int any_multi = warp_allreduce(lane < W ? sc.bnev[lane] : 0, [](int x, int y) { return x | y; });
+      const int nc0 = sc.ncand;
+      const bool x_owner = (xbest != ~0ull) && bl.xi == xfirst && bl.xb == xbest;
+      if (Umin == kInf && xbest == ~0ull) {
+        if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_INFEASIBLE);
+      } else if (nc0 == 0 && !any_multi) {
+        // no window of inexactly known cost can reach the exact best: the owner writes
+        if (x_owner) {
+          int nev = 0;
+          for (int k = bl.xi; k < bl.xe; ++k) nev += (__double_as_longlong(v.v_at(k)) >= 0);
+          write_result(a.out + p, bl.xi, bl.xe - 1, v.S_at(bl.xe) - v.S_at(bl.xi),
+                       __longlong_as_double((long long)xbest), nev, COOP_OK);
+        }
+      } else {
+        // ------------- candidates: exact 192-bit re-summation, RN, (cost, first) min ----
+        if (x_owner) {
+          int nev = 0;
+          for (int k = bl.xi; k < bl.xe; ++k) nev += (__double_as_longlong(v.v_at(k)) >= 0);
+          sc.xend = bl.xe;
+          sc.xnev = nev;
+        }
+        __syncthreads();
+        uint64_t best = xbest;  // meaningful in thread 0
+        int bfirst = xfirst, bend = xbest != ~0ull ? sc.xend : -1, bnev = xbest != ~0ull ? sc.xnev : 0;
+        const bool wmulti = __any_sync(0xffffffffu, bl.L <= thresh);  // this warp holds candidates
+        // rounds: the prebuilt list (no multi), or re-walks restricted to windows of
+        // kCandCap consecutive starts (cannot overflow the list)
+        const int rounds = any_multi ? (n + kCandCap - 1) / kCandCap : 1;
+        for (int rd = 0; rd < rounds; ++rd) {
+          if (any_multi) {
+            __syncthreads();
+            if (tid == 0) sc.ncand = 0;
+            __syncthreads();
+            const int w_lo = rd * kCandCap, w_hi = w_lo + kCandCap;
+            if (wmulti) {
+              LaneBest dummy = bl;
+              for (int sl = tid; sl < nslots; sl += T)
+                eval_start<1>(v, v.list[sl / K], sl % K, thresh, w_lo, w_hi, sc, dummy);
+            }
+            __syncthreads();
+          }
+          const int nc = min(sc.ncand, kCandCap);
+          if (nc <= W) {
+            // few candidates: the whole CTA sums each window (short latency chain)
+            for (int c = 0; c < nc; ++c) {
+              const uint32_t cd = sc.cand[c];
+              const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
+              U192 acc = u192_zero();
+              int nev = 0;
+              if (i + warp * 32 < e) {  // warp-uniform: warps without items skip
+                for (int k = i + tid; k < e; k += T) {
+                  const double hv = v.v_at(k);
+                  nev += (__double_as_longlong(hv) >= 0);
+                  acc = u192_add(acc, u192_from_double(hv));
+                }
+                acc = warp_sum192(acc, nev);
+              }
+              const int par = c & 1;
+              if (lane == 0) {
+                sc.part[par][warp][0] = acc.w0;
+                sc.part[par][warp][1] = acc.w1;
+                sc.part[par][warp][2] = acc.w2;
+                sc.partn[par][warp] = nev;
+              }
+              __syncthreads();
+              if (warp == 0) {
+                U192 t = u192_zero();
+                int tn = 0;
+                if (lane < W) {
+                  t.w0 = sc.part[par][lane][0];
+                  t.w1 = sc.part[par][lane][1];
+                  t.w2 = sc.part[par][lane][2];
+                  tn = sc.partn[par][lane];
+                }
+                t = warp_sum192(t, tn);
+                const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(t));
+                if (lane == 0 && better(cb, i, best, bfirst)) {
+                  best = cb;
+                  bfirst = i;
+                  bend = e;
+                  bnev = tn;
+                }
+              }
+            }
+          } else {
+            // many candidates: one warp per candidate window
+            uint64_t wbest = ~0ull;
+            int32_t wfirst = kInfIdx, wend = -1, wnev = 0;
+            for (int c = warp; c < nc; c += W) {
+              const uint32_t cd = sc.cand[c];
+              const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
+              U192 acc = u192_zero();
+              int nev = 0;
+              for (int k = i + lane; k < e; k += 32) {
+                const double hv = v.v_at(k);
+                nev += (__double_as_longlong(hv) >= 0);
+                acc = u192_add(acc, u192_from_double(hv));
+              }
+              acc = warp_sum192(acc, nev);
+              const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(acc));
+              if (better(cb, i, wbest, wfirst)) {
+                wbest = cb;
+                wfirst = i;
+                wend = e;
+                wnev = nev;
+              }
+            }
+            if (lane == 0) {
+              sc.bcost[warp] = wbest;
+              sc.bfirst[warp] = wfirst;
+              sc.bend[warp] = wend;
+              sc.bnev[warp] = wnev;
+            }
+            __syncthreads();
+            if (tid == 0) {
+              for (int w = 0; w < W; ++w) {
+                if (sc.bend[w] >= 0 && better(sc.bcost[w], sc.bfirst[w], best, bfirst)) {
+                  best = sc.bcost[w];
+                  bfirst = sc.bfirst[w];
+                  bend = sc.bend[w];
+                  bnev = sc.bnev[w];
+                }
+              }
+            }
+          }
+        }
+        if (tid == 0)
+          write_result(a.out + p, bfirst, bend - 1, v.S_at(bend) - v.S_at(bfirst),
+                       __longlong_as_double((long long)best), bnev, COOP_OK);
+      }
+      }
+    }
+  }
+}
+
 template <int K, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
     search_kernel(const __grid_constant__ CUtensorMap m_ss, const __grid_constant__ CUtensorMap m_c,
@@ -393,6 +811,28 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
   }
 
+  if (a.pending) {
+    // second pass after the streaming kernel: only the pools it marked COOP_PENDING_;
+    // chunks of T pools are scanned with one status read per thread, plain staging
+    for (int64_t c0 = (int64_t)blockIdx.x * T; c0 < a.n_pools; c0 += (int64_t)gridDim.x * T) {
+      __syncthreads();
+      if (tid == 0) sc.nplist = 0;
+      __syncthreads();
+      const int64_t q = c0 + tid;
+      if (q < a.n_pools && a.out[q].status == COOP_PENDING_) sc.plist[atomicAdd(&sc.nplist, 1)] = tid;
+      __syncthreads();
+      const int np = sc.nplist;
+      for (int u = 0; u < np; ++u) {
+        const int64_t p = c0 + sc.plist[u];
+        smem_t *stage = base_ptr;
+        stage_plain(a, stage, p);
+        __syncthreads();
+        search_pool<K>(a, sc, Ebuf, stage, p, a.req[p]);
+        __syncthreads();
+      }
+    }
+    return;
+  }
   int it = 0, s = 0;
   uint32_t phase = 0;
   for (int64_t p = blockIdx.x; p < a.n_pools; p += gridDim.x, ++it) {
@@ -404,412 +844,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
       stage_plain(a, stage, p);
       __syncthreads();
     }
-    PoolView v;
-    v.sr = stage;
-    v.hr = stage + a.region_bytes;
-    v.vr = stage + 2u * a.region_bytes;
-    v.list = Ebuf;
-    v.n = n;
-    v.R = Rraw < kRClamp ? Rraw : kRClamp;
-    v.gerr = a.gerr;
-    const int k0 = tid * K;
-
-    if (a.dbg == 1) {
-      if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK);
-      goto pool_done;
-    }
-    {
-      // ---------------- phase A: decode, validate, h = c/s, local prefixes -------------
-      bool bad = (Rraw == 0);
-      uint32_t barmask = 0, nzmask = 0;
-      uint64_t spre[K];
-      double hpre[K];
-      uint64_t sacc = 0;
-      double hacc = 0.0;
-      if (k0 + K <= n)  // warp-uniform except in the last warp
-        phase_a<K, true>(v, k0, n, bad, barmask, nzmask, spre, hpre, sacc, hacc);
-      else
-        phase_a<K, false>(v, k0, n, bad, barmask, nzmask, spre, hpre, sacc, hacc);
-
-      // ---------------- block scan: S (u64), H^ (fp64), next PINNED / next nonzero-h ------
-      uint64_t sinc = sacc;
-      double hinc = hacc;
-      int32_t fb = barmask ? k0 + __ffs(barmask) - 1 : kInfIdx;
-      int32_t fz = nzmask ? k0 + __ffs(nzmask) - 1 : kInfIdx;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t so = __shfl_up_sync(0xffffffffu, sinc, d);
-        const double ho = __shfl_up_sync(0xffffffffu, hinc, d);
-        const int32_t bo = __shfl_down_sync(0xffffffffu, fb, d);
-        const int32_t zo = __shfl_down_sync(0xffffffffu, fz, d);
-        if (lane >= d) {
-          sinc += so;
-          hinc = __dadd_rn(ho, hinc);
-        }
-        if (lane + d < 32) {
-          fb = min(fb, bo);
-          fz = min(fz, zo);
-        }
-      }
-      uint64_t sexc = __shfl_up_sync(0xffffffffu, sinc, 1);
-      double hexc = __shfl_up_sync(0xffffffffu, hinc, 1);
-      int32_t bexc = __shfl_down_sync(0xffffffffu, fb, 1);
-      int32_t zexc = __shfl_down_sync(0xffffffffu, fz, 1);
-      if (lane == 0) {
-        sexc = 0;
-        hexc = 0.0;
-      }
-      if (lane == 31) {
-        bexc = kInfIdx;
-        zexc = kInfIdx;
-        sc.wS[warp] = sinc;
-        sc.wH[warp] = hinc;
-      }
-      if (lane == 0) {
-        sc.wF[warp] = fb;
-        sc.wZ[warp] = fz;
-      }
-      const int bad_any = __syncthreads_or(bad);
-      uint64_t S_car, S_total;
-      double H_car;
-      int32_t nb_right, nz_right;
-      {
-        // cross-warp: lane l < W holds warp l's totals; shuffle scan over the (<= 16) warps
-        uint64_t ws = lane < W ? sc.wS[lane] : 0ull;
-        double wh = lane < W ? sc.wH[lane] : 0.0;
-        int32_t wb = lane < W ? sc.wF[lane] : kInfIdx;
-        int32_t wz = lane < W ? sc.wZ[lane] : kInfIdx;
-#pragma unroll
-        for (int d = 1; d < kMaxWarps; d <<= 1) {
-          const uint64_t so = __shfl_up_sync(0xffffffffu, ws, d);
-          const double ho = __shfl_up_sync(0xffffffffu, wh, d);
-          const int32_t bo = __shfl_down_sync(0xffffffffu, wb, d);
-          const int32_t zo = __shfl_down_sync(0xffffffffu, wz, d);
-          if (lane >= d) {
-            ws += so;
-            wh = __dadd_rn(ho, wh);
-          }
-          if (lane + d < 32) {
-            wb = min(wb, bo);
-            wz = min(wz, zo);
-          }
-        }
-        const uint64_t sprev = __shfl_sync(0xffffffffu, ws, warp ? warp - 1 : 0);
-        const double hprev = __shfl_sync(0xffffffffu, wh, warp ? warp - 1 : 0);
-        const int32_t bnext = __shfl_sync(0xffffffffu, wb, min(warp + 1, 31));
-        const int32_t znext = __shfl_sync(0xffffffffu, wz, min(warp + 1, 31));
-        S_car = (warp ? sprev : 0ull) + sexc;
-        H_car = __dadd_rn(warp ? hprev : 0.0, hexc);
-        nb_right = min(bexc, warp + 1 < W ? bnext : kInfIdx);
-        nz_right = min(zexc, warp + 1 < W ? znext : kInfIdx);
-        S_total = __shfl_sync(0xffffffffu, ws, W - 1);
-      }
-      v.S_total = S_total;
-      if (!bad_any) {
-#pragma unroll
-        for (int q = 0; q < K; q += 2) {
-          const int k = k0 + q;
-          if (k < n) {
-            const uint32_t o = swz((uint32_t)k);
-            sm<ulonglong2>(v.sr, o) = make_ulonglong2(S_car + spre[q], S_car + spre[q + 1]);
-            sm<double2>(v.hr, o) = make_double2(__dadd_rn(H_car, hpre[q]), __dadd_rn(H_car, hpre[q + 1]));
-          }
-        }
-        if (k0 <= n - 1 && n - 1 < k0 + K) {  // sentinels at slots n, n + 1
-          sm<uint64_t>(v.sr, swz((uint32_t)n)) = S_total;
-          sm<uint64_t>(v.sr, swz((uint32_t)n + 1u)) = ~0ull;
-          sm<double>(v.hr, swz((uint32_t)n)) = __dadd_rn(H_car, hacc);
-        }
-      }
-      __syncthreads();
-
-      if (bad_any || a.dbg == 2) {
-        if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_ERR_INVALID_ARG);
-      } else {
-        if (kPhaseHooks && a.dbg == 3) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
-        // ---------------- phase B0: zero-cost windows -------------------------------------
-        // A run of consecutive h = 0 items (FREE, or EVICTABLE with c = 0) is a zero-cost
-        // window iff its span covers R; the lowest such run head is the answer (exact cost
-        // 0 is the global minimum, R4).  Each thread checks the run heads of its chunk.
-        int zi = kInfIdx, ze = -1, znev = 0;
-        {
-          const int cnt = n - k0;
-          const uint32_t valid = cnt >= K ? (K == 32 ? ~0u : ((1u << K) - 1u)) : (cnt > 0 ? (1u << cnt) - 1u : 0u);
-          const uint32_t zm = valid & ~barmask & ~nzmask;
-          const uint32_t heads = zm & ~(zm << 1);
-          // items that alone cover R (sizes from the prefix registers; the chunk's last
-          // item is left to the span test below)
-          uint32_t cov = 0;
-#pragma unroll
-          for (int q = 0; q + 1 < K; ++q) cov |= (uint32_t)(spre[q + 1] - spre[q] >= v.R) << q;
-          const uint32_t one = heads & cov;  // zero windows [q, q]
-          const uint32_t lower = one ? (1u << (__ffs(one) - 1)) - 1u : ~0u;
-          // heads below the first of them whose run may be longer than one item
-          uint32_t multi = heads & ~one & lower & ((zm >> 1) | (1u << (K - 1)));
-          int zstop = n;
-          while (multi) {
-            const int q = __ffs(multi) - 1;
-            multi &= multi - 1u;
-            const uint32_t mb = barmask >> q, mz = nzmask >> q;
-            const int nb = mb ? k0 + q + __ffs(mb) - 1 : nb_right;
-            const int nz = mz ? k0 + q + __ffs(mz) - 1 : nz_right;
-            const int stop = min(min(nb, nz), n);
-            if (v.S_at(stop) - v.S_at(k0 + q) >= v.R) {
-              zi = k0 + q;
-              zstop = stop;
-              break;
-            }
-          }
-          if (zi == kInfIdx && one) {
-            zi = k0 + __ffs(one) - 1;
-            zstop = zi + 1;
-          }
-          if (zi != kInfIdx) {
-            const uint64_t target = v.S_at(zi) + v.R;
-            int lo = zi + 1, hi = zstop;
-            while (lo < hi) {
-              const int mid = (lo + hi) >> 1;
-              if (v.S_at(mid) >= target) hi = mid;
-              else lo = mid + 1;
-            }
-            ze = lo;
-            for (int k = zi; k < ze; ++k) znev += (__double_as_longlong(v.v_at(k)) >= 0);
-          }
-        }
-        const int zw = warp_allreduce(zi, [](int x, int y) { return min(x, y); });
-        if (lane == 0) sc.wZ[warp] = zw;
-        __syncthreads();
-        const int zmin = warp_allreduce(lane < W ? sc.wZ[lane] : kInfIdx, [](int x, int y) { return min(x, y); });
-        if (kPhaseHooks && a.dbg == 4) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
-        if (zmin != kInfIdx) {
-          if (zi == zmin) write_result(a.out + p, zi, ze - 1, v.S_at(ze) - v.S_at(zi), 0.0, znev, COOP_OK);
-        } else {
-        // ---------------- phase B1: chunk pruning -------------------------------------------
-        // Thread t's starts i in [k0, kl] have ends e(i) >= e(k0) (monotone) and prefixes
-        // H[i] <= H[kl], so every window cost there is >= H[e(k0)] - H[kl].  e(k0) by one
-        // binary search per thread; the first start's window (when PINNED-free) gives an
-        // upper bound; chunks whose lower bound exceeds the CTA's best upper bound by more
-        // than the filter's margin cannot hold the winner (nor tie it after rounding) and
-        // skip the per-start work.  Bounds: |C^ - C| <= gerr (H^[e] + H^[i]) for any pair.
-        const int kl = min(k0 + K, n) - 1;
-        int e0 = n + 1;
-        double LBt = kInf, Ut = kInf;
-        if (k0 < n && !(barmask & 1u)) {
-          const uint64_t target = S_car + spre[0] + v.R;  // S[k0] + R  (< 2^63)
-          int lo = k0 + 1, hi = n + 1;                    // S[n + 1] = ~0 >= target
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (v.S_at(mid) >= target) hi = mid;
-            else lo = mid + 1;
-          }
-          e0 = lo;
-        } else if (k0 < n) {
-          e0 = -1;  // first start PINNED: no sample; ends of the others found below
-        }
-        if (k0 < n && e0 <= n) {
-          const int nb = barmask ? k0 + __ffs(barmask) - 1 : nb_right;
-          double hl = hpre[0];  // hpre[kl - k0] with constant indices (stays in registers)
-#pragma unroll
-          for (int q = 1; q < K; ++q)
-            if (k0 + q <= kl) hl = hpre[q];
-          const double Hl = __dadd_rn(H_car, hl);
-          if (e0 >= 0) {
-            const double He = v.H_at(e0), Hk = __dadd_rn(H_car, hpre[0]);
-            if (nb >= e0) Ut = (He - Hk) + v.gerr * (He + Hk);
-            LBt = (He - Hl) - v.gerr * (He + Hl);
-          } else {
-            LBt = -kInf;  // no bound without e(k0): keep the chunk
-          }
-        }
-        {
-          const double uw = warp_allreduce(Ut, [](double x, double y) { return fmin(x, y); });
-          if (lane == 0) sc.wP[warp] = uw;
-          if (tid == 0) sc.nsurv = 0;
-        }
-        __syncthreads();
-        const double Upre = warp_allreduce(lane < W ? sc.wP[lane] : kInf,
-                                           [](double x, double y) { return fmin(x, y); });
-        const bool survive = (k0 < n) && (e0 <= n) && !(LBt > Upre * (1.0 + 0x1p-45));
-        {  // compact the surviving chunks (one shared atomic per warp)
-          const uint32_t bal = __ballot_sync(0xffffffffu, survive);
-          int wbase = 0;
-          if (lane == 0 && bal) wbase = atomicAdd(&sc.nsurv, __popc(bal));
-          wbase = __shfl_sync(0xffffffffu, wbase, 0);
-          if (survive)
-            v.list[wbase + __popc(bal & ((1u << lane) - 1u))] =
-                chunk_rec(k0, e0 >= 0 ? e0 : k0 + 1, barmask, nzmask, nb_right, nz_right);
-        }
-        __syncthreads();
-        if (kPhaseHooks && a.dbg == 5) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
-        // every start of the surviving chunks, spread evenly over the CTA's threads
-        const int nslots = sc.nsurv * K;
-        LaneBest bl;
-        bl.U = kInf; bl.L = kInf; bl.L2 = kInf; bl.li = -1; bl.le = -1;
-        bl.xb = ~0ull; bl.xi = kInfIdx; bl.xe = -1;
-        for (int sl = tid; sl < nslots; sl += T)
-          eval_start<0>(v, v.list[sl / K], sl % K, 0.0, 0, 0, sc, bl);
-        const double Uw = warp_allreduce(bl.U, [](double x, double y) { return fmin(x, y); });
-        const uint64_t xw = warp_allreduce(bl.xb, [](uint64_t x, uint64_t y) { return x < y ? x : y; });
-        if (lane == 0) {
-          sc.wU[warp] = Uw;
-          sc.bcost[warp] = xw;
-        }
-        if (tid == 0) sc.ncand = 0;
-        __syncthreads();
-        const double Umin = warp_allreduce(lane < W ? sc.wU[lane] : kInf,
-                                           [](double x, double y) { return fmin(x, y); });
-        const uint64_t xbest = warp_allreduce(lane < W ? sc.bcost[lane] : ~0ull,
-                                              [](uint64_t x, uint64_t y) { return x < y ? x : y; });
-        const double thresh = fmin(Umin, __longlong_as_double((long long)xbest)) * (1.0 + 0x1p-45);
-        if (kPhaseHooks && a.dbg == 6) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); goto pool_done; }
-        // a lane with exactly one start under the threshold appends it; two or more re-walk
-        const bool multi = (bl.L2 <= thresh);
-        if (bl.L <= thresh && !multi) {
-          const int slot = atomicAdd(&sc.ncand, 1);
-          if (slot < kCandCap) sc.cand[slot] = ((uint32_t)bl.li << 16) | (uint32_t)(bl.le - bl.li);
-        }
-        const int xiw = warp_allreduce(bl.xb == xbest ? bl.xi : kInfIdx, [](int x, int y) { return min(x, y); });
-        const int mw = __any_sync(0xffffffffu, multi) ? 1 : 0;
-        if (lane == 0) {
-          sc.bfirst[warp] = xiw;
-          sc.bnev[warp] = mw;
-        }
-        __syncthreads();
-        const int xfirst = warp_allreduce(lane < W ? sc.bfirst[lane] : kInfIdx, [](int x, int y) { return min(x, y); });
-        const int any_multi = warp_allreduce(lane < W ? sc.bnev[lane] : 0, [](int x, int y) { return x | y; });
-        const int nc0 = sc.ncand;
-        const bool x_owner = (xbest != ~0ull) && bl.xi == xfirst && bl.xb == xbest;
-        if (Umin == kInf && xbest == ~0ull) {
-          if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_INFEASIBLE);
-        } else if (nc0 == 0 && !any_multi) {
-          // no window of inexactly known cost can reach the exact best: the owner writes
-          if (x_owner) {
-            int nev = 0;
-            for (int k = bl.xi; k < bl.xe; ++k) nev += (__double_as_longlong(v.v_at(k)) >= 0);
-            write_result(a.out + p, bl.xi, bl.xe - 1, v.S_at(bl.xe) - v.S_at(bl.xi),
-                         __longlong_as_double((long long)xbest), nev, COOP_OK);
-          }
-        } else {
-          // ------------- candidates: exact 192-bit re-summation, RN, (cost, first) min ----
-          if (x_owner) {
-            int nev = 0;
-            for (int k = bl.xi; k < bl.xe; ++k) nev += (__double_as_longlong(v.v_at(k)) >= 0);
-            sc.xend = bl.xe;
-            sc.xnev = nev;
-          }
-          __syncthreads();
-          uint64_t best = xbest;  // meaningful in thread 0
-          int bfirst = xfirst, bend = xbest != ~0ull ? sc.xend : -1, bnev = xbest != ~0ull ? sc.xnev : 0;
-          const bool wmulti = __any_sync(0xffffffffu, bl.L <= thresh);  // this warp holds candidates
-          // rounds: the prebuilt list (no multi), or re-walks restricted to windows of
-          // kCandCap consecutive starts (cannot overflow the list)
-          const int rounds = any_multi ? (n + kCandCap - 1) / kCandCap : 1;
-          for (int rd = 0; rd < rounds; ++rd) {
-            if (any_multi) {
-              __syncthreads();
-              if (tid == 0) sc.ncand = 0;
-              __syncthreads();
-              const int w_lo = rd * kCandCap, w_hi = w_lo + kCandCap;
-              if (wmulti) {
-                LaneBest dummy = bl;
-                for (int sl = tid; sl < nslots; sl += T)
-                  eval_start<1>(v, v.list[sl / K], sl % K, thresh, w_lo, w_hi, sc, dummy);
-              }
-              __syncthreads();
-            }
-            const int nc = min(sc.ncand, kCandCap);
-            if (nc <= W) {
-              // few candidates: the whole CTA sums each window (short latency chain)
-              for (int c = 0; c < nc; ++c) {
-                const uint32_t cd = sc.cand[c];
-                const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
-                U192 acc = u192_zero();
-                int nev = 0;
-                if (i + warp * 32 < e) {  // warp-uniform: warps without items skip
-                  for (int k = i + tid; k < e; k += T) {
-                    const double hv = v.v_at(k);
-                    nev += (__double_as_longlong(hv) >= 0);
-                    acc = u192_add(acc, u192_from_double(hv));
-                  }
-                  acc = warp_sum192(acc, nev);
-                }
-                const int par = c & 1;
-                if (lane == 0) {
-                  sc.part[par][warp][0] = acc.w0;
-                  sc.part[par][warp][1] = acc.w1;
-                  sc.part[par][warp][2] = acc.w2;
-                  sc.partn[par][warp] = nev;
-                }
-                __syncthreads();
-                if (warp == 0) {
-                  U192 t = u192_zero();
-                  int tn = 0;
-                  if (lane < W) {
-                    t.w0 = sc.part[par][lane][0];
-                    t.w1 = sc.part[par][lane][1];
-                    t.w2 = sc.part[par][lane][2];
-                    tn = sc.partn[par][lane];
-                  }
-                  t = warp_sum192(t, tn);
-                  const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(t));
-                  if (lane == 0 && better(cb, i, best, bfirst)) {
-                    best = cb;
-                    bfirst = i;
-                    bend = e;
-                    bnev = tn;
-                  }
-                }
-              }
-            } else {
-              // many candidates: one warp per candidate window
-              uint64_t wbest = ~0ull;
-              int32_t wfirst = kInfIdx, wend = -1, wnev = 0;
-              for (int c = warp; c < nc; c += W) {
-                const uint32_t cd = sc.cand[c];
-                const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
-                U192 acc = u192_zero();
-                int nev = 0;
-                for (int k = i + lane; k < e; k += 32) {
-                  const double hv = v.v_at(k);
-                  nev += (__double_as_longlong(hv) >= 0);
-                  acc = u192_add(acc, u192_from_double(hv));
-                }
-                acc = warp_sum192(acc, nev);
-                const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(acc));
-                if (better(cb, i, wbest, wfirst)) {
-                  wbest = cb;
-                  wfirst = i;
-                  wend = e;
-                  wnev = nev;
-                }
-              }
-              if (lane == 0) {
-                sc.bcost[warp] = wbest;
-                sc.bfirst[warp] = wfirst;
-                sc.bend[warp] = wend;
-                sc.bnev[warp] = wnev;
-              }
-              __syncthreads();
-              if (tid == 0) {
-                for (int w = 0; w < W; ++w) {
-                  if (sc.bend[w] >= 0 && better(sc.bcost[w], sc.bfirst[w], best, bfirst)) {
-                    best = sc.bcost[w];
-                    bfirst = sc.bfirst[w];
-                    bend = sc.bend[w];
-                    bnev = sc.bnev[w];
-                  }
-                }
-              }
-            }
-          }
-          if (tid == 0)
-            write_result(a.out + p, bfirst, bend - 1, v.S_at(bend) - v.S_at(bfirst),
-                         __longlong_as_double((long long)best), bnev, COOP_OK);
-        }
-        }
-      }
-    }
-  pool_done:
+    search_pool<K>(a, sc, Ebuf, stage, p, Rraw);
     // every thread orders its generic-proxy writes into the stage (S / H^ / h write-back)
     // before the async-proxy (TMA) refill that the barrier releases
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -897,13 +932,14 @@ int launch_k(const Args &a0, cudaStream_t st) {
   memset(&m_c, 0, sizeof(m_c));
   memset(&m_s, 0, sizeof(m_s));
   a.use_tma = 0;
+  if (a.pending) a.stages = 1;
   {
     const char *d = getenv("COOP_SEARCH_DBG");
     a.dbg = d ? atoi(d) : 0;
   }
   const bool aligned = ((uintptr_t)a.ss % 16 == 0) && ((uintptr_t)a.cost % 16 == 0) &&
                        ((uintptr_t)a.stale % 16 == 0) && (a.stride % 16 == 0) &&
-                       (a.n_pools < (1ll << 31)) && !coop_force_plain_staging();
+                       (a.n_pools < (1ll << 31)) && !coop_force_plain_staging() && !a.pending;
   if (aligned && make_map(&m_ss, a.ss, a.stride, a.n_pools, a.box_rows) &&
       make_map(&m_c, a.cost, a.stride, a.n_pools, a.box_rows) &&
       make_map(&m_s, a.stale, a.stride, a.n_pools, a.box_rows))
@@ -925,8 +961,8 @@ int launch_k(const Args &a0, cudaStream_t st) {
 
 }  // namespace
 
-int launch_window_search(const coop_tables_soa *t, const uint64_t *requests, coop_window *out,
-                         cudaStream_t st) {
+int launch_window_search_cta(const coop_tables_soa *t, const uint64_t *requests, coop_window *out,
+                             cudaStream_t st, bool pending) {
   Args a;
   memset(&a, 0, sizeof(a));
   a.ss = t->size_state;
@@ -937,12 +973,22 @@ int launch_window_search(const coop_tables_soa *t, const uint64_t *requests, coo
   a.n_pools = t->n_pools;
   a.stride = t->pool_stride;
   a.n = t->n_blocks;
+  a.pending = pending ? 1 : 0;
   if (a.n_pools == 0) return COOP_OK;
   const char *two = getenv("COOP_SEARCH_TWO_CTA");  // profiling hook: 2 CTAs/SM, 1 stage
   if (two && two[0] == '1' && a.n <= 4096) return launch_k<16, 256, 2>(a, st);
   if (a.n <= 2048) return launch_k<8, 256, 2>(a, st);  // 2 CTAs per SM
   if (a.n <= 4096) return launch_k<8, 512, 2>(a, st);  // 2 CTAs per SM, 1 stage each
   return launch_k<16, 512, 1>(a, st);
+}
+
+int launch_window_search(const coop_tables_soa *t, const uint64_t *requests, coop_window *out,
+                         cudaStream_t st) {
+  if (!stream_search_enabled(t->n_blocks)) return launch_window_search_cta(t, requests, out, st, false);
+  // the warp-per-pool stream, then the CTA-per-pool kernel on the pools it left pending
+  int rc = launch_window_search_stream(t, requests, out, st);
+  if (rc != COOP_OK) return rc;
+  return launch_window_search_cta(t, requests, out, st, true);
 }
 
 }  // namespace coop
