@@ -988,6 +988,8 @@ int launch_window_search(const coop_tables_soa *t, const uint64_t *requests, coo
   // the warp-per-pool stream, then the CTA-per-pool kernel on the pools it left pending
   int rc = launch_window_search_stream(t, requests, out, st);
   if (rc != COOP_OK) return rc;
+  const char *v = getenv("COOP_SEARCH_IMPL");  // profiling hook: "stream_only" skips the second pass
+  if (v && v[0] == 's') return COOP_OK;
   return launch_window_search_cta(t, requests, out, st, true);
 }
 

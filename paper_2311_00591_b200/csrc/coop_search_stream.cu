@@ -191,6 +191,7 @@ struct PoolRun {
   int lpcar;       // last PINNED index before the tile (-1)
   int lnzcar;      // last nonzero-h index before the tile (-1)
   int stlast;      // st(e) of the last end of the previous tile if feasible, else -1
+  int stlast_known; // the last end of the previous tile was evaluated (its lane was active)
   int stmax;       // the largest st found so far (monotone lower bound), -1
   double Urun;     // running minimum of the upper bounds
   int ncand;
@@ -199,12 +200,92 @@ struct PoolRun {
   bool bad;        // lane-local
 };
 
-template <bool HOOK>
+// Validation (R7) and h of one item.  The filter only needs h within a relative error
+// delta (folded into gerr): h ~ c * r, r = 1/s from rcp.approx + one Newton step.  R7's
+// range test on RN(c/s) is decided from the exponents of c and s except in a thin band at
+// the bounds (and for c subnormal), where the exact IEEE division decides.
+__device__ __forceinline__ double rcp_nr(double s) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+  const double e = __fma_rn(-s, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
+struct ItemA {
+  double h;    // approximate h (0 for non-EVICTABLE and for h = 0)
+  bool nz;     // h != 0 (exact)
+  bool pin;
+  bool bad;
+  uint64_t size;
+};
+
+__device__ __forceinline__ ItemA decode_item(uint64_t sv, double cr, double sr, bool live) {
+  ItemA it;
+  const uint32_t svh = (uint32_t)(sv >> 32);
+  const uint32_t state = svh >> 30;
+  const bool ev = state == COOP_EVICTABLE;
+  it.size = live ? (sv & kSizeMask) : 0ull;
+  it.pin = live & (state == COOP_PINNED);
+  const uint32_t ch = (uint32_t)((uint64_t)__double_as_longlong(cr) >> 32);
+  const uint32_t cl = (uint32_t)__double_as_longlong(cr);
+  const uint32_t sh_ = (uint32_t)((uint64_t)__double_as_longlong(sr) >> 32);
+  const bool czero = ((ch & 0x7fffffffu) | cl) == 0u;
+  const bool c_ok = (ch < 0x7ff00000u) | ((ch == 0x80000000u) & (cl == 0u));  // finite, >= 0 (or -0)
+  const bool s_ok = (sh_ - 0x3ff00000u) < 0x40000000u;                       // finite, >= 1
+  // exponent difference: RN(c/s) lies in [2^(d-1), 2^(d+1)] for normal c; safely inside
+  // [2^-64, 2^60) when -63 <= d <= 58
+  const int d = (int)(ch >> 20) - (int)(sh_ >> 20);
+  bool h_ok = czero | ((unsigned)(d + 63) <= 121u);
+  bool nz = !czero;
+  const double r = rcp_nr(sr);
+  double h = ev ? cr * r : 0.0;
+  if (ev & c_ok & s_ok & !h_ok) {  // the band at the bounds: the exact division decides
+    const double hq = __ddiv_rn(cr, sr);
+    const uint32_t hh = (uint32_t)((uint64_t)__double_as_longlong(hq) >> 32) & 0x7fffffffu;
+    const uint32_t hl = (uint32_t)__double_as_longlong(hq);
+    const bool hzero = (hh | hl) == 0u;
+    h_ok = hzero | ((hh - 0x3bf00000u) < 0x07c00000u);
+    nz = !hzero;
+    h = hzero ? 0.0 : hq;
+  }
+  const bool size_bad = ((svh & 0x3fff0000u) != 0u) | ((sv & kSizeMask) == 0ull);
+  it.bad = live & (size_bad | (state == 3u) | (ev & !(c_ok & s_ok & h_ok)));
+  it.nz = live & ev & nz;
+  it.h = it.nz ? h : 0.0;
+  return it;
+}
+
+// largest i in [lo, hi] with S[i] <= tgt, given S[lo] <= tgt (bisection on the ring)
+__device__ __forceinline__ int ring_bisect(const WarpSmem &W, int lo, int hi, uint64_t tgt) {
+  if (W.hS[hi & HMASK] <= tgt) return hi;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (W.hS[mid & HMASK] <= tgt) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+// same, galloping up from lo (for the ends after the first: st moves little)
+__device__ __forceinline__ int ring_gallop(const WarpSmem &W, int lo, int hi, uint64_t tgt) {
+  int step = 1;
+  while (true) {
+    const int nx = min(lo + step, hi);
+    if (nx == lo || W.hS[nx & HMASK] > tgt) return ring_bisect(W, lo, nx, tgt);
+    lo = nx;
+    step <<= 1;
+  }
+}
+
+__device__ __forceinline__ int last_bit_idx(uint32_t m, int k0, int none) {  // highest set bit -> item index
+  return m ? k0 + 31 - __clz(m) : none;
+}
+
 __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRun &P, const Raw &r,
                                              int t, int lane) {
   const int n = A.n;
   const int kt = t * STILE;
   const int k0 = kt + 4 * lane;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   if (t == 0) {
     const uint64_t Rraw = A.req[P.p];
     P.R = Rraw < kRClamp ? Rraw : kRClamp;
@@ -214,14 +295,15 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
     P.lpcar = -1;
     P.lnzcar = -1;
     P.stlast = -1;
+    P.stlast_known = 1;
     P.stmax = -1;
-    P.Urun = __longlong_as_double(0x7ff0000000000000ll);
+    P.Urun = kInf;
     P.ncand = 0;
     P.zfound = false;
     P.overflow = false;
     P.zi = P.ze = -1;
   }
-  // ---- decode, validate (R7, same tests as coop_search.cu phase A), h = c/s (R1) -------
+  // ---- decode, validate (R7), h (R1, approximate for the filter), local prefixes ---------
   const uint64_t sv[4] = {r.a0.x, r.a0.y, r.a1.x, r.a1.y};
   const double cv[4] = {r.c0.x, r.c0.y, r.c1.x, r.c1.y};
   const double tv[4] = {r.s0.x, r.s0.y, r.s1.x, r.s1.y};
@@ -230,34 +312,19 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
   uint32_t pm = 0, zm = 0;  // PINNED / nonzero-h masks of the lane's items
   uint64_t sacc = 0;
   double hacc = 0.0;
+  bool bad = false;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const bool live = k0 + q < n;
-    const uint64_t s = sv[q];
-    const uint32_t svh = (uint32_t)(s >> 32);
-    const uint32_t state = svh >> 30;
-    const bool ev = state == COOP_EVICTABLE;
-    const uint64_t size = s & kSizeMask;
-    const double c = ev ? cv[q] : 1.0, st = ev ? tv[q] : 1.0;
-    const double hq = __ddiv_rn(c, st);  // h(t) = c(t)/s(t)
-    const uint32_t ch = (uint32_t)((uint64_t)__double_as_longlong(c) >> 32);
-    const uint32_t cl = (uint32_t)__double_as_longlong(c);
-    const uint32_t sh_ = (uint32_t)((uint64_t)__double_as_longlong(st) >> 32);
-    const uint32_t hh = (uint32_t)((uint64_t)__double_as_longlong(hq) >> 32) & 0x7fffffffu;
-    const uint32_t hl = (uint32_t)__double_as_longlong(hq);
-    const bool hzero = (hh | hl) == 0u;
-    const bool c_ok = (ch < 0x7ff00000u) | ((ch == 0x80000000u) & (cl == 0u));
-    const bool s_ok = (sh_ - 0x3ff00000u) < 0x40000000u;
-    const bool h_ok = hzero | ((hh - 0x3bf00000u) < 0x07c00000u);
-    const bool size_bad = ((svh & 0x3fff0000u) != 0u) | (size == 0ull);
-    if (live) P.bad |= size_bad | (state == 3u) | (ev & !(c_ok & s_ok & h_ok));
-    pm |= (uint32_t)(live & (state == COOP_PINNED)) << q;
-    zm |= (uint32_t)(live & ev & !hzero) << q;
-    sacc += live ? size : 0ull;
-    hacc = __dadd_rn(hacc, ev ? hq : 0.0);
+    const ItemA it = decode_item(sv[q], cv[q], tv[q], k0 + q < n);
+    bad |= it.bad;
+    pm |= (uint32_t)it.pin << q;
+    zm |= (uint32_t)it.nz << q;
+    sacc += it.size;
+    hacc = __dadd_rn(hacc, it.h);
     szi[q] = sacc;
     hi_[q] = hacc;
   }
+  P.bad |= bad;
   if (P.zfound) return;  // the answer is known; the rest of the pool is only validated
   // ---- warp scans: exclusive span / cost prefixes of the lane's first item --------------
   uint64_t s_in = sacc;
@@ -271,14 +338,9 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
       h_in = __dadd_rn(ho, h_in);
     }
   }
-  uint64_t s_ex = __shfl_up_sync(0xffffffffu, s_in, 1);
-  double h_ex = __shfl_up_sync(0xffffffffu, h_in, 1);
-  if (lane == 0) {
-    s_ex = 0;
-    h_ex = 0.0;
-  }
-  const uint64_t Sb = P.Scar + s_ex;
-  const double Hb = __dadd_rn(P.Hcar, h_ex);
+  const uint64_t Sb = P.Scar + (s_in - sacc);  // exact
+  const double hexc = __shfl_up_sync(0xffffffffu, h_in, 1);
+  const double Hb = __dadd_rn(P.Hcar, lane ? hexc : 0.0);
   uint64_t Sx[4], Sn[4];
   double Hx[4], Hn[4];
 #pragma unroll
@@ -288,13 +350,13 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
     Hx[q] = q ? __dadd_rn(Hb, hi_[q - 1]) : Hb;
     Hn[q] = __dadd_rn(Hb, hi_[q]);
   }
-  // ---- last PINNED / last nonzero index at or before each item --------------------------
+  // ---- last PINNED / last nonzero index before the lane's items ---------------------------
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t bp = __ballot_sync(0xffffffffu, pm != 0), bz = __ballot_sync(0xffffffffu, zm != 0);
-  const int mylp = pm ? k0 + 31 - __clz(pm) : -1, mylz = zm ? k0 + 31 - __clz(zm) : -1;
+  const int mylp = last_bit_idx(pm, k0, -1), mylz = last_bit_idx(zm, k0, -1);
   const int srcp = (bp & lt) ? 31 - __clz(bp & lt) : 0, srcz = (bz & lt) ? 31 - __clz(bz & lt) : 0;
   const int lpo = __shfl_sync(0xffffffffu, mylp, srcp), lzo = __shfl_sync(0xffffffffu, mylz, srcz);
-  const int lp_before = (bp & lt) ? lpo : P.lpcar;   // last PINNED before the lane's items
+  const int lp_before = (bp & lt) ? lpo : P.lpcar;
   const int lz_before = (bz & lt) ? lzo : P.lnzcar;
   // ---- history ring: this tile's S[k], H^[k] -----------------------------------------------
   {
@@ -305,82 +367,143 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
     *reinterpret_cast<double2 *>(&W.hH[slot + 2]) = make_double2(Hx[2], Hx[3]);
   }
   __syncwarp();
-  // ---- every end of the tile: latest start, window cost bounds -----------------------------
   const int oldest = max(0, kt + STILE - HCAP);  // first item still in the ring
-  int st_of[4];       // st(e) if the window (st(e), e) is feasible, else -1
-  bool fz[4];         // that window is a zero window
-  int zst[4];         // its lowest zero start (fz)
-  double Lb[4], Ub[4];
-  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-  int lbm = P.stmax;  // monotone lower bound of st
-  bool ovf = false;
+  // ---- lane pruning: the latest start of the lane's last end bounds all its windows ------
+  // For ends e0 <= e <= e3 of the lane, st(e) <= st(e3), so every window cost is >=
+  // H[e0 + 1] - H[st(e3)]; the window (st(e3), e3) itself, when PINNED-free, bounds the
+  // minimum from above.  Lanes whose bound cannot reach the running minimum skip their ends.
+  int e3q = -1;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int e = k0 + q;
-    st_of[q] = -1;
-    fz[q] = false;
-    zst[q] = -1;
-    Lb[q] = kInf;
-    Ub[q] = kInf;
-    const int lpe = ((pm >> q) & 1u) ? e : ((pm & ((1u << q) - 1u)) ? k0 + 31 - __clz(pm & ((1u << q) - 1u)) : lp_before);
-    const int lze = (zm & ((2u << q) - 1u)) ? k0 + 31 - __clz(zm & ((2u << q) - 1u)) : lz_before;
-    if (e >= n || lpe == e || Sn[q] < P.R) continue;
-    const uint64_t tgt = Sn[q] - P.R;  // starts i with S[i] <= tgt cover R
-    const int lbp = lpe + 1;
-    int lo = max(max(lbp, oldest), max(lbm, 0));
-    if (W.hS[lo & HMASK] > tgt) {  // no start >= lo
-      if (lo == oldest && oldest > lbp && oldest > lbm) ovf = true;  // window longer than the ring
-      continue;
-    }
-    // largest i in [lo, e] with S[i] <= tgt: gallop from lo, then bisect
-    int hi = lo, step = 1;
-    while (true) {
-      const int nx = min(hi + step, e);
-      if (nx == hi || W.hS[nx & HMASK] > tgt) break;
-      hi = nx;
-      step <<= 1;
-    }
-    int top = min(hi + step, e);  // S[top] > tgt unless top == e
-    if (W.hS[top & HMASK] <= tgt) {
-      hi = top;
-    } else {
-      while (top - hi > 1) {
-        const int mid = (hi + top) >> 1;
-        if (W.hS[mid & HMASK] <= tgt) hi = mid;
-        else top = mid;
+  for (int q = 0; q < 4; ++q)
+    if (k0 + q < n && !((pm >> q) & 1u) && Sn[q] >= P.R) e3q = q;
+  int st3 = -1;       // st_raw of the lane's last valid end (-1: none >= the lower bound)
+  bool ovf = false;
+  double Ul = kInf, Ll = kInf;
+  const int lbm0 = max(P.stmax, 0);
+  if (e3q >= 0) {
+    int e3 = k0, q3 = 0;
+#pragma unroll
+    for (int q = 1; q < 4; ++q)
+      if (q == e3q) {
+        e3 = k0 + q;
+        q3 = q;
       }
-    }
-    const int b = hi;
-    st_of[q] = b;
-    lbm = b;
-    if (lze < b) {
-      fz[q] = true;  // items (lze, e] are all zero: a zero-cost window
+    uint64_t sn3 = Sn[0];
+    double hn3 = Hn[0];
+#pragma unroll
+    for (int q = 1; q < 4; ++q)
+      if (q == q3) {
+        sn3 = Sn[q];
+        hn3 = Hn[q];
+      }
+    const uint64_t tgt = sn3 - P.R;
+    const int lo = max(oldest, lbm0);
+    if (W.hS[lo & HMASK] <= tgt) {
+      st3 = ring_bisect(W, lo, e3, tgt);
+      const int lp3 = (pm & ((2u << q3) - 1u)) ? last_bit_idx(pm & ((2u << q3) - 1u), k0, -1) : lp_before;
+      const double Hs = W.hH[st3 & HMASK];
+      const double err = A.gerr * (hn3 + Hs);
+      if (st3 > lp3) Ul = (hn3 - Hs) + err;  // a real (PINNED-free) window
+      // lower bound for every end of the lane (its first valid end's prefix)
+      int qf = 3;
+#pragma unroll
+      for (int q = 3; q >= 0; --q)
+        if (k0 + q < n && !((pm >> q) & 1u) && Sn[q] >= P.R) qf = q;
+      double hnf = Hn[0];
+#pragma unroll
+      for (int q = 1; q < 4; ++q)
+        if (q == qf) hnf = Hn[q];
+      Ll = (hnf - Hs) - A.gerr * (hnf + Hs);
     } else {
-      const double Hbv = W.hH[b & HMASK];
-      const double C = Hn[q] - Hbv;
-      const double err = A.gerr * (Hn[q] + Hbv);
-      Lb[q] = C - err;
-      Ub[q] = C + err;
+      Ll = -kInf;  // no start >= lo covers R for the last end: decided per end below
     }
   }
-  // a(e) = max(st(e-1), lp(e)): st(e-1) from the previous end (lane q-1, lane - 1, or tile)
+  double um = Ul;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) um = fmin(um, __shfl_xor_sync(0xffffffffu, um, d));
+  P.Urun = fmin(P.Urun, um);
+  const double thr = P.Urun * kMargin;
+  const bool active = (e3q >= 0) && (Ll <= thr);
+  // ---- the active lanes: every end, its latest start, window cost bounds --------------------
+  int st_of[4] = {-1, -1, -1, -1};  // st(e) if the window (st(e), e) is PINNED-free, else -1
+  bool fz[4] = {false, false, false, false};
+  double Lb[4] = {kInf, kInf, kInf, kInf}, Ub[4] = {kInf, kInf, kInf, kInf};
+  int lbm = P.stmax;
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = k0 + q;
+      const int lpe = ((pm >> q) & 1u) ? e : last_bit_idx(pm & ((1u << q) - 1u), k0, lp_before);
+      const int lze = last_bit_idx(zm & ((2u << q) - 1u), k0, lz_before);
+      if (e >= n || lpe == e || Sn[q] < P.R) continue;
+      const uint64_t tgt = Sn[q] - P.R;
+      const int lbp = lpe + 1;
+      const int lo = max(max(lbp, oldest), max(lbm, 0));
+      if (W.hS[lo & HMASK] > tgt) {
+        if (lo == oldest && oldest > lbp && oldest > lbm) ovf = true;
+        continue;
+      }
+      const int b = (q == 0 || lbm < 0) ? ring_bisect(W, lo, e, tgt) : ring_gallop(W, lo, e, tgt);
+      st_of[q] = b;
+      lbm = b;
+      if (lze < b) {
+        fz[q] = true;  // items (lze, e] are all zero: a zero-cost window
+      } else {
+        const double Hbv = W.hH[b & HMASK];
+        const double C = Hn[q] - Hbv;
+        const double err = A.gerr * (Hn[q] + Hbv);
+        Lb[q] = C - err;
+        Ub[q] = C + err;
+      }
+    }
+  } else if (st3 >= 0) {
+    lbm = st3;  // st is monotone: the lane's last end's start bounds later ends
+  }
+  // a(e) = max(st(e-1), lp(e)): starts of e lie in (a(e), st(e)]; the previous end's st
+  // comes from lane q-1, the previous lane, or the previous tile (only needed when the
+  // previous end is in an active lane; an inactive lane's ends cannot win -- their windows'
+  // exact costs exceed the minimum -- so a(e) only matters for ends of active lanes, whose
+  // previous end is either in the same lane or in the previous lane)
+  const bool prev_active = __shfl_up_sync(0xffffffffu, (int)active, 1);
   const int st_prev_lane = __shfl_up_sync(0xffffffffu, st_of[3], 1);
-  int a_of[4];
+  int a_of[4], zst[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int e = k0 + q;
-    const int lpe = ((pm >> q) & 1u) ? e : ((pm & ((1u << q) - 1u)) ? k0 + 31 - __clz(pm & ((1u << q) - 1u)) : lp_before);
-    const int sp = q ? st_of[q - 1] : (lane ? st_prev_lane : P.stlast);
+    const int lpe = ((pm >> q) & 1u) ? e : last_bit_idx(pm & ((1u << q) - 1u), k0, lp_before);
+    int sp;
+    bool known = true;
+    if (q) sp = st_of[q - 1];
+    else if (lane) {
+      sp = st_prev_lane;
+      known = prev_active;
+    } else {
+      sp = P.stlast;
+      known = P.stlast_known;
+    }
     a_of[q] = max(sp, lpe);
+    zst[q] = -1;
+    if (st_of[q] >= 0 && !known) {
+      // the previous end's start is unknown (inactive previous lane): recompute it here
+      const int ep = e - 1;
+      int spv = -1;
+      if (ep >= 0) {
+        uint64_t snp = Sx[q];  // S[e] = S[(e-1) + 1]
+        if (snp >= P.R) {
+          const uint64_t tgt = snp - P.R;
+          const int lo = max(oldest, lbm0);
+          if (W.hS[lo & HMASK] <= tgt) spv = ring_bisect(W, lo, ep, tgt);
+          else if (lo == oldest && oldest > lpe + 1) ovf = true;  // st(e-1) beyond the ring
+        }
+      }
+      a_of[q] = max(spv, lpe);
+    }
     if (st_of[q] >= 0 && a_of[q] >= st_of[q]) {  // (a, st(e)] empty: no canonical window ends at e
       fz[q] = false;
       Lb[q] = kInf;
       Ub[q] = kInf;
     }
-    if (fz[q]) {
-      const int lze = (zm & ((2u << q) - 1u)) ? k0 + 31 - __clz(zm & ((2u << q) - 1u)) : lz_before;
-      zst[q] = max(a_of[q], lze) + 1;  // <= st(e)
-    }
+    if (fz[q]) zst[q] = max(a_of[q], last_bit_idx(zm & ((2u << q) - 1u), k0, lz_before)) + 1;
   }
   // ---- carries to the next tile ---------------------------------------------------------
   P.Scar = __shfl_sync(0xffffffffu, Sn[3], 31);
@@ -391,7 +514,8 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
     P.lnzcar = __shfl_sync(0xffffffffu, lz_last, 31);
   }
   P.stlast = __shfl_sync(0xffffffffu, st_of[3], 31);
-  P.stmax = __reduce_max_sync(0xffffffffu, (unsigned)(lbm + 1)) - 1;
+  P.stlast_known = __shfl_sync(0xffffffffu, (int)active, 31);
+  P.stmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)(lbm + 1)) - 1;
   if (__any_sync(0xffffffffu, ovf)) P.overflow = true;
   // ---- zero windows: the earliest end with one gives the lowest start (exact, R4) -------
   {
@@ -414,15 +538,15 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
     }
   }
   // ---- candidates: ends whose lower bound can still reach the minimum -------------------
-  double um = fmin(fmin(Ub[0], Ub[1]), fmin(Ub[2], Ub[3]));
+  um = fmin(fmin(Ub[0], Ub[1]), fmin(Ub[2], Ub[3]));
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) um = fmin(um, __shfl_xor_sync(0xffffffffu, um, d));
   P.Urun = fmin(P.Urun, um);
-  const double thr = P.Urun * kMargin;
+  const double thr2 = P.Urun * kMargin;
   uint32_t want = 0;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) want |= (uint32_t)((Lb[q] <= thr) & (Ub[q] < kInf)) << q;
-  int nnew = __reduce_add_sync(0xffffffffu, (unsigned)__popc(want));
+  for (int q = 0; q < 4; ++q) want |= (uint32_t)((Lb[q] <= thr2) & (Ub[q] < kInf)) << q;
+  const int nnew = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(want));
   if (nnew == 0) return;
   if (P.ncand + nnew > CCAP) {  // prune the list against the current bound
     int keep = 0;
@@ -436,7 +560,7 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
         b_ = W.cb[c];
         a_ = W.ca[c];
         l_ = W.cl[c];
-        k = l_ <= thr;
+        k = l_ <= thr2;
       }
       const uint32_t bal = __ballot_sync(0xffffffffu, k);
       __syncwarp();
@@ -480,7 +604,7 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
   P.ncand += nnew;
 }
 
-__device__ __forceinline__ void finish_pool(const SArgs &A, WarpSmem &W, PoolRun &P, int lane) {
+__device__ __noinline__ void finish_pool(const SArgs &A, WarpSmem &W, PoolRun &P, int lane) {
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   coop_window *o = A.out + P.p;
   const bool bad = __any_sync(0xffffffffu, P.bad);
@@ -575,7 +699,6 @@ __device__ __forceinline__ void finish_pool(const SArgs &A, WarpSmem &W, PoolRun
   if (lane == 0) put_window(o, start, be, bspan, __longlong_as_double((long long)best), bnev, COOP_OK);
 }
 
-template <bool HOOK>
 __global__ void __launch_bounds__(SWARPS * 32, 2) search_stream_kernel(const SArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -593,30 +716,25 @@ __global__ void __launch_bounds__(SWARPS * 32, 2) search_stream_kernel(const SAr
   };
   norm(p1, t1);
   norm(p2, t2);
-  Raw ra, rb, rc;
-  if (p0 < A.n_pools) load_tile(A, ra, p0, t0, lane);
-  if (p1 < A.n_pools) load_tile(A, rb, p1, t1, lane);
+  Raw cur, nx1, nx2;
+  if (p0 < A.n_pools) load_tile(A, cur, p0, t0, lane);
+  if (p1 < A.n_pools) load_tile(A, nx1, p1, t1, lane);
   PoolRun P;
   P.p = p0;
   P.bad = false;
-  auto step = [&](Raw &cur, Raw &ahead2) -> bool {
-    if (p0 >= A.n_pools) return false;
-    if (p2 < A.n_pools) load_tile(A, ahead2, p2, t2, lane);
+  while (p0 < A.n_pools) {
+    if (p2 < A.n_pools) load_tile(A, nx2, p2, t2, lane);
     P.p = p0;
-    process_tile<HOOK>(A, W, P, cur, t0, lane);
+    process_tile(A, W, P, cur, t0, lane);
     if (t0 == nt - 1) finish_pool(A, W, P, lane);
+    cur = nx1;  // register rotation (one copy of the tile body keeps the code in the i-cache)
+    nx1 = nx2;
     p0 = p1;
     t0 = t1;
     p1 = p2;
     t1 = t2;
     ++t2;
     norm(p2, t2);
-    return true;
-  };
-  while (true) {
-    if (!step(ra, rc)) break;
-    if (!step(rb, ra)) break;
-    if (!step(rc, rb)) break;
   }
 }
 
@@ -642,14 +760,15 @@ int launch_window_search_stream(const coop_tables_soa *t, const uint64_t *reques
   A.ntiles = (A.n + STILE - 1) / STILE;
   A.vec = ((uintptr_t)A.ss % 16 == 0) && ((uintptr_t)A.cost % 16 == 0) && ((uintptr_t)A.stale % 16 == 0) &&
           (A.stride % 2 == 0);
-  // summation depth of any H^ entry <= 4 (lane) + 5 (warp scan) + 2 + ntiles (carry chain)
+  // summation depth of any H^ entry <= 4 (lane) + 5 (warp scan) + 2 + ntiles (carry chain);
+  // every h carries a relative error <= 2^-40 (rcp.approx + one Newton step)
   const int depth = 4 + 5 + 2 + A.ntiles + 2;
-  A.gerr = 2.0 * (double)(depth + 2) * 0x1p-53 + 0x1p-50;
+  A.gerr = 2.0 * (double)(depth + 2) * 0x1p-53 + 2.0 * 0x1p-39 + 0x1p-50;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = sizeof(WarpSmem) * SWARPS;
-  auto kern = search_stream_kernel<false>;
+  auto kern = search_stream_kernel;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return COOP_ERR_CUDA;
   int per_sm = 0;
