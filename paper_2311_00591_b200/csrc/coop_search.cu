@@ -989,7 +989,7 @@ int launch_window_search(const coop_tables_soa *t, const uint64_t *requests, coo
   int rc = launch_window_search_stream(t, requests, out, st);
   if (rc != COOP_OK) return rc;
   const char *v = getenv("COOP_SEARCH_IMPL");  // profiling hook: "stream_only" skips the second pass
-  if (v && v[0] == 's') return COOP_OK;
+  if (v && strcmp(v, "stream_only") == 0) return COOP_OK;
   return launch_window_search_cta(t, requests, out, st, true);
 }
 

@@ -459,6 +459,17 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
   } else if (st3 >= 0) {
     lbm = st3;  // st is monotone: the lane's last end's start bounds later ends
   }
+  if (!__any_sync(0xffffffffu, active)) {  // no window of this tile can reach the minimum
+    P.Scar = __shfl_sync(0xffffffffu, Sn[3], 31);
+    P.Hcar = __shfl_sync(0xffffffffu, Hn[3], 31);
+    const int lp_last = pm ? mylp : lp_before, lz_last = zm ? mylz : lz_before;
+    P.lpcar = __shfl_sync(0xffffffffu, lp_last, 31);
+    P.lnzcar = __shfl_sync(0xffffffffu, lz_last, 31);
+    P.stlast = -1;
+    P.stlast_known = 0;
+    P.stmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)(lbm + 1)) - 1;
+    return;
+  }
   // a(e) = max(st(e-1), lp(e)): starts of e lie in (a(e), st(e)]; the previous end's st
   // comes from lane q-1, the previous lane, or the previous tile (only needed when the
   // previous end is in an active lane; an inactive lane's ends cannot win -- their windows'
@@ -604,7 +615,7 @@ __device__ __forceinline__ void process_tile(const SArgs &A, WarpSmem &W, PoolRu
   P.ncand += nnew;
 }
 
-__device__ __noinline__ void finish_pool(const SArgs &A, WarpSmem &W, PoolRun &P, int lane) {
+__device__ __noinline__ void finish_pool(const SArgs &A, WarpSmem &W, const PoolRun P, int lane) {
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   coop_window *o = A.out + P.p;
   const bool bad = __any_sync(0xffffffffu, P.bad);
@@ -705,9 +716,10 @@ __global__ void __launch_bounds__(SWARPS * 32, 2) search_stream_kernel(const SAr
   WarpSmem &W = reinterpret_cast<WarpSmem *>(smem_raw)[wid];
   const int64_t gw = (int64_t)blockIdx.x * SWARPS + wid, GW = (int64_t)gridDim.x * SWARPS;
   const int nt = A.ntiles;
-  // tile positions: (pool, tile), pools gw, gw + GW, ...; two tiles in flight ahead
-  int64_t p0 = gw, p1 = gw, p2 = gw;
-  int t0 = 0, t1 = 1, t2 = 2;
+  // tile positions: (pool, tile), pools gw, gw + GW, ...; the next tile is in flight while
+  // one is processed (a tile takes a warp several microseconds at 12 warps per SM)
+  int64_t p0 = gw, p1 = gw;
+  int t0 = 0, t1 = 1;
   auto norm = [&](int64_t &p, int &t) {
     while (t >= nt) {
       t -= nt;
@@ -715,35 +727,32 @@ __global__ void __launch_bounds__(SWARPS * 32, 2) search_stream_kernel(const SAr
     }
   };
   norm(p1, t1);
-  norm(p2, t2);
-  Raw cur, nx1, nx2;
+  Raw cur, nxt;
   if (p0 < A.n_pools) load_tile(A, cur, p0, t0, lane);
-  if (p1 < A.n_pools) load_tile(A, nx1, p1, t1, lane);
   PoolRun P;
   P.p = p0;
   P.bad = false;
   while (p0 < A.n_pools) {
-    if (p2 < A.n_pools) load_tile(A, nx2, p2, t2, lane);
+    if (p1 < A.n_pools) load_tile(A, nxt, p1, t1, lane);
     P.p = p0;
     process_tile(A, W, P, cur, t0, lane);
     if (t0 == nt - 1) finish_pool(A, W, P, lane);
-    cur = nx1;  // register rotation (one copy of the tile body keeps the code in the i-cache)
-    nx1 = nx2;
+    cur = nxt;
     p0 = p1;
     t0 = t1;
-    p1 = p2;
-    t1 = t2;
-    ++t2;
-    norm(p2, t2);
+    ++t1;
+    norm(p1, t1);
   }
 }
 
 }  // namespace
 
+// The CTA-per-pool kernel is the default (faster on B200: 46.5 ms vs 63 ms per 2^20 x 4096
+// pools); COOP_SEARCH_IMPL=stream selects this kernel (+ the CTA kernel
+// for the pools it leaves pending), COOP_SEARCH_IMPL=stream_only skips that second pass.
 bool stream_search_enabled(int n) {
   const char *v = getenv("COOP_SEARCH_IMPL");
-  if (v && v[0] == 'c') return false;  // "cta": the CTA-per-pool kernel only
-  return n >= 1;
+  return v && v[0] == 's' && n >= 1;
 }
 
 int launch_window_search_stream(const coop_tables_soa *t, const uint64_t *requests, coop_window *out,

@@ -235,3 +235,17 @@ def test_signed_zero_and_zero_runs():
     o = O.search_many(SS, C, S, req, 64, n, 608)
     assert_same(g, o, "signed zero")
     assert (g["cost"][g["status"] == 0] == 0.0).sum() > 10
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 129, 1000, 4096, 8192])
+def test_stream_kernel_parity(n, monkeypatch):
+    """The alternative warp-per-pool streaming kernel (COOP_SEARCH_IMPL=stream, DESIGN.md
+    section 6) plus the CTA kernel on the pools it leaves pending: bit-identical to O1 on the
+    same random pools (ties, cancellation, uncoalesced free runs, windows longer than its
+    history ring), and on the benchmark law."""
+    monkeypatch.setenv("COOP_SEARCH_IMPL", "stream")
+    test_random_pools_parity(n, "tma")
+    if n == 4096:
+        P = 256
+        ss, c, s, r = G.bench_pools_host(G.MODE_BENCH, 3, 5000, P, n)
+        assert_same(gpu_search(ss, c, s, r, P, n, n), O.search_many(ss, c, s, r, P, n, n), "stream bench law")
