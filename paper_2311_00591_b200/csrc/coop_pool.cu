@@ -82,13 +82,12 @@ __device__ __forceinline__ void pool_load(const PArgs &pa, Shared &sh) {
   const int nflag = min(nt + 1, pa.k.tr.T);
   uint8_t *tflags = pa.k.ws + pa.k.lay.tflags;  // CTA slot 0 (Cell's layout)
   for (int b = tid; b < nb0; b += kThreads) {
-    sh.addr[0][b] = P.addr[b];
-    sh.size[0][b] = P.size[b];
-    sh.owner[0][b] = P.owner[b];
+    sh.addr[b] = P.addr[b];
+    sh.size[b] = P.size[b];
+    sh.owner[b] = P.owner[b];
   }
   for (int x = tid; x < nflag; x += kThreads) sh.tfl[x] = tflags[x];
   if (tid == 0) {
-    sh.cur = 0;
     sh.nb = nb0;
     sh.bytes_free = P.bytes_free;
     sh.clock = P.clock;
@@ -102,11 +101,11 @@ __device__ __forceinline__ void pool_store(const PArgs &pa, Shared &sh) {
   const int tid = threadIdx.x;
   const int nflag = min(P.n_tensors + 1, pa.k.tr.T);
   uint8_t *tflags = pa.k.ws + pa.k.lay.tflags;
-  const int nb1 = sh.nb, cur = sh.cur;
+  const int nb1 = sh.nb;
   for (int b = tid; b < nb1; b += kThreads) {
-    P.addr[b] = sh.addr[cur][b];
-    P.size[b] = sh.size[cur][b];
-    P.owner[b] = sh.owner[cur][b];
+    P.addr[b] = sh.addr[b];
+    P.size[b] = sh.size[b];
+    P.owner[b] = sh.owner[b];
   }
   for (int x = tid; x < nflag; x += kThreads) tflags[x] = sh.tfl[x];
   if (tid == 0) {
@@ -424,9 +423,14 @@ void pool_release(coop_pool_s *p) {
   delete p;
 }
 
+// dynamic shared memory of the pool kernels: Shared plus one flag byte per tensor id
+size_t pool_smem(const coop_pool_s *p) { return sizeof(Shared) + (size_t)(p->cfg.max_tensors + 15) / 16 * 16; }
+
 PArgs base_args(coop_pool_s *p) {
   PArgs a{};
   a.k.tr = p->td;
+  a.k.tfl_bytes = (p->cfg.max_tensors + 15) / 16 * 16;
+  a.k.walkers = 0;  // the online pool's graph grows: generic closure walk
   a.k.flags = p->cfg.flags;
   a.k.thr = p->cfg.class_threshold;
   a.k.max_depth = 512;
@@ -448,7 +452,7 @@ int service_ensure(coop_pool_s *p) {
     if (q == cudaErrorNotReady) return COOP_OK;
     if (q != cudaSuccess) return COOP_ERR_CUDA;
   }
-  pool_service_kernel<<<1, kThreads, sizeof(Shared), p->stream>>>(base_args(p), p->mb_dev, p->idle_ns);
+  pool_service_kernel<<<1, kThreads, pool_smem(p), p->stream>>>(base_args(p), p->mb_dev, p->idle_ns);
   if (cudaGetLastError() != cudaSuccess) return COOP_ERR_CUDA;
   p->launched = true;
   return COOP_OK;
@@ -519,7 +523,7 @@ int launch_call(coop_pool_s *p, int32_t kind, int32_t t, uint64_t size, int64_t 
   a.adv = adv;
   a.cost = cost;
   a.op_flags = op_flags;
-  pool_kernel<<<1, kThreads, sizeof(Shared), p->stream>>>(a);
+  pool_kernel<<<1, kThreads, pool_smem(p), p->stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
   if (prev != p->device) cudaSetDevice(prev);
@@ -591,10 +595,10 @@ extern "C" int coop_pool_init(const coop_pool_config *cfg, coop_pool_t *out) {
     if (cudaHostGetDevicePointer((void **)&p->mb_dev, p->mb_host, 0) != cudaSuccess) rc = COOP_ERR_CUDA;
   }
   if (rc == COOP_OK && cudaFuncSetAttribute(pool_service_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)sizeof(Shared)) != cudaSuccess)
+                                            (int)pool_smem(p)) != cudaSuccess)
     rc = COOP_ERR_CUDA;
   if (rc == COOP_OK && cudaFuncSetAttribute(pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)sizeof(Shared)) != cudaSuccess)
+                                            (int)pool_smem(p)) != cudaSuccess)
     rc = COOP_ERR_CUDA;
   if (rc != COOP_OK) {
     pool_release(p);

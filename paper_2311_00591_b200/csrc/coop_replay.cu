@@ -32,6 +32,12 @@ namespace {
 __global__ void __launch_bounds__(kThreads, 1) replay_kernel(const KArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   Shared &sh = *reinterpret_cast<Shared *>(smem);
+  if (a.g_smem) {  // the compact graph of the fast closure walk, once per CTA
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.tr.cg_cost);
+    uint4 *dst = reinterpret_cast<uint4 *>(sh.tfl + a.tfl_bytes);
+    for (int i = threadIdx.x; i < a.g_bytes / 16; i += kThreads) dst[i] = __ldg(src + i);
+    __syncthreads();
+  }
   for (int cell = blockIdx.x; cell < a.n_cells; cell += gridDim.x) {
     CellT<true> c(a, sh, cell);
     c.run(a.budgets[cell]);
@@ -56,6 +62,8 @@ struct coop_trace_s {
   std::vector<int32_t> cons_ptr, cons_idx, lock_ptr, lock_idx, die_ptr, die_idx;
   std::vector<int32_t> cons_head, cons_next, cons_out;  // the CSR as linked lists (device layout)
   std::vector<int32_t> rec;  // per tensor {cost lo, cost hi, in_beg, in_end} (device layout)
+  std::vector<unsigned char> cg;  // the compact graph of the fast closure walk (cg_offsets), or empty
+  int32_t cg_nnz = 0;
   void *dev = nullptr;
   TraceDev td{};
   unsigned char *ws = nullptr;
@@ -193,6 +201,40 @@ int validate_and_prepare(coop_trace_s &t) {
       t.lock_ptr[k + 1] = (int32_t)t.lock_idx.size();
     }
   }
+  // compact graph for the replay's fast closure walk (16-bit ids / offsets, 32-bit costs)
+  {
+    const int nnz = (int)t.in_idx.size();
+    bool ok = T < 65535 && nnz < 65535;
+    for (int k = 0; k < M && ok; ++k) ok = t.cost[k] < (1ll << 31);
+    t.cg.clear();
+    t.cg_nnz = 0;
+    if (ok) {
+      size_t off[6];
+      cg_offsets(T, nnz, off);
+      t.cg.assign(off[5], 0);
+      int32_t *cost = reinterpret_cast<int32_t *>(t.cg.data() + off[0]);
+      uint16_t *iptr = reinterpret_cast<uint16_t *>(t.cg.data() + off[1]);
+      uint16_t *cptr = reinterpret_cast<uint16_t *>(t.cg.data() + off[2]);
+      uint16_t *iidx = reinterpret_cast<uint16_t *>(t.cg.data() + off[3]);
+      uint16_t *cout = reinterpret_cast<uint16_t *>(t.cg.data() + off[4]);
+      int ni = 0;
+      for (int x = 0; x < T; ++x) {
+        const int p = t.producer[x];
+        cost[x] = p >= 0 ? (int32_t)t.cost[p] : -1;
+        iptr[x] = (uint16_t)ni;
+        if (p >= 0)
+          for (int j = t.in_ptr[p]; j < t.in_ptr[p + 1]; ++j) iidx[ni++] = (uint16_t)t.in_idx[j];
+      }
+      iptr[T] = (uint16_t)ni;
+      int nc = 0;
+      for (int x = 0; x < T; ++x) {
+        cptr[x] = (uint16_t)nc;
+        for (int j = t.cons_ptr[x]; j < t.cons_ptr[x + 1]; ++j) cout[nc++] = (uint16_t)t.out[t.cons_idx[j]];
+      }
+      cptr[T] = (uint16_t)nc;
+      t.cg_nnz = nnz;
+    }
+  }
   return COOP_OK;
 }
 
@@ -220,7 +262,7 @@ static int upload_trace(coop_trace_s *t) {
                o_phase = put(blob, t->phase), o_inp = put(blob, t->in_ptr), o_ini = put(blob, t->in_idx),
                o_cp = put(blob, t->cons_head), o_cn = put(blob, t->cons_next), o_ci = put(blob, t->cons_out), o_rec = put(blob, t->rec), o_lp = put(blob, t->lock_ptr),
                o_li = put(blob, t->lock_idx), o_dp = put(blob, t->die_ptr), o_di = put(blob, t->die_idx),
-               o_par = put(blob, t->params);
+               o_par = put(blob, t->params), o_cg = put(blob, t->cg);
   cudaGetDevice(&t->device);
   if (cudaMalloc(&t->dev, blob.size()) != cudaSuccess) {
     t->dev = nullptr;
@@ -255,6 +297,9 @@ static int upload_trace(coop_trace_s *t) {
   td.die_ptr = (const int32_t *)(b + o_dp);
   td.die_idx = (const int32_t *)(b + o_di);
   td.params = (const int32_t *)(b + o_par);
+  td.cg_nnz = t->cg_nnz;
+  td.cg_cost = t->cg.empty() ? nullptr : (const int32_t *)(b + o_cg);
+  td.cg_iptr = td.cg_cptr = td.cg_iidx = td.cg_cout = nullptr;  // carved from cg_cost by cg_offsets
   return COOP_OK;
 }
 
@@ -367,7 +412,27 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   if (cudaStreamWaitEvent(st, t->done, 0) != cudaSuccess) return COOP_ERR_CUDA;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
-  const size_t smem = sizeof(Shared);
+  // dynamic shared memory: Shared, the tensor flags, then (fast closure walk) the compact
+  // graph if it fits and as many walker bitmaps as fit (at least 32, at most kThreads)
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, t->device);
+  const int tfl_bytes = (t->T + 15) / 16 * 16;
+  const int vis_words = (t->T + 127) / 128 * 4;
+  const size_t base = sizeof(Shared) + (size_t)tfl_bytes;
+  int g_smem = 0, walkers = 0;
+  const int g_bytes = (int)t->cg.size();
+  const char *wenv = getenv("COOP_REPLAY_WALK");  // profiling hook: "generic" disables the fast walk
+  if (!t->cg.empty() && !(wenv && wenv[0] == 'g')) {
+    const size_t per = (size_t)vis_words * 4;
+    if (base + (size_t)g_bytes + 32 * per <= (size_t)max_smem) {
+      g_smem = 1;
+      walkers = (int)std::min<size_t>(kThreads, ((size_t)max_smem - base - g_bytes) / per);
+    } else if (base + 32 * per <= (size_t)max_smem) {
+      walkers = (int)std::min<size_t>(kThreads, ((size_t)max_smem - base) / per);
+    }
+    walkers = walkers / 32 * 32;  // whole warps
+  }
+  const size_t smem = base + (g_smem ? (size_t)g_bytes : 0) + (size_t)walkers * vis_words * 4;
   if (cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return COOP_ERR_CUDA;
   int per_sm = 1;
@@ -402,6 +467,11 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   a.log_cap = log ? log_cap : 0;
   a.ws = t->ws;
   a.lay = t->lay;
+  a.tfl_bytes = tfl_bytes;
+  a.g_smem = g_smem;
+  a.g_bytes = g_bytes;
+  a.walkers = walkers;
+  a.vis_words = vis_words;
   // each CTA owns a workspace slot: cells are assigned cyclically, CTA b takes cells
   // b, b + grid, ... and always uses slot b
   replay_kernel<<<(unsigned)cells, kThreads, smem, st>>>(a);

@@ -28,11 +28,7 @@ inline bool bad_flags(uint32_t f) {
 }
 constexpr int kMaxT = 16384;     // tensors per trace whose flags live in shared memory
 
-enum : uint8_t { TF_RES = 1, TF_BORN = 2, TF_DEAD = 4, TF_LOCK = 8,
-                 // replay only: the cached projected-cost closure of the tensor may be stale
-                 // (TF_DIRTY); the tensor's residency / liveness changed since the last
-                 // pressure event and it is on the changed list (TF_CHG)
-                 TF_DIRTY = 16, TF_CHG = 32 };
+enum : uint8_t { TF_RES = 1, TF_BORN = 2, TF_DEAD = 4, TF_LOCK = 8 };
 
 struct TraceDev {
   int32_t T, M, n_params;
@@ -56,11 +52,36 @@ struct TraceDev {
   const int32_t *lock_ptr, *lock_idx;
   const int32_t *die_ptr, *die_idx;
   const int32_t *params;
+  // replay only: the graph in the compact CSR form of the fast closure walk (16-bit tensor
+  // ids and offsets, 32-bit producer costs; -1 = no producer), or null when the trace is too
+  // large for it (T or edges >= 2^16, or a cost >= 2^31) -- then the generic walk is used
+  const int32_t *cg_cost;
+  const uint16_t *cg_iptr, *cg_iidx;  // inputs of producer(x): cg_iidx[cg_iptr[x] .. cg_iptr[x+1])
+  const uint16_t *cg_cptr, *cg_cout;  // outputs of the ops that read x
+  int32_t cg_nnz;
 };
+
+// Byte offsets of the compact graph's pieces in one contiguous blob (host upload and the
+// shared-memory copy use the same layout): cost int32[T], iptr u16[T+1], cptr u16[T+1],
+// iidx u16[nnz], cout u16[nnz]; each piece 16-byte aligned.  off[5] = total bytes.
+__host__ __device__ __forceinline__ void cg_offsets(int T, int nnz, size_t off[6]) {
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    const size_t r = o;
+    o = (o + b + 15) / 16 * 16;
+    return r;
+  };
+  off[0] = take((size_t)T * 4);
+  off[1] = take((size_t)(T + 1) * 2);
+  off[2] = take((size_t)(T + 1) * 2);
+  off[3] = take((size_t)nnz * 2);
+  off[4] = take((size_t)nnz * 2);
+  off[5] = o;
+}
 
 struct WsLayout {  // byte offsets inside one cell's workspace
   size_t tflags, pins, last_access, taddr, epochs, marks, stack, isz, ih, ist, S, H, B, trans, victims, cand, pacc,
-      cc, chg, dl, vis;
+      rst;
   size_t bytes;
 };
 
@@ -80,10 +101,7 @@ struct CellPtrs {
   int32_t *trans, *victims;
   int32_t *cand;
   int64_t *pacc;  // per (candidate, half) closure sums of the current pressure event
-  int64_t *cc;    // per tensor: cached |Anc| + |Desc| cost sums (valid unless TF_DIRTY)
-  int32_t *chg;   // tensors whose residency / liveness changed since the last event
-  int32_t *dl;    // candidate indices whose closure is recomputed at this event
-  uint32_t *vis;  // per (tensor, half): bitmap of the tensors its last closure walk examined
+  int32_t *rst;   // rematerialization stack: 4 x kStackCap (tensor, stage, input index, depth)
 };
 
 struct KArgs {
@@ -97,17 +115,24 @@ struct KArgs {
   int64_t log_cap;
   unsigned char *ws;
   WsLayout lay;
+  // dynamic shared memory after Shared: tfl (tfl_bytes), then (replay) the compact graph
+  // when it fits (g_smem), then `walkers` closure-walk bitmaps of vis_words words each
+  int32_t tfl_bytes;
+  int32_t g_smem;     // the compact graph is copied into shared memory
+  int32_t g_bytes;    // its size (16-byte multiple)
+  int32_t walkers;    // threads [0, walkers) walk closures (fast path); 0 = generic walk
+  int32_t vis_words;  // bitmap words per walker (ceil(T / 32), rounded to 4)
 };
 
 struct Shared {
-  uint64_t addr[2][kCap + 2];  // the inactive buffer doubles as search scratch (S, B, state)
-  uint64_t size[2][kCap + 2];
-  int32_t owner[2][kCap + 2];
-  uint8_t tfl[kMaxT];          // per-tensor flags TF_*
+  // the pool's address-ordered block table (single buffer; splices shift in place)
+  uint64_t addr[kCap + 2];
+  uint64_t size[kCap + 2];
+  int32_t owner[kCap + 2];
   uint64_t wS[kWarps];
   U192 wH[kWarps];
   int32_t wB[kWarps];
-  int32_t cur, nb;
+  int32_t nb;
   // CTA-uniform scalars (written by thread 0, published by a barrier)
   uint64_t bytes_free;
   int64_t clock;
@@ -118,19 +143,17 @@ struct Shared {
   uint64_t bcast_u;
   // counters (thread 0 only)
   coop_replay_result res;
-  // rematerialization stack
-  int32_t st_t[kStackCap], st_stage[kStackCap], st_idx[kStackCap], st_depth[kStackCap];
   // reductions
   uint64_t red64[2][kWarps];
   int32_t red32[2][kWarps];
   U192 red192[kWarps];
   int32_t redpar;
   int32_t ncand, cand_next;  // projected-cost work list of the current pressure event
-  int32_t nchg, chg_next;    // changed list (replay) and its invalidation work counter
-  int32_t ndirty;            // candidates whose closure is recomputed at this event
   // the last evicted window (read by the online calls): items, span, cost bits, victims
   int32_t win_first, win_last, nvict;
   uint64_t win_span, win_cost;
+  // dynamic tail: per-tensor flags TF_* (then the replay's graph and walker bitmaps)
+  alignas(16) uint8_t tfl[];
 };
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -207,6 +230,11 @@ struct CellT {
   int cell;
   uint32_t epoch;  // per-thread DFS epoch
   coop_event *log;
+  // fast closure walk (replay): the compact graph (shared memory or global) and this
+  // thread's visited bitmap in shared memory (threads < a.walkers)
+  const int32_t *gc;
+  const uint16_t *gip, *gcp, *gii, *gco;
+  uint32_t *vis;
 
   __device__ CellT(const KArgs &a_, Shared &sh_, int cell_) : a(a_), tr(a_.tr), sh(sh_), cell(cell_) {
     unsigned char *base = a.ws + (size_t)blockIdx.x * a.lay.bytes;  // this CTA's slot
@@ -227,19 +255,32 @@ struct CellT {
     w.victims = (int32_t *)(base + a.lay.victims);
     w.cand = (int32_t *)(base + a.lay.cand);
     w.pacc = (int64_t *)(base + a.lay.pacc);
-    w.cc = (int64_t *)(base + a.lay.cc);
-    w.chg = (int32_t *)(base + a.lay.chg);
-    w.dl = (int32_t *)(base + a.lay.dl);
-    w.vis = (uint32_t *)(base + a.lay.vis);
+    w.rst = (int32_t *)(base + a.lay.rst);
     log = a.log ? a.log + (size_t)cell * a.log_cap : nullptr;
+    gc = nullptr;
+    gip = gcp = gii = gco = nullptr;
+    vis = nullptr;
+    if (kRO && a.walkers > 0) {
+      size_t off[6];
+      cg_offsets(tr.T, tr.cg_nnz, off);
+      unsigned char *tail = sh.tfl + a.tfl_bytes;
+      const unsigned char *g = a.g_smem ? tail : reinterpret_cast<const unsigned char *>(tr.cg_cost);
+      gc = reinterpret_cast<const int32_t *>(g + off[0]);
+      gip = reinterpret_cast<const uint16_t *>(g + off[1]);
+      gcp = reinterpret_cast<const uint16_t *>(g + off[2]);
+      gii = reinterpret_cast<const uint16_t *>(g + off[3]);
+      gco = reinterpret_cast<const uint16_t *>(g + off[4]);
+      vis = reinterpret_cast<uint32_t *>(tail + (a.g_smem ? a.g_bytes : 0)) +
+            (size_t)threadIdx.x * a.vis_words;
+    }
   }
 
   __device__ __forceinline__ bool ok() const { return sh.status == COOP_OK; }
   __device__ __forceinline__ int nin(int op) const { return tr.in_ptr[op + 1] - tr.in_ptr[op]; }
   __device__ __forceinline__ int in_at(int op, int j) const { return tr.in_idx[tr.in_ptr[op] + j]; }
-  __device__ __forceinline__ uint64_t *A() { return sh.addr[sh.cur]; }
-  __device__ __forceinline__ uint64_t *Z() { return sh.size[sh.cur]; }
-  __device__ __forceinline__ int32_t *O() { return sh.owner[sh.cur]; }
+  __device__ __forceinline__ uint64_t *A() { return sh.addr; }
+  __device__ __forceinline__ uint64_t *Z() { return sh.size; }
+  __device__ __forceinline__ int32_t *O() { return sh.owner; }
 
   __device__ void log_ev(int kind, int op, int t, uint64_t addr) {  // thread 0 only
     const int64_t i = sh.res.n_events++;
@@ -251,17 +292,6 @@ struct CellT {
       e.pad = 0;
       e.addr = addr;
       log[i] = e;
-    }
-  }
-
-  // Thread 0 only: tensor t's residency / liveness changed (R18's closures may change for
-  // the resident tensors next to it); recorded once per event for the replay's closure cache.
-  __device__ __forceinline__ void changed(int t) {
-    if constexpr (kRO) {
-      if (!(sh.tfl[t] & TF_CHG)) {
-        sh.tfl[t] |= TF_CHG | TF_DIRTY;
-        w.chg[sh.nchg++] = t;
-      }
     }
   }
 
@@ -278,29 +308,42 @@ struct CellT {
   }
 
   // replace blocks [lo, hi] (hi >= lo - 1; hi = lo - 1 means pure insertion at lo) by the
-  // m new blocks nb_[0..m) -- one parallel copy into the other buffer
-  __device__ void splice(int lo, int hi, int m, const uint64_t *na, const uint64_t *nz, const int32_t *no) {
-    const int nb = sh.nb, cur = sh.cur, nxt = cur ^ 1;
+  // m new blocks na/nz/no[0..m) -- in place: every thread reads the entries it will write
+  // (at most kCap / kThreads of them) into registers, one barrier, then writes them
+  __device__ __noinline__ void splice(int lo, int hi, int m, const uint64_t *na, const uint64_t *nz, const int32_t *no) {
+    constexpr int kPer = (kCap + 2 + kThreads - 1) / kThreads;
+    const int nb = sh.nb;
     const int removed = hi - lo + 1;
     const int nnb = nb - removed + m;
-    for (int j = threadIdx.x; j < nnb; j += kThreads) {
-      uint64_t ad, sz;
-      int32_t ow;
-      if (j < lo) {
-        ad = sh.addr[cur][j]; sz = sh.size[cur][j]; ow = sh.owner[cur][j];
-      } else if (j < lo + m) {
-        ad = na[j - lo]; sz = nz[j - lo]; ow = no[j - lo];
-      } else {
-        const int s = j - m + removed;
-        ad = sh.addr[cur][s]; sz = sh.size[cur][s]; ow = sh.owner[cur][s];
+    uint64_t ra[kPer], rz[kPer];
+    int32_t ro[kPer];
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int j = lo + r * kThreads + (int)threadIdx.x;  // new position, >= lo
+      if (j < nnb) {
+        if (j < lo + m) {
+          ra[r] = na[j - lo];
+          rz[r] = nz[j - lo];
+          ro[r] = no[j - lo];
+        } else {
+          const int src = j - m + removed;
+          ra[r] = sh.addr[src];
+          rz[r] = sh.size[src];
+          ro[r] = sh.owner[src];
+        }
       }
-      sh.addr[nxt][j] = ad;
-      sh.size[nxt][j] = sz;
-      sh.owner[nxt][j] = ow;
     }
     __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int j = lo + r * kThreads + (int)threadIdx.x;
+      if (j < nnb) {
+        sh.addr[j] = ra[r];
+        sh.size[j] = rz[r];
+        sh.owner[j] = ro[r];
+      }
+    }
     if (threadIdx.x == 0) {
-      sh.cur = nxt;
       sh.nb = nnb;
       if (nnb > sh.res.max_blocks) sh.res.max_blocks = nnb;
     }
@@ -363,7 +406,6 @@ struct CellT {
     release(b);
     if (threadIdx.x == 0) {
       sh.tfl[t] &= (uint8_t)~TF_RES;
-      changed(t);
       log_ev(4, sh.cur_op, t, ad);
     }
     __syncthreads();
@@ -414,93 +456,93 @@ struct CellT {
   // one pass after a barrier forms c(t) and h.  A node is marked when pushed, so every
   // node enters a walk's stack at most once: the per-thread stack (T entries) cannot
   // overflow.
-  // next visited-mark epoch of this thread (one byte per tensor and thread, epoch & 255;
-  // the marks are cleared when the epoch wraps, every 255 walks)
-  __device__ __forceinline__ uint8_t next_epoch(uint8_t *mk, int Tp) {
-    uint8_t ep = (uint8_t)++epoch;
-    if (ep == 0) {
-      for (int x = 0; x < Tp; x += 16) *reinterpret_cast<uint4 *>(mk + x) = make_uint4(0, 0, 0, 0);
-      ep = (uint8_t)++epoch;
+  // Replay fast path of the same sums: the compact graph in shared memory and one visited
+  // BITMAP per walking thread in shared memory (threads [0, a.walkers) walk, the others
+  // wait at the barrier), so a DFS step is a handful of shared-memory accesses instead of
+  // dependent global loads; long chains of evicted tensors (the thrashing BiLSTM cells)
+  // are walked several times faster.  Same work items (candidate, half), same sets.
+  __device__ void closures_fast(const int32_t *cand, int ncand) {
+    if ((int)threadIdx.x < a.walkers) {
+      uint32_t *mk = vis;
+      const int VW = a.vis_words;
+      int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
+      const int nitems = 2 * ncand;
+      while (true) {
+        const int it = atomicAdd(&sh.cand_next, 1);
+        if (it >= nitems) break;
+        const int t = O()[cand[it >> 1]];
+        const int stage = it & 1;
+        for (int q = 0; q < VW; q += 4) *reinterpret_cast<uint4 *>(mk + q) = make_uint4(0, 0, 0, 0);
+        mk[t >> 5] |= 1u << (t & 31);
+        int sp = 0;
+        int64_t acc = 0;
+        // push y if eligible and new (mark at push: a node enters the stack at most once)
+        auto push = [&](int y) {
+          const uint8_t f = sh.tfl[y];
+          const bool el = stage == 0 ? !(f & TF_RES) : ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD));
+          const uint32_t bit = 1u << (y & 31);
+          if (el && !(mk[y >> 5] & bit)) {
+            mk[y >> 5] |= bit;
+            stk[sp++] = y;
+          }
+        };
+        auto expand = [&](int x) {
+          if (stage == 0) {
+            const int j1 = gip[x + 1];
+            for (int j = gip[x]; j < j1; ++j) push(gii[j]);
+          } else {
+            const int j1 = gcp[x + 1];
+            for (int j = gcp[x]; j < j1; ++j) push(gco[j]);
+          }
+        };
+        expand(t);  // roots: t's producer's inputs / its consumers' outputs
+        while (sp > 0) {
+          const int x = stk[--sp];
+          const int32_t cx = gc[x];
+          // ancestors: non-resident (pushed so) and recomputable; descendants: evicted and
+          // live (pushed so)
+          if (stage == 0 && cx < 0) continue;
+          acc += cx;
+          expand(x);
+        }
+        w.pacc[it] = acc;
+      }
     }
-    return ep;
-  }
-
-  // Replay closure cache.  Anc(t) / Desc(t) (and so the cached sums) depend only on the
-  // flags of the tensors their walks EXAMINE: the nodes summed and every neighbour tested
-  // for eligibility.  Each walk records that examined set in a per-(tensor, half) bitmap
-  // (w.vis); if no examined node changed its residency / liveness since the walk, a new
-  // walk would take exactly the same steps, so the cached sums are exact.  A candidate is
-  // re-walked iff its cache is invalid (TF_DIRTY: it became resident, or was not a
-  // candidate at the last event) or its bitmaps hold a tensor of the changed list.
-  __device__ __forceinline__ uint32_t *vis_of(int t, int half) const {
-    return w.vis + ((size_t)2 * t + half) * (size_t)((tr.T + 127) / 128 * 4);
   }
 
   __device__ void projected_costs(const int32_t *cand, int ncand, int pol = 0) {
+    if (kRO && a.walkers > 0) {
+      closures_fast(cand, ncand);
+      finish_costs(cand, ncand, pol);
+      return;
+    }
     // visited marks: one byte per tensor and thread (epoch & 255; cleared on wrap), four
     // times denser than word epochs so a walking thread's marks stay in L1
     const int Tp = (tr.T + 15) & ~15;  // per-thread stride, 16-byte aligned (uint4 clears)
     uint8_t *mk = reinterpret_cast<uint8_t *>(w.marks) + (size_t)threadIdx.x * Tp;
     int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
-    // replay: walk only the candidates whose cached closure may be stale
-    int nwork = ncand;
-    const int32_t *wl = nullptr;
-    const int VW = (tr.T + 127) / 128 * 4;  // bitmap words per (tensor, half), uint4-aligned
-    if constexpr (kRO) {
-      const int nchg = sh.nchg;
-      if (threadIdx.x == 0) sh.ndirty = 0;
-      __syncthreads();
-      for (int ci = threadIdx.x; ci < ncand; ci += kThreads) {
-        const int t = O()[cand[ci]];
-        bool d = (sh.tfl[t] & TF_DIRTY) || nchg > 64;
-        if (!d) {
-          const uint32_t *v0 = vis_of(t, 0), *v1 = vis_of(t, 1);
-          for (int k = 0; k < nchg && !d; ++k) {
-            const int x = w.chg[k];
-            d = ((v0[x >> 5] | v1[x >> 5]) >> (x & 31)) & 1u;
-          }
-        }
-        if (d) {
-          sh.tfl[t] |= TF_DIRTY;  // distinct candidates: distinct bytes
-          w.dl[atomicAdd(&sh.ndirty, 1)] = ci;
-        }
-      }
-      __syncthreads();
-      for (int k = threadIdx.x; k < nchg; k += kThreads) sh.tfl[w.chg[k]] &= (uint8_t)~TF_CHG;
-      __syncthreads();
-      if (threadIdx.x == 0) sh.nchg = 0;
-      nwork = sh.ndirty;
-      wl = w.dl;
-    }
-    uint32_t *bm = nullptr;  // the current walk's examined-set bitmap (replay)
-    auto note = [&](int y) {
-      if constexpr (kRO) atomicOr(&bm[y >> 5], 1u << (y & 31));  // fire-and-forget (RED)
-    };
-    const int nitems = 2 * nwork;
-    int sp = 0, it = -1, stage = 0, slot = 0;
+    const int nitems = 2 * ncand;
+    int sp = 0, it = -1, stage = 0;
     int64_t acc = 0;
     uint8_t ep = 0;
     while (true) {
       if (sp == 0) {
-        if (it >= 0) w.pacc[slot] = acc;
+        if (it >= 0) w.pacc[it] = acc;
         it = atomicAdd(&sh.cand_next, 1);
         if (it >= nitems) break;
-        const int ci = wl ? wl[it >> 1] : (it >> 1);
-        const int t = O()[cand[ci]];
+        const int t = O()[cand[it >> 1]];
         stage = it & 1;
-        slot = 2 * ci + stage;
         acc = 0;
-        ep = next_epoch(mk, Tp);
-        mk[t] = ep;
-        if constexpr (kRO) {
-          bm = vis_of(t, stage);
-          for (int q = 0; q < VW; q += 4) *reinterpret_cast<uint4 *>(bm + q) = make_uint4(0, 0, 0, 0);
+        ep = (uint8_t)++epoch;
+        if (ep == 0) {  // epoch wrap (every 255 walks): clear this thread's marks
+          for (int x = 0; x < Tp; x += 16) *reinterpret_cast<uint4 *>(mk + x) = make_uint4(0, 0, 0, 0);
+          ep = (uint8_t)++epoch;
         }
+        mk[t] = ep;
         if (stage == 0) {  // the ancestors' roots: t's producer's inputs
           const int4 r = ldg_if<kRO>(&tr.rec[t]);
           for (int j = r.z; j < r.w; ++j) {
             const int y = ldg_if<kRO>(&tr.in_idx[j]);
-            note(y);
             if (dfs_elig(y, 0) && mk[y] != ep) {
               mk[y] = ep;
               stk[sp++] = y;
@@ -509,7 +551,6 @@ struct CellT {
         } else {  // the descendants' roots: the outputs of t's consumers
           for (int e = ldg_if<kRO>(&tr.cons_head[t]); e >= 0; e = ldg_if<kRO>(&tr.cons_next[e])) {
             const int y = ldg_if<kRO>(&tr.cons_out[e]);
-            note(y);
             if (dfs_elig(y, 1) && mk[y] != ep) {
               mk[y] = ep;
               stk[sp++] = y;
@@ -535,9 +576,6 @@ struct CellT {
 #pragma unroll
           for (int k = 0; k < 4; ++k) y[k] = j0 + k < r.w ? ldg_if<kRO>(&tr.in_idx[j0 + k]) : -1;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (y[k] >= 0) note(y[k]);
-#pragma unroll
           for (int k = 0; k < 4; ++k) m[k] = (y[k] >= 0 && dfs_elig(y[k], 0)) ? mk[y[k]] : ep;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -553,7 +591,6 @@ struct CellT {
       } else {
         for (int e = ldg_if<kRO>(&tr.cons_head[x]); e >= 0; e = ldg_if<kRO>(&tr.cons_next[e])) {
           const int y = ldg_if<kRO>(&tr.cons_out[e]);
-          note(y);
           if (dfs_elig(y, 1) && mk[y] != ep) {
             mk[y] = ep;
             stk[sp++] = y;
@@ -561,26 +598,17 @@ struct CellT {
         }
       }
     }
+    finish_costs(cand, ncand, pol);
+  }
+
+  // c(t) = producer cost + the two sums; h = c / s (Coop), c / (m s) (DTR), c / ((m +
+  // adjacent free bytes) s) (DTE)
+  __device__ void finish_costs(const int32_t *cand, int ncand, int pol) {
     __syncthreads();
-    // c(t) = producer cost + the two sums; h = c / s (Coop), c / (m s) (DTR), c / ((m +
-    // adjacent free bytes) s) (DTE)
     for (int ci = threadIdx.x; ci < ncand; ci += kThreads) {
       const int b = cand[ci];
       const int t = O()[b];
-      int64_t closure;
-      if constexpr (kRO) {
-        const uint8_t f = sh.tfl[t];
-        if (f & TF_DIRTY) {  // walked at this event: refresh the cache
-          closure = w.pacc[2 * ci] + w.pacc[2 * ci + 1];
-          w.cc[t] = closure;
-          sh.tfl[t] = f & (uint8_t)~TF_DIRTY;
-        } else {
-          closure = w.cc[t];
-        }
-      } else {
-        closure = w.pacc[2 * ci] + w.pacc[2 * ci + 1];
-      }
-      const int64_t c = rec_cost(ldg_if<kRO>(&tr.rec[t])) + closure;
+      const int64_t c = rec_cost(ldg_if<kRO>(&tr.rec[t])) + w.pacc[2 * ci] + w.pacc[2 * ci + 1];
       int64_t s = sh.clock - w.last_access[t];  // staleness (R17)
       if (s < 1) s = 1;
       double den = (double)s;  // Coop: h = c/s (R1)
@@ -624,8 +652,6 @@ struct CellT {
         const int o = O()[b];
         if (o != kFree && !ldg_if<kRO>(&tr.unevict[o]) && w.pins[o] == 0 && !(sh.tfl[o] & TF_LOCK))
           w.cand[atomicAdd(&sh.ncand, 1)] = b;
-        else if (kRO && o != kFree)
-          sh.tfl[o] |= TF_DIRTY;  // not a candidate: its cache is not kept up to date
       }
       __syncthreads();
       const int nc = sh.ncand;
@@ -652,7 +678,6 @@ struct CellT {
         const int o = O()[bmin];
         const uint64_t ad = A()[bmin];
         sh.tfl[o] &= (uint8_t)~TF_RES;
-        changed(o);
         sh.res.evictions++;
         log_ev(3, sh.cur_op, o, ad);
         uint64_t d = sh.res.digest;  // R29
@@ -681,10 +706,10 @@ struct CellT {
       sh.cand_next = 0;
     }
     __syncthreads();
-    const int nb = sh.nb, nx = sh.cur ^ 1;
-    uint64_t *S = sh.addr[nx];
-    int32_t *Bc = reinterpret_cast<int32_t *>(sh.size[nx]);
-    int32_t *St = sh.owner[nx];
+    const int nb = sh.nb;
+    uint64_t *S = w.S;   // span prefix (workspace, L1-resident)
+    int32_t *Bc = w.B;   // PINNED-count prefix
+    uint8_t *St = w.ist; // item states
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // item view (contiguous chunk per thread): FREE -> h = 0; unevictable / pinned /
     // locked -> barrier; else h = c/s with the projected cost and the staleness
@@ -698,8 +723,6 @@ struct CellT {
         st = COOP_FREE;
       } else if (ldg_if<kRO>(&tr.unevict[o]) || w.pins[o] > 0 || (sh.tfl[o] & TF_LOCK)) {
         st = COOP_PINNED;
-        // not a candidate: this event's changes are not checked against its cache
-        if constexpr (kRO) sh.tfl[o] |= TF_DIRTY;
       } else {
         st = COOP_EVICTABLE;
         w.cand[atomicAdd(&sh.ncand, 1)] = b;
@@ -830,7 +853,6 @@ struct CellT {
         w.victims[sh.nvict++] = o;
         const uint64_t ad = A()[b];
         sh.tfl[o] &= (uint8_t)~TF_RES;
-        changed(o);
         sh.res.evictions++;
         log_ev(3, sh.cur_op, o, ad);
         d = splitmix64(d ^ (((uint64_t)(uint32_t)sh.cur_op << 32) | (uint32_t)o));  // R29
@@ -863,8 +885,6 @@ struct CellT {
         w.taddr[t] = ad;
         sh.tfl[src] &= (uint8_t)~TF_RES;
         sh.tfl[t] |= TF_RES;
-        changed(src);
-        changed(t);
         sh.res.inplace_reuse++;
         log_ev(2, op, t, ad);
       }
@@ -904,7 +924,6 @@ struct CellT {
     if (threadIdx.x == 0) {
       w.taddr[t] = at;
       sh.tfl[t] |= TF_RES;
-      changed(t);
       log_ev(kind, op, t, at);
     }
     __syncthreads();
@@ -916,17 +935,17 @@ struct CellT {
   __device__ void materialize(int t0) {
     if (threadIdx.x == 0) {
       sh.sp = 1;
-      sh.st_t[0] = t0;
-      sh.st_stage[0] = 0;
-      sh.st_idx[0] = 0;
-      sh.st_depth[0] = 0;
+      w.rst[0 * kStackCap + 0] = t0;
+      w.rst[1 * kStackCap + 0] = 0;
+      w.rst[2 * kStackCap + 0] = 0;
+      w.rst[3 * kStackCap + 0] = 0;
     }
     __syncthreads();
     while (sh.sp > 0 && ok()) {
       const int f = sh.sp - 1;
-      const int t = sh.st_t[f], depth = sh.st_depth[f];
+      const int t = w.rst[0 * kStackCap + f], depth = w.rst[3 * kStackCap + f];
       const int op = tr.producer[t];
-      if (sh.st_stage[f] == 0) {
+      if (w.rst[1 * kStackCap + f] == 0) {
         __syncthreads();
         if (threadIdx.x == 0) {
           if (depth > a.max_depth) {
@@ -937,7 +956,7 @@ struct CellT {
             sh.res.fail_op = sh.cur_op;
           } else {
             if (depth > sh.res.max_depth) sh.res.max_depth = depth;
-            sh.st_stage[f] = 1;
+            w.rst[1 * kStackCap + f] = 1;
           }
         }
         __syncthreads();
@@ -946,26 +965,26 @@ struct CellT {
         __syncthreads();
         continue;
       }
-      if (sh.st_stage[f] == 1) {
-        int j = sh.st_idx[f];
+      if (w.rst[1 * kStackCap + f] == 1) {
+        int j = w.rst[2 * kStackCap + f];
         const int n = nin(op);
         while (j < n && (sh.tfl[in_at(op, j)] & TF_RES)) ++j;
         __syncthreads();
         if (threadIdx.x == 0) {
           if (j < n) {
-            sh.st_idx[f] = j + 1;
+            w.rst[2 * kStackCap + f] = j + 1;
             if (sh.sp >= kStackCap) {
               sh.status = COOP_ERR_THRASHED;
               sh.res.fail_op = sh.cur_op;
             } else {
               const int g = sh.sp++;
-              sh.st_t[g] = in_at(op, j);
-              sh.st_stage[g] = 0;
-              sh.st_idx[g] = 0;
-              sh.st_depth[g] = depth + 1;
+              w.rst[0 * kStackCap + g] = in_at(op, j);
+              w.rst[1 * kStackCap + g] = 0;
+              w.rst[2 * kStackCap + g] = 0;
+              w.rst[3 * kStackCap + g] = depth + 1;
             }
           } else {
-            sh.st_stage[f] = 2;
+            w.rst[1 * kStackCap + f] = 2;
           }
         }
         __syncthreads();
@@ -1008,11 +1027,10 @@ struct CellT {
       w.taddr[t] = 0;
     }
     if (threadIdx.x == 0) {
-      sh.cur = 0;
       sh.nb = 1;
-      sh.addr[0][0] = 0;
-      sh.size[0][0] = budget;
-      sh.owner[0][0] = kFree;
+      sh.addr[0] = 0;
+      sh.size[0] = budget;
+      sh.owner[0] = kFree;
       sh.bytes_free = budget;
       sh.clock = 0;
       sh.status = COOP_OK;
@@ -1023,7 +1041,6 @@ struct CellT {
       sh.res.digest = 0x9E3779B97F4A7C15ull;
       sh.res.budget = budget;
       sh.res.max_blocks = 1;
-      sh.nchg = 0;
     }
     epoch = w.epochs[threadIdx.x];
     __syncthreads();
@@ -1046,7 +1063,6 @@ struct CellT {
         if (threadIdx.x == 0) {
           w.taddr[t] = at;
           sh.tfl[t] = TF_RES | TF_BORN;
-          changed(t);
           log_ev(0, -1, t, at);
         }
         __syncthreads();
@@ -1095,10 +1111,7 @@ struct CellT {
       __syncthreads();
       // deaths after op k (R20) merged with transient dead recomputes (R22), ascending id
       if (threadIdx.x == 0) {
-        for (int j = tr.die_ptr[k]; j < tr.die_ptr[k + 1]; ++j) {
-          sh.tfl[tr.die_idx[j]] |= TF_DEAD;
-          changed(tr.die_idx[j]);
-        }
+        for (int j = tr.die_ptr[k]; j < tr.die_ptr[k + 1]; ++j) sh.tfl[tr.die_idx[j]] |= TF_DEAD;
         // insertion-sort the transient list (small) and merge with the (sorted) die list
         int *tl = w.trans;
         const int nt = sh.ntrans;
@@ -1164,10 +1177,7 @@ WsLayout make_layout(int T) {
   L.victims = take((size_t)kCap * 4);
   L.cand = take((size_t)(kCap + 2) * 4);
   L.pacc = take((size_t)(kCap + 2) * 2 * 8);
-  L.cc = take((size_t)T * 8);
-  L.chg = take((size_t)T * 4);
-  L.dl = take((size_t)(kCap + 2) * 4);
-  L.vis = take((size_t)2 * T * ((T + 127) / 128 * 4) * 4);
+  L.rst = take((size_t)4 * kStackCap * 4);
   L.bytes = o;
   return L;
 }
