@@ -467,45 +467,49 @@ struct CellT {
       const int VW = a.vis_words;
       int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
       const int nitems = 2 * ncand;
-      while (true) {
-        const int it = atomicAdd(&sh.cand_next, 1);
-        if (it >= nitems) break;
-        const int t = O()[cand[it >> 1]];
-        const int stage = it & 1;
-        for (int q = 0; q < VW; q += 4) *reinterpret_cast<uint4 *>(mk + q) = make_uint4(0, 0, 0, 0);
-        mk[t >> 5] |= 1u << (t & 31);
-        int sp = 0;
-        int64_t acc = 0;
-        // push y if eligible and new (mark at push: a node enters the stack at most once)
-        auto push = [&](int y) {
-          const uint8_t f = sh.tfl[y];
-          const bool el = stage == 0 ? !(f & TF_RES) : ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD));
-          const uint32_t bit = 1u << (y & 31);
-          if (el && !(mk[y >> 5] & bit)) {
-            mk[y >> 5] |= bit;
-            stk[sp++] = y;
-          }
-        };
-        auto expand = [&](int x) {
-          if (stage == 0) {
-            const int j1 = gip[x + 1];
-            for (int j = gip[x]; j < j1; ++j) push(gii[j]);
-          } else {
-            const int j1 = gcp[x + 1];
-            for (int j = gcp[x]; j < j1; ++j) push(gco[j]);
-          }
-        };
-        expand(t);  // roots: t's producer's inputs / its consumers' outputs
-        while (sp > 0) {
-          const int x = stk[--sp];
-          const int32_t cx = gc[x];
-          // ancestors: non-resident (pushed so) and recomputable; descendants: evicted and
-          // live (pushed so)
-          if (stage == 0 && cx < 0) continue;
-          acc += cx;
-          expand(x);
+      int sp = 0, it = -1, stage = 0;
+      int64_t acc = 0;
+      // push y if eligible and new (mark at push: a node enters the stack at most once)
+      auto push = [&](int y) {
+        const uint8_t f = sh.tfl[y];
+        const bool el = stage == 0 ? !(f & TF_RES) : ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD));
+        const uint32_t bit = 1u << (y & 31);
+        if (el && !(mk[y >> 5] & bit)) {
+          mk[y >> 5] |= bit;
+          stk[sp++] = y;
         }
-        w.pacc[it] = acc;
+      };
+      auto expand = [&](int x) {
+        if (stage == 0) {
+          const int j1 = gip[x + 1];
+          for (int j = gip[x]; j < j1; ++j) push(gii[j]);
+        } else {
+          const int j1 = gcp[x + 1];
+          for (int j = gcp[x]; j < j1; ++j) push(gco[j]);
+        }
+      };
+      // one flat loop: every iteration either starts the next work item or pops one node,
+      // so the lanes of a warp stay converged while their closures differ in size
+      while (true) {
+        if (sp == 0) {
+          if (it >= 0) w.pacc[it] = acc;
+          it = atomicAdd(&sh.cand_next, 1);
+          if (it >= nitems) break;
+          const int t = O()[cand[it >> 1]];
+          stage = it & 1;
+          acc = 0;
+          for (int q = 0; q < VW; q += 4) *reinterpret_cast<uint4 *>(mk + q) = make_uint4(0, 0, 0, 0);
+          mk[t >> 5] |= 1u << (t & 31);
+          expand(t);  // roots: t's producer's inputs / its consumers' outputs
+          continue;
+        }
+        const int x = stk[--sp];
+        const int32_t cx = gc[x];
+        // ancestors: non-resident (pushed so) and recomputable; descendants: evicted and
+        // live (pushed so)
+        if (stage == 0 && cx < 0) continue;
+        acc += cx;
+        expand(x);
       }
     }
   }
