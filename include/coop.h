@@ -220,6 +220,28 @@ int coop_replay_trace(coop_trace_t trace, const uint64_t *budgets, int32_t n_bud
 
 
 /*
+ * coop_replay_snapshots -- the second config-4 workload of SURVEY.md 8(d): the pools the
+ * window search really sees.  Replays `trace` once under `budget` with the Coop policy
+ * (flags as coop_replay_trace; the DTR / DTE baselines have no window search ->
+ * COOP_ERR_INVALID_ARG) and records, at each of the first `cap` pressure events whose pool
+ * holds at most n_max blocks, the address-ordered item view that the sliding-window search
+ * ran on (R10-R18): one row of a coop_window_search_batched table with
+ * pool_stride = n_max -- size | state << 62 per block, cost = c(t) (R18) and stale = s(t)
+ * (R17) as binary64 for EVICTABLE blocks (0 / 1 otherwise), padded with trailing PINNED
+ * items of size 1 (a trailing barrier cannot change any window, index or span) -- plus the
+ * request (requests[k]) and the window the replay evicted (windows[k], as the batched
+ * search reports it; status COOP_INFEASIBLE when none existed).  DEVICE arrays:
+ * size_state / cost / stale [cap * n_max], requests / windows [cap], count (int64: events
+ * recorded), out (the cell's coop_replay_result).  n_max in [1, COOP_MAX_BLOCKS].
+ * Asynchronous on `stream`; same handle rules as coop_replay_trace.
+ */
+int coop_replay_snapshots(coop_trace_t trace, uint64_t budget, uint32_t flags,
+                          uint32_t class_threshold, int32_t max_depth, int32_t n_max, int64_t cap,
+                          uint64_t *size_state, double *cost, double *stale, uint64_t *requests,
+                          coop_window *windows, int64_t *count, coop_replay_result *out,
+                          coop_stream_t stream);
+
+/*
  * coop_budget_search -- the two budget metrics of Sec. 4.2 and App. C
  * for one trace, by waves of coop_replay_trace (one CTA per budget):
  *   min budget    = the smallest budget at which the replay completes (status COOP_OK),

@@ -170,6 +170,9 @@ lib.coop_replay_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int
                                   ctypes.c_uint32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_int64, ctypes.c_void_p]
 lib.coop_replay_trace.restype = ctypes.c_int
+lib.coop_replay_snapshots.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                      ctypes.c_int32, ctypes.c_int32, ctypes.c_int64] + [ctypes.c_void_p] * 8
+lib.coop_replay_snapshots.restype = ctypes.c_int
 
 
 class Trace:
@@ -225,6 +228,34 @@ class Trace:
                                    _stream_handle(stream))
         if rc != OK:
             raise CoopError(rc, "coop_replay_trace")
+
+    def snapshots_device(self, budget: int, flags: int, n_max: int, ss, cost, stale, requests, windows,
+                         count, out, cap: int, class_threshold: int = 0, max_depth: int = 0, stream=None) -> None:
+        """coop_replay_snapshots into device buffers (torch tensors); asynchronous."""
+        rc = lib.coop_replay_snapshots(self.handle, int(budget), int(flags), int(class_threshold),
+                                       int(max_depth), int(n_max), int(cap), _ptr(ss), _ptr(cost),
+                                       _ptr(stale), _ptr(requests), _ptr(windows), _ptr(count), _ptr(out),
+                                       _stream_handle(stream))
+        if rc != OK:
+            raise CoopError(rc, "coop_replay_snapshots")
+
+    def snapshots(self, budget: int, flags: int, n_max: int, cap: int):
+        """Synchronous: -> dict of device tensors ss / cost / stale [cap * n_max], requests [cap],
+        windows (raw int64 [cap * 4]), plus count (int) and the replay result record."""
+        import torch
+        d = dict(ss=torch.empty(cap * n_max, dtype=torch.int64, device="cuda"),
+                 cost=torch.empty(cap * n_max, dtype=torch.float64, device="cuda"),
+                 stale=torch.empty(cap * n_max, dtype=torch.float64, device="cuda"),
+                 requests=torch.empty(cap, dtype=torch.int64, device="cuda"),
+                 windows=torch.empty(cap * 4, dtype=torch.int64, device="cuda"))
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        out = torch.empty(REPLAY_RESULT_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+        self.snapshots_device(budget, flags, n_max, d["ss"], d["cost"], d["stale"], d["requests"],
+                              d["windows"], cnt, out, cap)
+        torch.cuda.synchronize()
+        d["count"] = int(cnt.item())
+        d["result"] = out.cpu().numpy().view(REPLAY_RESULT_DTYPE)[0]
+        return d
 
     def replay(self, budgets, flags, log_cap: int = 0, class_threshold: int = 0, max_depth: int = 0):
         """Synchronous convenience wrapper -> (results [n], events [n, log_cap] or None)."""

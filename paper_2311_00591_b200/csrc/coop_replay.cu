@@ -377,9 +377,19 @@ extern "C" int coop_trace_peak_live(coop_trace_t t, uint32_t flags, uint64_t *ou
   return COOP_OK;
 }
 
+struct SnapSink {
+  uint64_t *ss;
+  double *c, *s;
+  uint64_t *req;
+  coop_window *win;
+  int64_t *count;
+  int64_t cap;
+  int32_t n;
+};
+
 static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_budgets, uint32_t flags,
                             uint32_t class_threshold, int32_t max_depth, coop_replay_result *out,
-                            coop_event *log, int64_t log_cap, cudaStream_t st);
+                            coop_event *log, int64_t log_cap, cudaStream_t st, const SnapSink *snap = nullptr);
 
 extern "C" int coop_replay_trace(coop_trace_t t, const uint64_t *budgets, int32_t n_budgets,
                                  uint32_t flags, uint32_t class_threshold, int32_t max_depth,
@@ -404,7 +414,7 @@ extern "C" int coop_replay_trace(coop_trace_t t, const uint64_t *budgets, int32_
 
 static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_budgets, uint32_t flags,
                             uint32_t class_threshold, int32_t max_depth, coop_replay_result *out,
-                            coop_event *log, int64_t log_cap, cudaStream_t st) {
+                            coop_event *log, int64_t log_cap, cudaStream_t st, const SnapSink *snap) {
   const int up = upload_trace(t);
   if (up != COOP_OK) return up;
   if (!t->done && cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming) != cudaSuccess) return COOP_ERR_CUDA;
@@ -422,9 +432,10 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   int g_smem = 0, walkers = 0;
   const int g_bytes = (int)t->cg.size();
   const char *wenv = getenv("COOP_REPLAY_WALK");  // profiling hook: "generic" disables the fast walk
+  const char *genv = getenv("COOP_REPLAY_GSMEM");  // profiling hook: "0" keeps the graph in global memory
   if (!t->cg.empty() && !(wenv && wenv[0] == 'g')) {
     const size_t per = (size_t)vis_words * 4;
-    if (base + (size_t)g_bytes + 32 * per <= (size_t)max_smem) {
+    if (!(genv && genv[0] == '0') && base + (size_t)g_bytes + 32 * per <= (size_t)max_smem) {
       g_smem = 1;
       walkers = (int)std::min<size_t>(kThreads, ((size_t)max_smem - base - g_bytes) / per);
     } else if (base + 32 * per <= (size_t)max_smem) {
@@ -472,11 +483,45 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   a.g_bytes = g_bytes;
   a.walkers = walkers;
   a.vis_words = vis_words;
+  if (snap) {
+    if (cudaMemsetAsync(snap->count, 0, sizeof(int64_t), st) != cudaSuccess) return COOP_ERR_CUDA;
+    a.snap_ss = snap->ss;
+    a.snap_c = snap->c;
+    a.snap_s = snap->s;
+    a.snap_req = snap->req;
+    a.snap_win = snap->win;
+    a.snap_count = snap->count;
+    a.snap_cap = snap->cap;
+    a.snap_n = snap->n;
+  }
   // each CTA owns a workspace slot: cells are assigned cyclically, CTA b takes cells
   // b, b + grid, ... and always uses slot b
   replay_kernel<<<(unsigned)cells, kThreads, smem, st>>>(a);
   if (cudaGetLastError() != cudaSuccess) return COOP_ERR_CUDA;
   return cudaEventRecord(t->done, st) == cudaSuccess ? COOP_OK : COOP_ERR_CUDA;
+}
+
+extern "C" int coop_replay_snapshots(coop_trace_t t, uint64_t budget, uint32_t flags, uint32_t class_threshold,
+                                     int32_t max_depth, int32_t n_max, int64_t cap, uint64_t *size_state,
+                                     double *cost, double *stale, uint64_t *requests, coop_window *windows,
+                                     int64_t *count, coop_replay_result *out, coop_stream_t stream) {
+  if (!t || budget < 1 || bad_flags(flags) || (flags & (COOP_F_POLICY_DTR | COOP_F_POLICY_DTE)) ||
+      max_depth > 1024 || n_max < 1 || n_max > COOP_MAX_BLOCKS || cap < 0 || !out || !count)
+    return COOP_ERR_INVALID_ARG;
+  if (cap > 0 && (!size_state || !cost || !stale || !requests || !windows)) return COOP_ERR_INVALID_ARG;
+  if (!is_device_ptr(out) || !is_device_ptr(count) ||
+      (cap > 0 && (!is_device_ptr(size_state) || !is_device_ptr(cost) || !is_device_ptr(stale) ||
+                   !is_device_ptr(requests) || !is_device_ptr(windows))))
+    return COOP_ERR_INVALID_ARG;
+  if (t->T > kMaxT) return COOP_ERR_NOMEM;
+  SnapSink snap{size_state, cost, stale, requests, windows, count, cap, n_max};
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (t->dev && prev != t->device) cudaSetDevice(t->device);
+  const int rc = replay_on_device(t, &budget, 1, flags, class_threshold, max_depth, out, nullptr, 0,
+                                  (cudaStream_t)stream, &snap);
+  if (prev != t->device) cudaSetDevice(prev);
+  return rc;
 }
 
 // ------------------------------------------------------------------ budget searches (R45)

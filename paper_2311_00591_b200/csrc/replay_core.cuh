@@ -81,7 +81,7 @@ __host__ __device__ __forceinline__ void cg_offsets(int T, int nnz, size_t off[6
 
 struct WsLayout {  // byte offsets inside one cell's workspace
   size_t tflags, pins, last_access, taddr, epochs, marks, stack, isz, ih, ist, S, H, B, trans, victims, cand, pacc,
-      rst;
+      rst, vc, vs;
   size_t bytes;
 };
 
@@ -102,6 +102,7 @@ struct CellPtrs {
   int32_t *cand;
   int64_t *pacc;  // per (candidate, half) closure sums of the current pressure event
   int32_t *rst;   // rematerialization stack: 4 x kStackCap (tensor, stage, input index, depth)
+  int64_t *vc, *vs;  // c(t) and s(t) of the item view's EVICTABLE blocks (snapshots)
 };
 
 struct KArgs {
@@ -122,6 +123,15 @@ struct KArgs {
   int32_t g_bytes;    // its size (16-byte multiple)
   int32_t walkers;    // threads [0, walkers) walk closures (fast path); 0 = generic walk
   int32_t vis_words;  // bitmap words per walker (ceil(T / 32), rounded to 4)
+  // coop_replay_snapshots: the item view of every Coop pressure event (one cell), as rows
+  // of a batched-search table (stride snap_n), plus the request and the evicted window
+  uint64_t *snap_ss;
+  double *snap_c, *snap_s;
+  uint64_t *snap_req;
+  coop_window *snap_win;
+  int64_t *snap_count;
+  int64_t snap_cap;
+  int32_t snap_n;
 };
 
 struct Shared {
@@ -256,6 +266,8 @@ struct CellT {
     w.cand = (int32_t *)(base + a.lay.cand);
     w.pacc = (int64_t *)(base + a.lay.pacc);
     w.rst = (int32_t *)(base + a.lay.rst);
+    w.vc = (int64_t *)(base + a.lay.vc);
+    w.vs = (int64_t *)(base + a.lay.vs);
     log = a.log ? a.log + (size_t)cell * a.log_cap : nullptr;
     gc = nullptr;
     gip = gcp = gii = gco = nullptr;
@@ -625,6 +637,10 @@ struct CellT {
         den = __dmul_rn((double)m, (double)s);
       }
       w.ih[b] = __ddiv_rn((double)c, den);
+      if (a.snap_ss) {
+        w.vc[b] = c;
+        w.vs[b] = s;
+      }
     }
   }
 
@@ -738,6 +754,33 @@ struct CellT {
     __syncthreads();
     projected_costs(w.cand, sh.ncand);
     __syncthreads();
+    int snap = -1;  // coop_replay_snapshots: this event's row
+    if (a.snap_ss) {
+      if (threadIdx.x == 0) {
+        const int64_t k = *a.snap_count;
+        sh.bcast_i = (k < a.snap_cap && nb <= a.snap_n) ? (int32_t)k : -1;
+      }
+      __syncthreads();
+      snap = sh.bcast_i;
+      if (snap >= 0) {
+        const size_t row = (size_t)snap * a.snap_n;
+        for (int b = threadIdx.x; b < a.snap_n; b += kThreads) {
+          uint64_t ss = (1ull | ((uint64_t)COOP_PINNED << 62));  // padding: PINNED, size 1
+          double c = 0.0, sv = 1.0;
+          if (b < nb) {
+            ss = Z()[b] | ((uint64_t)St[b] << 62);
+            if (St[b] == COOP_EVICTABLE) {
+              c = (double)w.vc[b];
+              sv = (double)w.vs[b];
+            }
+          }
+          a.snap_ss[row + b] = ss;
+          a.snap_c[row + b] = c;
+          a.snap_s[row + b] = sv;
+        }
+        if (threadIdx.x == 0) a.snap_req[snap] = need;
+      }
+    }
     uint64_t ls = 0;
     U192 lh = u192_zero();
     int lb = 0;
@@ -829,6 +872,16 @@ struct CellT {
       if (dt > sh.res.search_ns_max) sh.res.search_ns_max = dt;
     }
     if (cmin == ~0ull) {
+      if (snap >= 0 && threadIdx.x == 0) {  // no window: the batched search's INFEASIBLE record
+        coop_window wv;
+        wv.first = wv.last = -1;
+        wv.span = 0;
+        wv.cost = __longlong_as_double(0x7ff0000000000000ll);
+        wv.n_evict = 0;
+        wv.status = COOP_INFEASIBLE;
+        a.snap_win[snap] = wv;
+        *a.snap_count = snap + 1;
+      }
       __syncthreads();
       return false;
     }
@@ -864,6 +917,17 @@ struct CellT {
         sh.bytes_free += Z()[b];
       }
       sh.res.digest = d;
+      if (snap >= 0) {  // the window the replay evicts, as a coop_window
+        coop_window wv;
+        wv.first = first;
+        wv.last = last;
+        wv.span = sh.win_span;
+        wv.cost = __longlong_as_double((long long)cmin);
+        wv.n_evict = sh.nvict;
+        wv.status = COOP_OK;
+        a.snap_win[snap] = wv;
+        *a.snap_count = snap + 1;
+      }
     }
     __syncthreads();
     // the window and its free neighbours coalesce into one free block
@@ -1182,6 +1246,8 @@ WsLayout make_layout(int T) {
   L.cand = take((size_t)(kCap + 2) * 4);
   L.pacc = take((size_t)(kCap + 2) * 2 * 8);
   L.rst = take((size_t)4 * kStackCap * 4);
+  L.vc = take((size_t)(kCap + 2) * 8);
+  L.vs = take((size_t)(kCap + 2) * 8);
   L.bytes = o;
   return L;
 }
