@@ -365,6 +365,74 @@ def replay_bench(world: int, rank: int, steps: int, with_config5: bool, with_ora
     return out, launches
 
 
+def snapshot_bench(dev, steps: int, total: int = 1 << 16, n_max: int = N_BLOCKS):
+    """BASELINE config 4's second workload: the item views the replay's
+    window search really sees.  GPU replays of the eight DNN traces at several budgets record
+    every Coop pressure event's view (coop_replay_snapshots, untimed) as rows of a batched
+    table padded to n_max with trailing PINNED items; coop_window_search_batched is then
+    timed over all rows, and its windows are compared with the windows the replays evicted."""
+    import numpy as np
+    import torch
+
+    from gen import dnn
+    from paper_2311_00591_b200 import coop
+    flags = coop.F_PARTITION | coop.F_INPLACE
+    ss = torch.empty(total * n_max, dtype=torch.int64, device=dev)
+    cst = torch.empty(total * n_max, dtype=torch.float64, device=dev)
+    stl = torch.empty(total * n_max, dtype=torch.float64, device=dev)
+    req = torch.empty(total, dtype=torch.int64, device=dev)
+    win = torch.empty(total * 4, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    res = torch.empty(coop.REPLAY_RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    k, per_trace = 0, {}
+    t_cap = time.perf_counter()
+    plan = [(name, f) for f in (0.35, 0.5, 0.65, 0.8) for name in dnn.DNNS
+            if not (name == "bilstm" and f < 0.5)]
+    for name, f in plan:
+        if k >= total:
+            break
+        t = coop.Trace(dnn.dnn(name))
+        cap = min(4096, total - k)
+        t.snapshots_device(int(t.peak_live(flags) * f), flags, n_max, ss[k * n_max:], cst[k * n_max:],
+                           stl[k * n_max:], req[k:], win[4 * k:], cnt, res, cap)
+        torch.cuda.synchronize()
+        got = int(cnt.item())
+        per_trace[f"{name}@{f}"] = got
+        k += got
+        t.close()
+    t_cap = time.perf_counter() - t_cap
+    if k == 0:
+        return None
+    out = torch.empty(k * 4, dtype=torch.int64, device=dev)
+
+    def step():
+        coop.window_search_batched(ss, cst, stl, req, out, k, n_max, n_max)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    g = coop.windows_from_device(out)
+    w = coop.windows_from_device(win[:4 * k])
+    mism = int(sum((g[f] != w[f]).sum() for f in ("status", "first", "last", "span", "n_evict"))
+               + (g["cost"].view(np.uint64) != w["cost"].view(np.uint64)).sum())
+    bytes_q = 24 * n_max + 8 + 32
+    return {"workload": "replay snapshots: the item views of the Coop pressure events of GPU replays of "
+                        "the eight DNN traces (budgets 35/50/65/80 % of peak, <= 4096 per cell), padded "
+                        f"to {n_max} blocks with trailing PINNED items",
+            "queries": k, "per_cell": per_trace, "ms_per_step": ms, "queries_per_s": k / (ms / 1e3),
+            "achieved_GBps": k * bytes_q / (ms / 1e3) / 1e9,
+            "parity": {"field_mismatches_vs_replay_windows": mism, "queries": k},
+            "capture_s": t_cap}
+
+
 def config1_latency(dev, calls: int = 2000):
     """BASELINE config 1: one 32-block query per call (launch + stream sync, host wall
     clock), and the same launch captured in a CUDA graph; the paper's < 0.4 us
@@ -558,6 +626,7 @@ def main():
             "kernel": "coop::search_kernel", "kernel_ms_mean": kmean,
             "kernel_ms_min": min(kernel_ms), "frac_of_8TBps": achieved / 8000.0}
     lat1 = config1_latency(dev) if rank == 0 else None
+    snap = snapshot_bench(dev, 10) if (rank == 0 and not args.no_replay) else None
     replay, replay_launches = None, 0
     with_oracle = (rank == 0 and world == 1 and not args.no_cpu_baseline)
     if not args.no_replay:
@@ -583,7 +652,7 @@ def main():
                                parallelism=f"dp{world} (pool shards, weak scaling)"),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": args.steps, "clocks": clk,
-                "config1_latency": lat1, "replay": replay,
+                "config1_latency": lat1, "snapshot_workload": snap, "replay": replay,
                 "results": {"status_counts": stat, "records_sha256": job_sha,
                             "gather_ms": gather_ms, "records": int(len(res_all)),
                             "gather": "NCCL all_gather_into_tensor of the 32-byte windows"

@@ -377,6 +377,14 @@ extern "C" int coop_trace_peak_live(coop_trace_t t, uint32_t flags, uint64_t *ou
   return COOP_OK;
 }
 
+static int64_t *coop__last_phase_buf = nullptr;
+// test / profiling hook (not part of the ABI): copy the last replay's phase times (8 per cell)
+extern "C" int coop__replay_phase_ns(int64_t *host, int32_t n_cells) {
+  if (!coop__last_phase_buf) return COOP_ERR_INVALID_ARG;
+  return cudaMemcpy(host, coop__last_phase_buf, (size_t)n_cells * 64, cudaMemcpyDeviceToHost) == cudaSuccess
+             ? COOP_OK : COOP_ERR_CUDA;
+}
+
 struct SnapSink {
   uint64_t *ss;
   double *c, *s;
@@ -483,6 +491,21 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   a.g_bytes = g_bytes;
   a.walkers = walkers;
   a.vis_words = vis_words;
+  {  // profiling hook: COOP_REPLAY_PHASES=1 accumulates per-phase pressure-event times per cell
+    static int64_t *pbuf = nullptr;
+    static size_t pcap = 0;
+    const char *pe = getenv("COOP_REPLAY_PHASES");
+    if (pe && pe[0] == '1') {
+      if ((size_t)n_budgets * 8 > pcap) {
+        if (pbuf) cudaFree(pbuf);
+        pcap = (size_t)n_budgets * 8;
+        if (cudaMalloc(&pbuf, pcap * 8) != cudaSuccess) return COOP_ERR_NOMEM;
+      }
+      cudaMemsetAsync(pbuf, 0, (size_t)n_budgets * 64, st);
+      a.phase_ns = pbuf;
+      coop__last_phase_buf = pbuf;
+    }
+  }
   if (snap) {
     if (cudaMemsetAsync(snap->count, 0, sizeof(int64_t), st) != cudaSuccess) return COOP_ERR_CUDA;
     a.snap_ss = snap->ss;

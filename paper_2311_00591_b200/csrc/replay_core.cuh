@@ -132,6 +132,7 @@ struct KArgs {
   int64_t *snap_count;
   int64_t snap_cap;
   int32_t snap_n;
+  int64_t *phase_ns;  // profiling hook (COOP_REPLAY_PHASES): per cell, ns in 8 pressure-event phases
 };
 
 struct Shared {
@@ -752,8 +753,10 @@ struct CellT {
       St[b] = st;
     }
     __syncthreads();
+    const uint64_t t1 = gtimer();
     projected_costs(w.cand, sh.ncand);
     __syncthreads();
+    const uint64_t t2 = gtimer();
     int snap = -1;  // coop_replay_snapshots: this event's row
     if (a.snap_ss) {
       if (threadIdx.x == 0) {
@@ -863,6 +866,7 @@ struct CellT {
         besti = i;
       }
     }
+    const uint64_t t3 = gtimer();
     const uint64_t cmin = cta_min_u64(sh, bestc);
     const int first = cta_min_i32(sh, bestc == cmin ? besti : 0x7fffffff);
     if (threadIdx.x == 0) {
@@ -937,6 +941,15 @@ struct CellT {
     const uint64_t na = A()[lo], nz = A()[hi] + Z()[hi] - A()[lo];
     const int32_t no = kFree;
     splice(lo, hi, 1, &na, &nz, &no);
+    if (a.phase_ns && threadIdx.x == 0) {  // view, closures, scans + ends + costs, argmin + evict + splice
+      int64_t *pn = a.phase_ns + (size_t)cell * 8;
+      const uint64_t t4 = gtimer();
+      pn[0] += (int64_t)(t1 - t0);
+      pn[1] += (int64_t)(t2 - t1);
+      pn[2] += (int64_t)(t3 - t2);
+      pn[3] += (int64_t)(t4 - t3);
+      pn[4] += 1;
+    }
     return true;
   }
 

@@ -19,3 +19,10 @@ t = time.time(); o, _ = O.replay(tr, budgets[0], 3); do = time.time() - t
 print(name, frac, "gpu ms", round(dt * 1e3, 2), "oracle ms", round(do * 1e3, 2), "status", r["status"], o["status"],
       "press", r["pressure"], "remat", r["remat"], "evict", r["evictions"], "ops", tr.n_ops,
       "search_ns_total", r["search_ns_total"], "digest_eq", int(r["digest"]) == int(o["digest"]))
+if os.environ.get("COOP_REPLAY_PHASES") == "1":
+    import ctypes
+    buf = np.zeros(8 * ncell, np.int64)
+    coop.lib.coop__replay_phase_ns(ctypes.c_void_p(buf.ctypes.data), ncell)
+    ev = max(1, buf[4])
+    print("per event (us): view %.1f  closures %.1f  scans+ends %.1f  argmin+evict+splice %.1f  events %d" %
+          tuple([buf[i] / ev / 1e3 for i in range(4)] + [buf[4]]))
