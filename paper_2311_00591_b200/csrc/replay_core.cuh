@@ -21,6 +21,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kCap = 4096;       // blocks per pool held by the kernel (COOP_ERR_NOMEM beyond)
 constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
 constexpr int kFree = -1;
+constexpr int kSeg = 64;  // replay fast walk: stack entries per walker kept in shared memory
 
 // replay / pool flag validation: known bits, at most one baseline policy
 inline bool bad_flags(uint32_t f) {
@@ -246,6 +247,7 @@ struct CellT {
   const int32_t *gc;
   const uint16_t *gip, *gcp, *gii, *gco;
   uint32_t *vis;
+  uint16_t *seg;  // the bottom kSeg entries of this walker's DFS stack (shared memory)
 
   __device__ CellT(const KArgs &a_, Shared &sh_, int cell_) : a(a_), tr(a_.tr), sh(sh_), cell(cell_) {
     unsigned char *base = a.ws + (size_t)blockIdx.x * a.lay.bytes;  // this CTA's slot
@@ -273,6 +275,7 @@ struct CellT {
     gc = nullptr;
     gip = gcp = gii = gco = nullptr;
     vis = nullptr;
+    seg = nullptr;
     if (kRO && a.walkers > 0) {
       size_t off[6];
       cg_offsets(tr.T, tr.cg_nnz, off);
@@ -285,6 +288,9 @@ struct CellT {
       gco = reinterpret_cast<const uint16_t *>(g + off[4]);
       vis = reinterpret_cast<uint32_t *>(tail + (a.g_smem ? a.g_bytes : 0)) +
             (size_t)threadIdx.x * a.vis_words;
+      seg = reinterpret_cast<uint16_t *>(tail + (a.g_smem ? a.g_bytes : 0) +
+                                         (size_t)a.walkers * a.vis_words * 4) +
+            (size_t)threadIdx.x * kSeg;
     }
   }
 
@@ -478,7 +484,8 @@ struct CellT {
     if ((int)threadIdx.x < a.walkers) {
       uint32_t *mk = vis;
       const int VW = a.vis_words;
-      int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
+      int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;  // entries beyond kSeg (global)
+      uint16_t *sg = seg;
       const int nitems = 2 * ncand;
       int sp = 0, it = -1, stage = 0;
       int64_t acc = 0;
@@ -489,7 +496,9 @@ struct CellT {
         const uint32_t bit = 1u << (y & 31);
         if (el && !(mk[y >> 5] & bit)) {
           mk[y >> 5] |= bit;
-          stk[sp++] = y;
+          if (sp < kSeg) sg[sp] = (uint16_t)y;
+          else stk[sp - kSeg] = y;
+          ++sp;
         }
       };
       auto expand = [&](int x) {
@@ -516,7 +525,8 @@ struct CellT {
           expand(t);  // roots: t's producer's inputs / its consumers' outputs
           continue;
         }
-        const int x = stk[--sp];
+        --sp;
+        const int x = sp < kSeg ? (int)sg[sp] : stk[sp - kSeg];
         const int32_t cx = gc[x];
         // ancestors: non-resident (pushed so) and recomputable; descendants: evicted and
         // live (pushed so)
@@ -1151,14 +1161,13 @@ struct CellT {
     }
     for (int k = 0; k < M && ok(); ++k) {
       const int n = nin(k), o = tr.out[k], src = tr.src[k];
-      if (threadIdx.x == 0) {
-        sh.cur_op = k;
-        sh.ntrans = 0;
-      }
+      if (threadIdx.x == 0) sh.cur_op = k;  // read by thread 0 only
       for (int j = threadIdx.x; j < n; j += kThreads) atomicAdd(&w.pins[in_at(k, j)], 1);
       for (int j = tr.lock_ptr[k] + threadIdx.x; j < tr.lock_ptr[k + 1]; j += kThreads)
         sh.tfl[tr.lock_idx[j]] |= TF_LOCK;  // R36
       __syncthreads();
+      // reset after the barrier: every thread has read the previous op's count (racecheck)
+      if (threadIdx.x == 0) sh.ntrans = 0;
       for (int j = 0; j < n && ok(); ++j) {
         const int u = in_at(k, j);
         const bool res = sh.tfl[u] & TF_RES;
