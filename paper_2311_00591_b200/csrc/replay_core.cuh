@@ -22,6 +22,18 @@ constexpr int kCap = 4096;       // blocks per pool held by the kernel (COOP_ERR
 constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
 constexpr int kFree = -1;
 constexpr int kSeg = 64;  // replay fast walk: stack entries per walker kept in shared memory
+constexpr int kOpChunk = 32;   // replay: trace ops whose records are staged in shared memory at once
+constexpr int kListCap = 384;  // their input / death / lock lists staged with them (else read from L2)
+
+// one trace op, staged in shared memory (replay op loop): everything the op loop reads
+struct OpRec {
+  int32_t in_beg, in_end, die_beg, die_end, lock_beg, lock_end;
+  int32_t out, src;
+  int64_t cost;
+  uint64_t out_size;
+  int32_t right;  // Alg. 1 placement side of the op (R12-R13)
+  int32_t pad;
+};
 
 // replay / pool flag validation: known bits, at most one baseline policy
 inline bool bad_flags(uint32_t f) {
@@ -164,6 +176,13 @@ struct Shared {
   // the last evicted window (read by the online calls): items, span, cost bits, victims
   int32_t win_first, win_last, nvict;
   uint64_t win_span, win_cost;
+  // replay op loop: the records and lists of the current chunk of kOpChunk ops
+  OpRec ops[kOpChunk];
+  int32_t op_base;                    // first op of the staged chunk
+  int32_t l_in0, l_die0, l_lock0;     // first list index staged for each list
+  int32_t l_in1, l_die1, l_lock1;     // one past the last staged (lists longer than kListCap: global)
+  int32_t lin[kListCap], ldie[kListCap], llock[kListCap];
+  uint8_t ldie_unev[kListCap];        // unevict flag of each staged dying tensor
   // dynamic tail: per-tensor flags TF_* (then the replay's graph and walker bitmaps)
   alignas(16) uint8_t tfl[];
 };
@@ -336,31 +355,33 @@ struct CellT {
     const int nnb = nb - removed + m;
     uint64_t ra[kPer], rz[kPer];
     int32_t ro[kPer];
+    // entries at or after the first one that moves: the new blocks, then the tail shifted
+    // by m - removed (nothing moves when the tail does not shift: those are rewritten in
+    // place with their own values)
+    const int top = (m == removed) ? lo + m : nnb;
 #pragma unroll
     for (int r = 0; r < kPer; ++r) {
       const int j = lo + r * kThreads + (int)threadIdx.x;  // new position, >= lo
-      if (j < nnb) {
-        if (j < lo + m) {
-          ra[r] = na[j - lo];
-          rz[r] = nz[j - lo];
-          ro[r] = no[j - lo];
-        } else {
-          const int src = j - m + removed;
-          ra[r] = sh.addr[src];
-          rz[r] = sh.size[src];
-          ro[r] = sh.owner[src];
-        }
+      if (j >= top) break;
+      if (j < lo + m) {
+        ra[r] = na[j - lo];
+        rz[r] = nz[j - lo];
+        ro[r] = no[j - lo];
+      } else {
+        const int src = j - m + removed;
+        ra[r] = sh.addr[src];
+        rz[r] = sh.size[src];
+        ro[r] = sh.owner[src];
       }
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kPer; ++r) {
       const int j = lo + r * kThreads + (int)threadIdx.x;
-      if (j < nnb) {
-        sh.addr[j] = ra[r];
-        sh.size[j] = rz[r];
-        sh.owner[j] = ro[r];
-      }
+      if (j >= top) break;
+      sh.addr[j] = ra[r];
+      sh.size[j] = rz[r];
+      sh.owner[j] = ro[r];
     }
     if (threadIdx.x == 0) {
       sh.nb = nnb;
@@ -965,8 +986,10 @@ struct CellT {
 
   // ---------------------------------------------------------------- Alg. 1
   __device__ void allocate(int op, int t, bool allow_inplace, int kind) {
-    const uint64_t need = tr.size[t];
-    const int src = tr.src[op];
+    allocate_with(op, t, tr.size[t], tr.src[op], goes_right(op), allow_inplace, kind);
+  }
+  // the same with the op's fields already at hand (the replay's staged op records)
+  __device__ void allocate_with(int op, int t, uint64_t need, int src, bool right, bool allow_inplace, int kind) {
     if (allow_inplace && src >= 0 && (a.flags & COOP_F_INPLACE)) {  // addr <- input.addr
       const uint64_t ad = w.taddr[src];
       const int b = block_of_addr(ad);
@@ -982,7 +1005,6 @@ struct CellT {
       __syncthreads();
       return;
     }
-    const bool right = goes_right(op);
     int i = find_fit(need, right);
     uint64_t at;
     if (i < 0) {
@@ -1108,6 +1130,57 @@ struct CellT {
     }
   }
 
+  // Stage the records of ops [k0, k0 + kOpChunk) and their lists into shared memory: two
+  // rounds of independent loads by all threads instead of a dozen dependent L2 round
+  // trips per op in the op loop.  Called by every thread; ends with a barrier.
+  __device__ void stage_ops(int k0) {
+    const int M = tr.M;
+    const int nk = min(kOpChunk, M - k0);
+    __syncthreads();  // the previous chunk is no longer read
+    for (int i = threadIdx.x; i < nk; i += kThreads) {
+      const int k = k0 + i;
+      OpRec r;
+      r.in_beg = tr.in_ptr[k];
+      r.in_end = tr.in_ptr[k + 1];
+      r.die_beg = tr.die_ptr[k];
+      r.die_end = tr.die_ptr[k + 1];
+      r.lock_beg = tr.lock_ptr[k];
+      r.lock_end = tr.lock_ptr[k + 1];
+      r.out = tr.out[k];
+      r.src = tr.src[k];
+      r.cost = tr.cost[k];
+      r.out_size = tr.size[r.out];
+      r.right = goes_right(k) ? 1 : 0;
+      r.pad = 0;
+      sh.ops[i] = r;
+    }
+    if (threadIdx.x == 0) {
+      sh.op_base = k0;
+      const int ke = k0 + nk;
+      sh.l_in0 = tr.in_ptr[k0];
+      sh.l_in1 = min(tr.in_ptr[ke], sh.l_in0 + kListCap);
+      sh.l_die0 = tr.die_ptr[k0];
+      sh.l_die1 = min(tr.die_ptr[ke], sh.l_die0 + kListCap);
+      sh.l_lock0 = tr.lock_ptr[k0];
+      sh.l_lock1 = min(tr.lock_ptr[ke], sh.l_lock0 + kListCap);
+    }
+    __syncthreads();
+    for (int j = sh.l_in0 + threadIdx.x; j < sh.l_in1; j += kThreads) sh.lin[j - sh.l_in0] = tr.in_idx[j];
+    for (int j = sh.l_die0 + threadIdx.x; j < sh.l_die1; j += kThreads) {
+      const int t = tr.die_idx[j];
+      sh.ldie[j - sh.l_die0] = t;
+      sh.ldie_unev[j - sh.l_die0] = ldg_if<kRO>(&tr.unevict[t]);
+    }
+    for (int j = sh.l_lock0 + threadIdx.x; j < sh.l_lock1; j += kThreads) sh.llock[j - sh.l_lock0] = tr.lock_idx[j];
+    __syncthreads();
+  }
+  __device__ __forceinline__ int st_in(int j) const { return j < sh.l_in1 ? sh.lin[j - sh.l_in0] : tr.in_idx[j]; }
+  __device__ __forceinline__ int st_die(int j) const { return j < sh.l_die1 ? sh.ldie[j - sh.l_die0] : tr.die_idx[j]; }
+  __device__ __forceinline__ bool st_die_unev(int j) const {
+    return j < sh.l_die1 ? sh.ldie_unev[j - sh.l_die0] : ldg_if<kRO>(&tr.unevict[tr.die_idx[j]]);
+  }
+  __device__ __forceinline__ int st_lock(int j) const { return j < sh.l_lock1 ? sh.llock[j - sh.l_lock0] : tr.lock_idx[j]; }
+
   // ---------------------------------------------------------------- the op loop
   __device__ void run(uint64_t budget) {
     const int T = tr.T, M = tr.M;
@@ -1160,40 +1233,42 @@ struct CellT {
       }
     }
     for (int k = 0; k < M && ok(); ++k) {
-      const int n = nin(k), o = tr.out[k], src = tr.src[k];
+      if (k % kOpChunk == 0) stage_ops(k);
+      const OpRec R = sh.ops[k - sh.op_base];
+      const int n = R.in_end - R.in_beg, o = R.out, src = R.src;
       if (threadIdx.x == 0) sh.cur_op = k;  // read by thread 0 only
-      for (int j = threadIdx.x; j < n; j += kThreads) atomicAdd(&w.pins[in_at(k, j)], 1);
-      for (int j = tr.lock_ptr[k] + threadIdx.x; j < tr.lock_ptr[k + 1]; j += kThreads)
-        sh.tfl[tr.lock_idx[j]] |= TF_LOCK;  // R36
+      for (int j = threadIdx.x; j < n; j += kThreads) atomicAdd(&w.pins[st_in(R.in_beg + j)], 1);
+      for (int j = R.lock_beg + threadIdx.x; j < R.lock_end; j += kThreads)
+        sh.tfl[st_lock(j)] |= TF_LOCK;  // R36
       __syncthreads();
       // reset after the barrier: every thread has read the previous op's count (racecheck)
       if (threadIdx.x == 0) sh.ntrans = 0;
       for (int j = 0; j < n && ok(); ++j) {
-        const int u = in_at(k, j);
+        const int u = st_in(R.in_beg + j);
         const bool res = sh.tfl[u] & TF_RES;
         __syncthreads();
         if (!res) materialize(u);
       }
-      for (int j = tr.lock_ptr[k]; j < tr.lock_ptr[k + 1] && ok(); ++j) {
-        const int u = tr.lock_idx[j];
+      for (int j = R.lock_beg; j < R.lock_end && ok(); ++j) {
+        const int u = st_lock(j);
         const bool res = sh.tfl[u] & TF_RES;
         __syncthreads();
         if (!res) materialize(u);
       }
       if (!ok()) break;
-      allocate(k, o, true, 1);
+      allocate_with(k, o, R.out_size, src, R.right != 0, true, 1);
       if (!ok()) break;
       if (threadIdx.x == 0) {
         sh.tfl[o] |= TF_BORN;
-        sh.clock += tr.cost[k];
-        sh.res.base_us += tr.cost[k];
-        sh.res.total_us += tr.cost[k];
+        sh.clock += R.cost;
+        sh.res.base_us += R.cost;
+        sh.res.total_us += R.cost;
         log_ev(6, k, o, w.taddr[o]);
       }
       __syncthreads();
       const int64_t clk = sh.clock;
       for (int j = threadIdx.x; j < n; j += kThreads) {
-        const int u = in_at(k, j);
+        const int u = st_in(R.in_beg + j);
         w.last_access[u] = clk;
         atomicSub(&w.pins[u], 1);
       }
@@ -1201,7 +1276,7 @@ struct CellT {
       __syncthreads();
       // deaths after op k (R20) merged with transient dead recomputes (R22), ascending id
       if (threadIdx.x == 0) {
-        for (int j = tr.die_ptr[k]; j < tr.die_ptr[k + 1]; ++j) sh.tfl[tr.die_idx[j]] |= TF_DEAD;
+        for (int j = R.die_beg; j < R.die_end; ++j) sh.tfl[st_die(j)] |= TF_DEAD;
         // insertion-sort the transient list (small) and merge with the (sorted) die list
         int *tl = w.trans;
         const int nt = sh.ntrans;
@@ -1214,19 +1289,25 @@ struct CellT {
       }
       __syncthreads();
       {
-        int pd = tr.die_ptr[k];
-        const int pe = tr.die_ptr[k + 1];
+        int pd = R.die_beg;
+        const int pe = R.die_end;
         int pt = 0;
         const int nt = sh.ntrans;
         int last = -1;
         while (pd < pe || pt < nt) {
           int t;
-          if (pt >= nt || (pd < pe && tr.die_idx[pd] <= w.trans[pt])) t = tr.die_idx[pd++];
-          else t = w.trans[pt++];
+          bool unev;
+          if (pt >= nt || (pd < pe && st_die(pd) <= w.trans[pt])) {
+            unev = st_die_unev(pd);
+            t = st_die(pd++);
+          } else {
+            t = w.trans[pt++];
+            unev = ldg_if<kRO>(&tr.unevict[t]);
+          }
           if (t == last) continue;
           last = t;
           const uint8_t f = sh.tfl[t];
-          const bool keep = tr.unevict[t] && t != src;
+          const bool keep = unev && t != src;
           __syncthreads();
           if ((f & TF_DEAD) && (f & TF_RES) && !keep) free_tensor(t);
         }
