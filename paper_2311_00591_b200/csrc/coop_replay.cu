@@ -442,7 +442,7 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   const char *wenv = getenv("COOP_REPLAY_WALK");  // profiling hook: "generic" disables the fast walk
   const char *genv = getenv("COOP_REPLAY_GSMEM");  // profiling hook: "0" keeps the graph in global memory
   if (!t->cg.empty() && !(wenv && wenv[0] == 'g')) {
-    const size_t per = (size_t)vis_words * 4 + kSeg * 2;  // bitmap + shared stack segment
+    const size_t per = (size_t)vis_words * 4;  // one visited bitmap per walker
     if (!(genv && genv[0] == '0') && base + (size_t)g_bytes + 32 * per <= (size_t)max_smem) {
       g_smem = 1;
       walkers = (int)std::min<size_t>(kThreads, ((size_t)max_smem - base - g_bytes) / per);
@@ -451,7 +451,7 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
     }
     walkers = walkers / 32 * 32;  // whole warps
   }
-  const size_t smem = base + (g_smem ? (size_t)g_bytes : 0) + (size_t)walkers * ((size_t)vis_words * 4 + kSeg * 2);
+  const size_t smem = base + (g_smem ? (size_t)g_bytes : 0) + (size_t)walkers * vis_words * 4;
   if (cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return COOP_ERR_CUDA;
   int per_sm = 1;

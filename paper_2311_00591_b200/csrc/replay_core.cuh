@@ -21,7 +21,6 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kCap = 4096;       // blocks per pool held by the kernel (COOP_ERR_NOMEM beyond)
 constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
 constexpr int kFree = -1;
-constexpr int kSeg = 64;  // replay fast walk: stack entries per walker kept in shared memory
 constexpr int kOpChunk = 32;   // replay: trace ops whose records are staged in shared memory at once
 constexpr int kListCap = 384;  // their input / death / lock lists staged with them (else read from L2)
 
@@ -266,7 +265,6 @@ struct CellT {
   const int32_t *gc;
   const uint16_t *gip, *gcp, *gii, *gco;
   uint32_t *vis;
-  uint16_t *seg;  // the bottom kSeg entries of this walker's DFS stack (shared memory)
 
   __device__ CellT(const KArgs &a_, Shared &sh_, int cell_) : a(a_), tr(a_.tr), sh(sh_), cell(cell_) {
     unsigned char *base = a.ws + (size_t)blockIdx.x * a.lay.bytes;  // this CTA's slot
@@ -294,7 +292,6 @@ struct CellT {
     gc = nullptr;
     gip = gcp = gii = gco = nullptr;
     vis = nullptr;
-    seg = nullptr;
     if (kRO && a.walkers > 0) {
       size_t off[6];
       cg_offsets(tr.T, tr.cg_nnz, off);
@@ -307,9 +304,7 @@ struct CellT {
       gco = reinterpret_cast<const uint16_t *>(g + off[4]);
       vis = reinterpret_cast<uint32_t *>(tail + (a.g_smem ? a.g_bytes : 0)) +
             (size_t)threadIdx.x * a.vis_words;
-      seg = reinterpret_cast<uint16_t *>(tail + (a.g_smem ? a.g_bytes : 0) +
-                                         (size_t)a.walkers * a.vis_words * 4) +
-            (size_t)threadIdx.x * kSeg;
+
     }
   }
 
@@ -505,8 +500,7 @@ struct CellT {
     if ((int)threadIdx.x < a.walkers) {
       uint32_t *mk = vis;
       const int VW = a.vis_words;
-      int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;  // entries beyond kSeg (global)
-      uint16_t *sg = seg;
+      int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
       const int nitems = 2 * ncand;
       int sp = 0, it = -1, stage = 0;
       int64_t acc = 0;
@@ -517,9 +511,7 @@ struct CellT {
         const uint32_t bit = 1u << (y & 31);
         if (el && !(mk[y >> 5] & bit)) {
           mk[y >> 5] |= bit;
-          if (sp < kSeg) sg[sp] = (uint16_t)y;
-          else stk[sp - kSeg] = y;
-          ++sp;
+          stk[sp++] = y;
         }
       };
       auto expand = [&](int x) {
@@ -546,8 +538,7 @@ struct CellT {
           expand(t);  // roots: t's producer's inputs / its consumers' outputs
           continue;
         }
-        --sp;
-        const int x = sp < kSeg ? (int)sg[sp] : stk[sp - kSeg];
+        const int x = stk[--sp];
         const int32_t cx = gc[x];
         // ancestors: non-resident (pushed so) and recomputable; descendants: evicted and
         // live (pushed so)

@@ -16,7 +16,7 @@ for r in rows:
     tot[name] += ms
     cnt[name] += 1
 all_ms = sum(tot.values())
-lines = ["# round 1 launch list (ncu --metrics gpu__time_duration.sum --clock-control none) of:",
+lines = ["# launch list (ncu --metrics gpu__time_duration.sum --clock-control none) of:",
          f"#   {cmd}",
          "# cold-cache, serialised per-launch times: compare shares, not absolutes",
          f"{'kernel':70s} {'launches':>8s} {'total ms':>10s} {'share':>7s}"]
