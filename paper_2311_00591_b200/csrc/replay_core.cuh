@@ -151,7 +151,7 @@ struct Shared {
   // the pool's address-ordered block table (single buffer; splices shift in place)
   uint64_t addr[kCap + 2];
   uint64_t size[kCap + 2];
-  int32_t owner[kCap + 2];
+  int16_t owner[kCap + 2];  // tensor id (< kMaxT = 16384) or kFree
   uint64_t wS[kWarps];
   U192 wH[kWarps];
   int32_t wB[kWarps];
@@ -313,7 +313,7 @@ struct CellT {
   __device__ __forceinline__ int in_at(int op, int j) const { return tr.in_idx[tr.in_ptr[op] + j]; }
   __device__ __forceinline__ uint64_t *A() { return sh.addr; }
   __device__ __forceinline__ uint64_t *Z() { return sh.size; }
-  __device__ __forceinline__ int32_t *O() { return sh.owner; }
+  __device__ __forceinline__ int16_t *O() { return sh.owner; }
 
   __device__ void log_ev(int kind, int op, int t, uint64_t addr) {  // thread 0 only
     const int64_t i = sh.res.n_events++;
@@ -376,7 +376,7 @@ struct CellT {
       if (j >= top) break;
       sh.addr[j] = ra[r];
       sh.size[j] = rz[r];
-      sh.owner[j] = ro[r];
+      sh.owner[j] = (int16_t)ro[r];
     }
     if (threadIdx.x == 0) {
       sh.nb = nnb;
