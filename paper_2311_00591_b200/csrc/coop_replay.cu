@@ -38,6 +38,11 @@ __global__ void __launch_bounds__(kThreads, 1) replay_kernel(const KArgs a) {
     for (int i = threadIdx.x; i < a.g_bytes / 16; i += kThreads) dst[i] = __ldg(src + i);
     __syncthreads();
   }
+  if (a.warp_bfs) {  // the warps' visited bitmaps start (and stay, between items) all zero
+    uint32_t *v = reinterpret_cast<uint32_t *>(sh.tfl + a.tfl_bytes + (a.g_smem ? a.g_bytes : 0));
+    for (int i = threadIdx.x; i < kWarps * a.vis_words; i += kThreads) v[i] = 0u;
+    __syncthreads();
+  }
   for (int cell = blockIdx.x; cell < a.n_cells; cell += gridDim.x) {
     CellT<true> c(a, sh, cell);
     c.run(a.budgets[cell]);
@@ -437,21 +442,38 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   const int tfl_bytes = (t->T + 15) / 16 * 16;
   const int vis_words = (t->T + 127) / 128 * 4;
   const size_t base = sizeof(Shared) + (size_t)tfl_bytes;
-  int g_smem = 0, walkers = 0;
+  int g_smem = 0, walkers = 0, warp_bfs = 0;
   const int g_bytes = (int)t->cg.size();
-  const char *wenv = getenv("COOP_REPLAY_WALK");  // profiling hook: "generic" disables the fast walk
-  const char *genv = getenv("COOP_REPLAY_GSMEM");  // profiling hook: "0" keeps the graph in global memory
+  // profiling hooks: COOP_REPLAY_WALK = "generic" (round 1's per-thread walk over the global
+  // graph), "lane" (per-thread walkers with shared-memory bitmaps), "warp" (one closure per
+  // warp, edge-parallel BFS); COOP_REPLAY_GSMEM=0 keeps the compact graph in global memory.
+  // Default: per-thread walkers when at least 128 of them fit, else the warp BFS (large T:
+  // few bitmaps fit, and those traces -- BiLSTM, GPT-3 -- have long closures).
+  const char *wenv = getenv("COOP_REPLAY_WALK");
+  const char *genv = getenv("COOP_REPLAY_GSMEM");
+  const bool gsm_ok = !(genv && genv[0] == '0');
+  const size_t warp_extra = (size_t)kWarps * ((size_t)vis_words * 4 + (size_t)kRing * 2);
   if (!t->cg.empty() && !(wenv && wenv[0] == 'g')) {
     const size_t per = (size_t)vis_words * 4;  // one visited bitmap per walker
-    if (!(genv && genv[0] == '0') && base + (size_t)g_bytes + 32 * per <= (size_t)max_smem) {
+    if (gsm_ok && base + (size_t)g_bytes + 32 * per <= (size_t)max_smem) {
       g_smem = 1;
       walkers = (int)std::min<size_t>(kThreads, ((size_t)max_smem - base - g_bytes) / per);
     } else if (base + 32 * per <= (size_t)max_smem) {
       walkers = (int)std::min<size_t>(kThreads, ((size_t)max_smem - base) / per);
     }
     walkers = walkers / 32 * 32;  // whole warps
+    const bool want_warp = wenv ? wenv[0] == 'w' : walkers < 128;
+    if (want_warp) {
+      const int gs = gsm_ok && base + (size_t)g_bytes + warp_extra <= (size_t)max_smem;
+      if (gs || base + warp_extra <= (size_t)max_smem) {
+        g_smem = gs;
+        walkers = kThreads;
+        warp_bfs = 1;
+      }
+    }
   }
-  const size_t smem = base + (g_smem ? (size_t)g_bytes : 0) + (size_t)walkers * vis_words * 4;
+  const size_t smem = base + (g_smem ? (size_t)g_bytes : 0) +
+                      (warp_bfs ? warp_extra : (size_t)walkers * vis_words * 4);
   if (cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return COOP_ERR_CUDA;
   int per_sm = 1;
@@ -490,6 +512,7 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   a.g_smem = g_smem;
   a.g_bytes = g_bytes;
   a.walkers = walkers;
+  a.warp_bfs = warp_bfs;
   a.vis_words = vis_words;
   {  // profiling hook: COOP_REPLAY_PHASES=1 accumulates per-phase pressure-event times per cell
     static int64_t *pbuf = nullptr;

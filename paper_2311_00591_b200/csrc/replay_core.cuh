@@ -23,6 +23,7 @@ constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
 constexpr int kFree = -1;
 constexpr int kOpChunk = 32;   // replay: trace ops whose records are staged in shared memory at once
 constexpr int kListCap = 384;  // their input / death / lock lists staged with them (else read from L2)
+constexpr int kRing = 2048;    // replay warp BFS: per-warp queue ring (uint16 entries, shared memory)
 
 // one trace op, staged in shared memory (replay op loop): everything the op loop reads
 struct OpRec {
@@ -134,6 +135,7 @@ struct KArgs {
   int32_t g_smem;     // the compact graph is copied into shared memory
   int32_t g_bytes;    // its size (16-byte multiple)
   int32_t walkers;    // threads [0, walkers) walk closures (fast path); 0 = generic walk
+  int32_t warp_bfs;   // fast path by whole warps: one closure per warp, edge-parallel BFS
   int32_t vis_words;  // bitmap words per walker (ceil(T / 32), rounded to 4)
   // coop_replay_snapshots: the item view of every Coop pressure event (one cell), as rows
   // of a batched-search table (stride snap_n), plus the request and the evicted window
@@ -265,6 +267,7 @@ struct CellT {
   const int32_t *gc;
   const uint16_t *gip, *gcp, *gii, *gco;
   uint32_t *vis;
+  uint16_t *ring;  // warp BFS: this warp's queue ring
 
   __device__ CellT(const KArgs &a_, Shared &sh_, int cell_) : a(a_), tr(a_.tr), sh(sh_), cell(cell_) {
     unsigned char *base = a.ws + (size_t)blockIdx.x * a.lay.bytes;  // this CTA's slot
@@ -292,6 +295,7 @@ struct CellT {
     gc = nullptr;
     gip = gcp = gii = gco = nullptr;
     vis = nullptr;
+    ring = nullptr;
     if (kRO && a.walkers > 0) {
       size_t off[6];
       cg_offsets(tr.T, tr.cg_nnz, off);
@@ -302,8 +306,14 @@ struct CellT {
       gcp = reinterpret_cast<const uint16_t *>(g + off[2]);
       gii = reinterpret_cast<const uint16_t *>(g + off[3]);
       gco = reinterpret_cast<const uint16_t *>(g + off[4]);
-      vis = reinterpret_cast<uint32_t *>(tail + (a.g_smem ? a.g_bytes : 0)) +
-            (size_t)threadIdx.x * a.vis_words;
+      if (a.warp_bfs) {  // one bitmap per warp, then one queue ring per warp
+        unsigned char *vb = tail + (a.g_smem ? a.g_bytes : 0);
+        vis = reinterpret_cast<uint32_t *>(vb) + (size_t)(threadIdx.x >> 5) * a.vis_words;
+        ring = reinterpret_cast<uint16_t *>(vb + (size_t)kWarps * a.vis_words * 4) + (size_t)(threadIdx.x >> 5) * kRing;
+      } else {
+        vis = reinterpret_cast<uint32_t *>(tail + (a.g_smem ? a.g_bytes : 0)) +
+              (size_t)threadIdx.x * a.vis_words;
+      }
 
     }
   }
@@ -549,9 +559,141 @@ struct CellT {
     }
   }
 
+  // The same sums with a whole WARP per work item: an edge-parallel breadth-first walk
+  // over the warp's queue ring (shared memory) with one visited bitmap per warp (test-and-set
+  // by atomicOr: two lanes may reach the same node in one step).  Every lane of every warp
+  // works -- the per-thread walk keeps only the walkers whose bitmaps fit busy and its lanes
+  // diverge (9 threads per executed instruction on BiLSTM) -- and a long chain of evicted
+  // tensors costs one queue step per BFS level instead of a serial pop per node.  A warp
+  // whose ring would overflow redoes that item with the per-thread DFS on lane 0.
+  __device__ void closures_warp(const int32_t *cand, int ncand) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t *mk = vis;  // all zero between items
+    uint16_t *q = ring;
+    const int VW = a.vis_words;
+    const int nitems = 2 * ncand;
+    while (true) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(&sh.cand_next, 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= nitems) break;
+      const int t = O()[cand[it >> 1]];
+      const int stage = it & 1;
+      const uint16_t *lst = stage == 0 ? gii : gco;
+      const uint16_t *ptr = stage == 0 ? gip : gcp;
+      int64_t acc = 0;
+      int head = 0, tail = 0;
+      bool ovf = false;
+      if (lane == 0) mk[t >> 5] |= 1u << (t & 31);
+      __syncwarp();
+      // expand the edges [b, e) of the lane's node (d = e - b, 0 for none), all lanes' edges
+      // spread over the warp; new eligible nodes are appended to the ring
+      auto expand_batch = [&](int b, int d) {
+        int off = d;  // inclusive scan of the degrees
+#pragma unroll
+        for (int k = 1; k < 32; k <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, off, k);
+          if (lane >= k) off += o;
+        }
+        const int D = __shfl_sync(0xffffffffu, off, 31);
+        const int ex = off - d;  // exclusive
+        for (int k0 = 0; k0 < D; k0 += 32) {
+          const int k = k0 + lane;
+          // owner lane of edge k: the last lane whose exclusive offset is <= k (binary search
+          // over the lanes' offsets by shuffles, executed by every lane); a lane with no
+          // edges shares its offset with the next lane, so the last one always has edges
+          int lo = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int cl = lo + step;
+            const int exo = __shfl_sync(0xffffffffu, ex, cl & 31);
+            if (cl < 32 && exo <= k) lo = cl;
+          }
+          const int bo = __shfl_sync(0xffffffffu, b, lo), exo = __shfl_sync(0xffffffffu, ex, lo);
+          bool nw = false;
+          int y = 0;
+          if (k < D) {
+            y = lst[bo + (k - exo)];
+            const uint8_t f = sh.tfl[y];
+            const bool el = stage == 0 ? !(f & TF_RES) : ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD));
+            if (el) {
+              const uint32_t bit = 1u << (y & 31);
+              nw = !(mk[y >> 5] & bit) && !(atomicOr(&mk[y >> 5], bit) & bit);
+            }
+          }
+          const uint32_t bal = __ballot_sync(0xffffffffu, nw);
+          if (tail - head + __popc(bal) > kRing) ovf = true;
+          else if (nw) q[(tail + __popc(bal & lt)) & (kRing - 1)] = (uint16_t)y;
+          tail += __popc(bal);
+        }
+      };
+      {  // roots: t's producer's inputs / its consumers' outputs
+        const int b = lane == 0 ? ptr[t] : 0, e = lane == 0 ? ptr[t + 1] : 0;
+        expand_batch(b, e - b);
+      }
+      __syncwarp();
+      while (head < tail && !__any_sync(0xffffffffu, ovf)) {
+        const int n = min(32, tail - head);
+        int b = 0, d = 0;
+        if (lane < n) {
+          const int x = q[(head + lane) & (kRing - 1)];
+          const int32_t cx = gc[x];
+          // ancestors: non-resident (queued so) and recomputable; descendants: evicted and
+          // live (queued so)
+          if (!(stage == 0 && cx < 0)) {
+            acc += cx;
+            b = ptr[x];
+            d = ptr[x + 1] - b;
+          }
+        }
+        head += n;
+        __syncwarp();
+        expand_batch(b, d);
+        __syncwarp();
+      }
+      const bool overflow = __any_sync(0xffffffffu, ovf);
+#pragma unroll
+      for (int k = 16; k > 0; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
+      // clear the bitmap (warp-parallel)
+      for (int k = lane; k < VW; k += 32) mk[k] = 0u;
+      __syncwarp();
+      if (overflow) {  // a frontier wider than the ring: redo this item depth-first on lane 0
+        if (lane == 0) {
+          int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
+          int sp = 0;
+          acc = 0;
+          mk[t >> 5] |= 1u << (t & 31);
+          auto push = [&](int y) {
+            const uint8_t f = sh.tfl[y];
+            const bool el = stage == 0 ? !(f & TF_RES) : ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD));
+            const uint32_t bit = 1u << (y & 31);
+            if (el && !(mk[y >> 5] & bit)) {
+              mk[y >> 5] |= bit;
+              stk[sp++] = y;
+            }
+          };
+          for (int j = ptr[t]; j < ptr[t + 1]; ++j) push(lst[j]);
+          while (sp > 0) {
+            const int x = stk[--sp];
+            const int32_t cx = gc[x];
+            if (stage == 0 && cx < 0) continue;
+            acc += cx;
+            for (int j = ptr[x]; j < ptr[x + 1]; ++j) push(lst[j]);
+          }
+        }
+        __syncwarp();
+        for (int k = lane; k < VW; k += 32) mk[k] = 0u;
+        __syncwarp();
+      }
+      if (lane == 0) w.pacc[it] = acc;
+    }
+  }
+
   __device__ void projected_costs(const int32_t *cand, int ncand, int pol = 0) {
     if (kRO && a.walkers > 0) {
-      closures_fast(cand, ncand);
+      if (a.warp_bfs) closures_warp(cand, ncand);
+      else closures_fast(cand, ncand);
       finish_costs(cand, ncand, pol);
       return;
     }

@@ -156,3 +156,21 @@ def test_dead_diamond_gpu(n):
     tr = TR.dead_diamond_trace(n)
     res = check(tr, [3 * n + 5, 3 * n + 8], 0, log_cap=1000, ctx="dead_diamond")
     assert int(res[0]["remat"]) == 3 * n + 2
+
+
+@pytest.mark.parametrize("walk", ["warp", "lane", "generic"])
+def test_closure_walk_variants(walk, monkeypatch):
+    """Every projected-cost walk of the replay engine (the warp BFS,
+    the per-thread walk over the shared-memory graph, round 1's generic walk) is bit-exact
+    with O2 on thrashing DNN cells and random traces."""
+    monkeypatch.setenv("COOP_REPLAY_WALK", walk)
+    for name, fracs in (("bilstm", (0.3,)), ("gpt3_2.7b", (0.45,)), ("inception_v3", (0.3,)), ("unet", (0.45,))):
+        tr = dnn.dnn(name)
+        flags = coop.F_PARTITION | coop.F_INPLACE
+        peak = O.peak_live(tr, flags)
+        check(tr, [int(peak * f) for f in fracs], flags, ctx=f"{walk} {name}")
+    rng = np.random.default_rng(42)
+    for _ in range(6):
+        tr = TR.random_trace(rng, n_params=2, n_fwd=10, iters=2, inplace_p=0.25)
+        peak = O.peak_live(tr, 3)
+        check(tr, [max(1, int(peak * 0.5)), max(1, int(peak * 0.7))], 3, log_cap=2000, ctx=f"{walk} random")
