@@ -38,9 +38,10 @@ __global__ void __launch_bounds__(kThreads, 1) replay_kernel(const KArgs a) {
     for (int i = threadIdx.x; i < a.g_bytes / 16; i += kThreads) dst[i] = __ldg(src + i);
     __syncthreads();
   }
-  if (a.warp_bfs) {  // the warps' visited bitmaps start (and stay, between items) all zero
+  if (a.warp_bfs) {  // the warps' / groups' visited bitmaps start (and stay, between items) all zero
     uint32_t *v = reinterpret_cast<uint32_t *>(sh.tfl + a.tfl_bytes + (a.g_smem ? a.g_bytes : 0));
-    for (int i = threadIdx.x; i < kWarps * a.vis_words; i += kThreads) v[i] = 0u;
+    const int nbm = a.warp_bfs == 2 ? kGroups : kWarps;
+    for (int i = threadIdx.x; i < nbm * a.vis_words; i += kThreads) v[i] = 0u;
     __syncthreads();
   }
   for (int cell = blockIdx.x; cell < a.n_cells; cell += gridDim.x) {
@@ -453,6 +454,7 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   const char *genv = getenv("COOP_REPLAY_GSMEM");
   const bool gsm_ok = !(genv && genv[0] == '0');
   const size_t warp_extra = (size_t)kWarps * ((size_t)vis_words * 4 + (size_t)kRing * 2);
+  const size_t group_extra = (size_t)kGroups * ((size_t)vis_words * 4 + (size_t)kGRing * 2);
   if (!t->cg.empty() && !(wenv && wenv[0] == 'g')) {
     const size_t per = (size_t)vis_words * 4;  // one visited bitmap per walker
     if (gsm_ok && base + (size_t)g_bytes + 32 * per <= (size_t)max_smem) {
@@ -462,7 +464,16 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
       walkers = (int)std::min<size_t>(kThreads, ((size_t)max_smem - base) / per);
     }
     walkers = walkers / 32 * 32;  // whole warps
-    const bool want_warp = wenv ? wenv[0] == 'w' : walkers < 128;
+    const bool want_group = wenv ? wenv[0] == 'G' : walkers < 128;
+    const bool want_warp = wenv ? wenv[0] == 'w' : false;
+    if (want_group) {
+      const int gs = gsm_ok && base + (size_t)g_bytes + group_extra <= (size_t)max_smem;
+      if (gs || base + group_extra <= (size_t)max_smem) {
+        g_smem = gs;
+        walkers = kThreads;
+        warp_bfs = 2;
+      }
+    }
     if (want_warp) {
       const int gs = gsm_ok && base + (size_t)g_bytes + warp_extra <= (size_t)max_smem;
       if (gs || base + warp_extra <= (size_t)max_smem) {
@@ -473,7 +484,7 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
     }
   }
   const size_t smem = base + (g_smem ? (size_t)g_bytes : 0) +
-                      (warp_bfs ? warp_extra : (size_t)walkers * vis_words * 4);
+                      (warp_bfs == 2 ? group_extra : warp_bfs ? warp_extra : (size_t)walkers * vis_words * 4);
   if (cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return COOP_ERR_CUDA;
   int per_sm = 1;

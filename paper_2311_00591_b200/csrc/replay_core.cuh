@@ -24,6 +24,9 @@ constexpr int kFree = -1;
 constexpr int kOpChunk = 32;   // replay: trace ops whose records are staged in shared memory at once
 constexpr int kListCap = 384;  // their input / death / lock lists staged with them (else read from L2)
 constexpr int kRing = 2048;    // replay warp BFS: per-warp queue ring (uint16 entries, shared memory)
+constexpr int kGL = 8;         // replay group BFS: lanes per group (4 groups per warp)
+constexpr int kGroups = kThreads / kGL;
+constexpr int kGRing = 256;    // replay group BFS: per-group queue ring
 
 // one trace op, staged in shared memory (replay op loop): everything the op loop reads
 struct OpRec {
@@ -135,7 +138,8 @@ struct KArgs {
   int32_t g_smem;     // the compact graph is copied into shared memory
   int32_t g_bytes;    // its size (16-byte multiple)
   int32_t walkers;    // threads [0, walkers) walk closures (fast path); 0 = generic walk
-  int32_t warp_bfs;   // fast path by whole warps: one closure per warp, edge-parallel BFS
+  int32_t warp_bfs;   // fast path by whole warps (1) or by 8-lane groups (2): one closure per
+                      // warp / group, edge-parallel BFS
   int32_t vis_words;  // bitmap words per walker (ceil(T / 32), rounded to 4)
   // coop_replay_snapshots: the item view of every Coop pressure event (one cell), as rows
   // of a batched-search table (stride snap_n), plus the request and the evicted window
@@ -306,7 +310,11 @@ struct CellT {
       gcp = reinterpret_cast<const uint16_t *>(g + off[2]);
       gii = reinterpret_cast<const uint16_t *>(g + off[3]);
       gco = reinterpret_cast<const uint16_t *>(g + off[4]);
-      if (a.warp_bfs) {  // one bitmap per warp, then one queue ring per warp
+      if (a.warp_bfs == 2) {  // one bitmap per 8-lane group, then one queue ring per group
+        unsigned char *vb = tail + (a.g_smem ? a.g_bytes : 0);
+        vis = reinterpret_cast<uint32_t *>(vb) + (size_t)(threadIdx.x / kGL) * a.vis_words;
+        ring = reinterpret_cast<uint16_t *>(vb + (size_t)kGroups * a.vis_words * 4) + (size_t)(threadIdx.x / kGL) * kGRing;
+      } else if (a.warp_bfs) {  // one bitmap per warp, then one queue ring per warp
         unsigned char *vb = tail + (a.g_smem ? a.g_bytes : 0);
         vis = reinterpret_cast<uint32_t *>(vb) + (size_t)(threadIdx.x >> 5) * a.vis_words;
         ring = reinterpret_cast<uint16_t *>(vb + (size_t)kWarps * a.vis_words * 4) + (size_t)(threadIdx.x >> 5) * kRing;
@@ -690,9 +698,142 @@ struct CellT {
     }
   }
 
+  // The warp BFS with four independent 8-lane groups per warp: a BiLSTM closure's frontier
+  // is 2-4 nodes wide, so 8 lanes keep most of the edge parallelism while 32 closures are
+  // walked at once per CTA instead of 8.  One flat loop per group: every iteration either
+  // starts the group's next work item (seeding its queue with the roots) or expands one
+  // batch of up to 8 queued nodes edge-parallel, so the groups of a warp stay converged.
+  __device__ void closures_group(const int32_t *cand, int ncand) {
+    const int lane = threadIdx.x & 31, gl = lane & (kGL - 1);
+    const int gbase = lane & ~(kGL - 1);
+    const uint32_t gmask = 0xffu << gbase;
+    const unsigned glt = (1u << gl) - 1u;
+    uint32_t *mk = vis;  // all zero between items
+    uint16_t *q = ring;
+    const int VW = a.vis_words;
+    const int nitems = 2 * ncand;
+    int it = -1, t = 0, stage = 0, head = 0, tail = 0;
+    bool live = false, ovf = false;
+    int64_t acc = 0;
+    const uint16_t *lst = gii, *ptr = gip;
+    // expand the edges [b, b + d) of each lane's node, spread over the group's lanes
+    auto expand_batch = [&](int b, int d) {
+      int off = d;
+#pragma unroll
+      for (int k = 1; k < kGL; k <<= 1) {
+        const int o = __shfl_up_sync(gmask, off, k, kGL);
+        if (gl >= k) off += o;
+      }
+      const int D = __shfl_sync(gmask, off, kGL - 1, kGL);
+      const int ex = off - d;
+      for (int k0 = 0; k0 < D; k0 += kGL) {
+        const int k = k0 + gl;
+        int lo = 0;
+#pragma unroll
+        for (int step = kGL / 2; step > 0; step >>= 1) {
+          const int cl = lo + step;
+          const int exo = __shfl_sync(gmask, ex, cl & (kGL - 1), kGL);
+          if (cl < kGL && exo <= k) lo = cl;
+        }
+        const int bo = __shfl_sync(gmask, b, lo, kGL), exo = __shfl_sync(gmask, ex, lo, kGL);
+        bool nw = false;
+        int y = 0;
+        if (k < D) {
+          y = lst[bo + (k - exo)];
+          const uint8_t f = sh.tfl[y];
+          const bool el = stage == 0 ? !(f & TF_RES) : ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD));
+          if (el) {
+            const uint32_t bit = 1u << (y & 31);
+            nw = !(mk[y >> 5] & bit) && !(atomicOr(&mk[y >> 5], bit) & bit);
+          }
+        }
+        const uint32_t bal = (__ballot_sync(gmask, nw) >> gbase) & 0xffu;
+        if (tail - head + __popc(bal) > kGRing) ovf = true;
+        else if (nw) q[(tail + __popc(bal & glt)) & (kGRing - 1)] = (uint16_t)y;
+        tail += __popc(bal);
+      }
+    };
+    while (true) {
+      if (!live) {
+        if (it >= 0) {  // finish the previous item
+#pragma unroll
+          for (int k = kGL / 2; k > 0; k >>= 1) acc += __shfl_xor_sync(gmask, acc, k, kGL);
+          for (int k = gl; k < VW; k += kGL) mk[k] = 0u;
+          __syncwarp(gmask);
+          if (ovf) {  // a frontier wider than the ring: redo the item depth-first on one lane
+            if (gl == 0) {
+              int32_t *stk = w.stack + (size_t)threadIdx.x * tr.T;
+              int sp = 0;
+              acc = 0;
+              mk[t >> 5] |= 1u << (t & 31);
+              auto push = [&](int y) {
+                const uint8_t f = sh.tfl[y];
+                const bool el = stage == 0 ? !(f & TF_RES) : ((f & TF_BORN) && !(f & TF_RES) && !(f & TF_DEAD));
+                const uint32_t bit = 1u << (y & 31);
+                if (el && !(mk[y >> 5] & bit)) {
+                  mk[y >> 5] |= bit;
+                  stk[sp++] = y;
+                }
+              };
+              for (int j = ptr[t]; j < ptr[t + 1]; ++j) push(lst[j]);
+              while (sp > 0) {
+                const int x = stk[--sp];
+                const int32_t cx = gc[x];
+                if (stage == 0 && cx < 0) continue;
+                acc += cx;
+                for (int j = ptr[x]; j < ptr[x + 1]; ++j) push(lst[j]);
+              }
+            }
+            __syncwarp(gmask);
+            for (int k = gl; k < VW; k += kGL) mk[k] = 0u;
+            __syncwarp(gmask);
+          }
+          if (gl == 0) w.pacc[it] = acc;
+        }
+        int nit = 0;
+        if (gl == 0) nit = atomicAdd(&sh.cand_next, 1);
+        it = __shfl_sync(gmask, nit, 0, kGL);
+        if (it >= nitems) break;
+        t = O()[cand[it >> 1]];
+        stage = it & 1;
+        lst = stage == 0 ? gii : gco;
+        ptr = stage == 0 ? gip : gcp;
+        acc = 0;
+        head = tail = 0;
+        ovf = false;
+        if (gl == 0) mk[t >> 5] |= 1u << (t & 31);
+        __syncwarp(gmask);
+        const int b = gl == 0 ? ptr[t] : 0, e = gl == 0 ? ptr[t + 1] : 0;
+        expand_batch(b, e - b);  // roots: t's producer's inputs / its consumers' outputs
+        __syncwarp(gmask);
+        live = head < tail && !ovf;
+        continue;
+      }
+      const int n = min(kGL, tail - head);
+      int b = 0, d = 0;
+      if (gl < n) {
+        const int x = q[(head + gl) & (kGRing - 1)];
+        const int32_t cx = gc[x];
+        // ancestors: non-resident (queued so) and recomputable; descendants: evicted and
+        // live (queued so)
+        if (!(stage == 0 && cx < 0)) {
+          acc += cx;
+          b = ptr[x];
+          d = ptr[x + 1] - b;
+        }
+      }
+      head += n;
+      __syncwarp(gmask);
+      expand_batch(b, d);
+      __syncwarp(gmask);
+      live = head < tail && !ovf;
+    }
+  }
+
   __device__ void projected_costs(const int32_t *cand, int ncand, int pol = 0) {
     if (kRO && a.walkers > 0) {
-      if (a.warp_bfs) closures_warp(cand, ncand);
+      if (a.warp_bfs == 2) closures_group(cand, ncand);
+      else if (a.warp_bfs) closures_warp(cand, ncand);
       else closures_fast(cand, ncand);
       finish_costs(cand, ncand, pol);
       return;

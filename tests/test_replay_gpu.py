@@ -158,7 +158,7 @@ def test_dead_diamond_gpu(n):
     assert int(res[0]["remat"]) == 3 * n + 2
 
 
-@pytest.mark.parametrize("walk", ["warp", "lane", "generic"])
+@pytest.mark.parametrize("walk", ["Group", "warp", "lane", "generic"])
 def test_closure_walk_variants(walk, monkeypatch):
     """Every projected-cost walk of the replay engine (the warp BFS,
     the per-thread walk over the shared-memory graph, round 1's generic walk) is bit-exact
