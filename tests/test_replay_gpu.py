@@ -174,3 +174,20 @@ def test_closure_walk_variants(walk, monkeypatch):
         tr = TR.random_trace(rng, n_params=2, n_fwd=10, iters=2, inplace_p=0.25)
         peak = O.peak_live(tr, 3)
         check(tr, [max(1, int(peak * 0.5)), max(1, int(peak * 0.7))], 3, log_cap=2000, ctx=f"{walk} random")
+
+
+def test_r37_block_capacity_nomem():
+    """DESIGN.md R37: the replay kernel holds at most 4096 blocks per pool in shared memory;
+    a pool that needs more ends with COOP_ERR_NOMEM at the op that would exceed it (the
+    oracle's own limit is the search's 8192, so it completes).  4200 one-byte tensors stay
+    live until a final op reads them all."""
+    b = TR.Builder("many_blocks")
+    xs = [b.op([], 1, 1) for _ in range(4200)]
+    b.op(xs, 1, 1)
+    tr = b.build()
+    budget = 100000
+    res, _ = coop.Trace(tr).replay([budget], 0)
+    assert int(res[0]["status"]) == coop.ERR_NOMEM
+    assert int(res[0]["max_blocks"]) <= 4096
+    want, _ = O.replay(tr, budget, 0)
+    assert int(want["status"]) == O.OK

@@ -1,5 +1,5 @@
 """Map an ncu SASS source-page CSV onto CUDA source lines via nvdisasm -g line info.
-usage: sass_lines.py <ncu_sass.csv> <lib.so> <kernel-substring> [top]"""
+usage: [SORT=stall] sass_lines.py <ncu_sass.csv> <lib.so> <kernel-substring> [top]"""
 import collections, csv, os, re, subprocess, sys, tempfile
 
 csv_path, lib, ksub = sys.argv[1:4]
@@ -54,9 +54,10 @@ def src(fn, l):
             L = src_cache[p]
             return L[l - 1].strip()[:70] if 0 < l <= len(L) else ""
     return ""
-print("--- by executed instructions")
-for k, v in agg_e.most_common(top):
-    print(f"{v / tot_e * 100:5.1f}% exec {agg_s[k] / tot_s * 100:5.1f}% stall  {k[0]}:{k[1]}  {src(*k)}")
+by_stall = os.environ.get("SORT") == "stall"
+print("--- by " + ("warp stall samples" if by_stall else "executed instructions"))
+for k, v in (agg_s if by_stall else agg_e).most_common(top):
+    print(f"{agg_e[k] / tot_e * 100:5.1f}% exec {agg_s[k] / tot_s * 100:5.1f}% stall  {k[0]}:{k[1]}  {src(*k)}")
 
 if os.environ.get("RANGES"):
     print("--- by line range")
