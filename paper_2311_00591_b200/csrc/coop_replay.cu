@@ -464,8 +464,8 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
       walkers = (int)std::min<size_t>(kThreads, ((size_t)max_smem - base) / per);
     }
     walkers = walkers / 32 * 32;  // whole warps
-    const bool want_group = wenv ? wenv[0] == 'G' : walkers < 128;
-    const bool want_warp = wenv ? wenv[0] == 'w' : false;
+    const bool want_group = wenv && wenv[0] == 'G';
+    const bool want_warp = wenv ? wenv[0] == 'w' : walkers < 128;
     if (want_group) {
       const int gs = gsm_ok && base + (size_t)g_bytes + group_extra <= (size_t)max_smem;
       if (gs || base + group_extra <= (size_t)max_smem) {
