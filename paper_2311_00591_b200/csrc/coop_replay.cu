@@ -24,6 +24,8 @@
 #include <new>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "replay_core.cuh"
 
 namespace coop {
@@ -44,11 +46,33 @@ __global__ void __launch_bounds__(kThreads, 1) replay_kernel(const KArgs a) {
     for (int i = threadIdx.x; i < nbm * a.vis_words; i += kThreads) v[i] = 0u;
     __syncthreads();
   }
-  for (int cell = blockIdx.x; cell < a.n_cells; cell += gridDim.x) {
-    CellT<true> c(a, sh, cell);
-    c.run(a.budgets[cell]);
-    if (threadIdx.x == 0) a.out[cell] = sh.res;
-    __syncthreads();
+  if (!a.helper) {
+    for (int cell = blockIdx.x; cell < a.n_cells; cell += gridDim.x) {
+      CellT<true> c(a, sh, cell);
+      c.run(a.budgets[cell]);
+      if (threadIdx.x == 0) a.out[cell] = sh.res;
+      __syncthreads();
+    }
+    return;
+  }
+  // clusters of two CTAs: rank 0 replays the cells of the cluster, rank 1 helps with the
+  // projected-cost closures of every pressure event (CellT::cluster_helper)
+  cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+  const int csize = a.helper + 1;
+  const int slot = (int)blockIdx.x / csize, nslots = (int)gridDim.x / csize;
+  if (cl.block_rank() == 0) {
+    for (int cell = slot; cell < a.n_cells; cell += nslots) {
+      CellT<true> c(a, sh, cell, slot);
+      c.run(a.budgets[cell]);
+      if (threadIdx.x == 0) a.out[cell] = sh.res;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) sh.helper_cmd = 2;  // exit
+    cl.sync();  // A
+    cl.sync();  // the helper has read the command
+  } else {
+    CellT<true> c(a, sh, -1, slot, (int)cl.block_rank());
+    c.cluster_helper();
   }
 }
 
@@ -490,8 +514,41 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, replay_kernel, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  // concurrent cells = min(n_budgets, resident CTAs); the workspace holds that many
-  const size_t cells = (size_t)std::min<int64_t>(n_budgets, (int64_t)sms * per_sm);
+  // cluster helpers: more SMs walking the closures of each cell (COOP_REPLAY_HELPER=0..3
+  // overrides the default below)
+  int helper = 0;
+  if (walkers > 0) {
+    const char *henv = getenv("COOP_REPLAY_HELPER");
+    // helpers per cell, 0..3.  Default (measured on B200): none for traces below 4096
+    // tensors (their closures are short: ResNet-50 loses more to the per-event cluster
+    // barriers than it gains); for larger traces 1 when the cells fill a quarter to half of
+    // the SMs (all of them then still run at once: config 3, 64 GPT-3 cells on 128 SMs), else
+    // 3 (a sweep's time is its slowest cell: the BiLSTM 256-cell sweep 50 -> 31 / 23 / 20 s
+    // with 1 / 2 / 3 helpers)
+    if (henv) helper = std::max(0, std::min(kMaxCluster - 1, atoi(henv)));
+    else if (t->T >= 4096)
+      helper = ((int64_t)n_budgets * 4 > (int64_t)sms && (int64_t)n_budgets * 2 <= (int64_t)sms) ? 1 : 3;
+  }
+  int max_clusters = 0;
+  if (helper) {
+    cudaLaunchConfig_t qc = {};
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = (unsigned)(helper + 1);
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    qc.gridDim = dim3((unsigned)(helper + 1) * (unsigned)(sms / (helper + 1)), 1, 1);
+    qc.blockDim = dim3(kThreads, 1, 1);
+    qc.dynamicSmemBytes = smem;
+    qc.attrs = qa;
+    qc.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, replay_kernel, &qc) != cudaSuccess || max_clusters < 1) {
+      cudaGetLastError();
+      helper = 0;
+    }
+  }
+  // concurrent cells = min(n_budgets, resident CTAs or clusters); the workspace holds that many
+  const size_t cells = (size_t)std::min<int64_t>(n_budgets, helper ? (int64_t)max_clusters : (int64_t)sms * per_sm);
   if (cells > t->ws_cells) {
     if (t->ws) cudaFree(t->ws);
     t->ws = nullptr;
@@ -551,9 +608,26 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
     a.snap_cap = snap->cap;
     a.snap_n = snap->n;
   }
-  // each CTA owns a workspace slot: cells are assigned cyclically, CTA b takes cells
-  // b, b + grid, ... and always uses slot b
-  replay_kernel<<<(unsigned)cells, kThreads, smem, st>>>(a);
+  // each CTA (cluster) owns a workspace slot: cells are assigned cyclically, slot b takes
+  // cells b, b + slots, ...
+  a.helper = helper;
+  if (helper) {
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = (unsigned)(helper + 1);
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    lc.gridDim = dim3((unsigned)(helper + 1) * (unsigned)cells, 1, 1);
+    lc.blockDim = dim3(kThreads, 1, 1);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    lc.attrs = la;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, replay_kernel, a) != cudaSuccess) return COOP_ERR_CUDA;
+  } else {
+    replay_kernel<<<(unsigned)cells, kThreads, smem, st>>>(a);
+  }
   if (cudaGetLastError() != cudaSuccess) return COOP_ERR_CUDA;
   return cudaEventRecord(t->done, st) == cudaSuccess ? COOP_OK : COOP_ERR_CUDA;
 }

@@ -2,6 +2,7 @@
 // (coop_replay.cu, one CTA per (trace, budget) cell) and the online single-pool calls
 // (coop_pool.cu, one CTA per call on a persistent device-resident pool).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -23,6 +24,7 @@ constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
 constexpr int kFree = -1;
 constexpr int kOpChunk = 32;   // replay: trace ops whose records are staged in shared memory at once
 constexpr int kListCap = 384;  // their input / death / lock lists staged with them (else read from L2)
+constexpr int kMaxCluster = 4;  // replay: CTAs per cell (the leader + up to 3 closure helpers)
 constexpr int kRing = 2048;    // replay warp BFS: per-warp queue ring (uint16 entries, shared memory)
 constexpr int kGL = 8;         // replay group BFS: lanes per group (4 groups per warp)
 constexpr int kGroups = kThreads / kGL;
@@ -97,7 +99,7 @@ __host__ __device__ __forceinline__ void cg_offsets(int T, int nnz, size_t off[6
 
 struct WsLayout {  // byte offsets inside one cell's workspace
   size_t tflags, pins, last_access, taddr, epochs, marks, stack, isz, ih, ist, S, H, B, trans, victims, cand, pacc,
-      rst, vc, vs;
+      rst, vc, vs, ctid;
   size_t bytes;
 };
 
@@ -119,6 +121,7 @@ struct CellPtrs {
   int64_t *pacc;  // per (candidate, half) closure sums of the current pressure event
   int32_t *rst;   // rematerialization stack: 4 x kStackCap (tensor, stage, input index, depth)
   int64_t *vc, *vs;  // c(t) and s(t) of the item view's EVICTABLE blocks (snapshots)
+  int32_t *ctid;     // the current event's candidate tensors (read by both CTAs of a cluster)
 };
 
 struct KArgs {
@@ -138,6 +141,8 @@ struct KArgs {
   int32_t g_smem;     // the compact graph is copied into shared memory
   int32_t g_bytes;    // its size (16-byte multiple)
   int32_t walkers;    // threads [0, walkers) walk closures (fast path); 0 = generic walk
+  int32_t helper;     // replay: helper CTAs per cell (thread-block clusters of helper + 1 CTAs:
+                      // the others walk projected-cost closures with the leader, cluster_helper)
   int32_t warp_bfs;   // fast path by whole warps (1) or by 8-lane groups (2): one closure per
                       // warp / group, edge-parallel BFS
   int32_t vis_words;  // bitmap words per walker (ceil(T / 32), rounded to 4)
@@ -178,6 +183,7 @@ struct Shared {
   U192 red192[kWarps];
   int32_t redpar;
   int32_t ncand, cand_next;  // projected-cost work list of the current pressure event
+  int32_t helper_cmd;        // cluster helper: 1 = walk this event's items, 2 = exit
   // the last evicted window (read by the online calls): items, span, cost bits, victims
   int32_t win_first, win_last, nvict;
   uint64_t win_span, win_cost;
@@ -272,16 +278,20 @@ struct CellT {
   const uint16_t *gip, *gcp, *gii, *gco;
   uint32_t *vis;
   uint16_t *ring;  // warp BFS: this warp's queue ring
+  int *wcnt;       // the work-item counter of the current event (local, or the cluster leader's)
 
-  __device__ CellT(const KArgs &a_, Shared &sh_, int cell_) : a(a_), tr(a_.tr), sh(sh_), cell(cell_) {
-    unsigned char *base = a.ws + (size_t)blockIdx.x * a.lay.bytes;  // this CTA's slot
+  // slot: the workspace slot (the CTA, or the cluster, that runs the cell); helper: this is
+  // the second CTA of a cluster (its walkers use the upper half of the DFS stacks)
+  __device__ CellT(const KArgs &a_, Shared &sh_, int cell_, int slot = -1, int rank = 0)
+      : a(a_), tr(a_.tr), sh(sh_), cell(cell_) {
+    unsigned char *base = a.ws + (size_t)(slot >= 0 ? slot : (int)blockIdx.x) * a.lay.bytes;
     w.tflags = (uint8_t *)(base + a.lay.tflags);
     w.pins = (int32_t *)(base + a.lay.pins);
     w.last_access = (int64_t *)(base + a.lay.last_access);
     w.taddr = (uint64_t *)(base + a.lay.taddr);
     w.epochs = (uint32_t *)(base + a.lay.epochs);
     w.marks = (uint32_t *)(base + a.lay.marks);
-    w.stack = (int32_t *)(base + a.lay.stack);
+    w.stack = (int32_t *)(base + a.lay.stack) + (size_t)rank * kThreads * tr.T;
     w.isz = (uint64_t *)(base + a.lay.isz);
     w.ih = (double *)(base + a.lay.ih);
     w.ist = (uint8_t *)(base + a.lay.ist);
@@ -295,11 +305,13 @@ struct CellT {
     w.rst = (int32_t *)(base + a.lay.rst);
     w.vc = (int64_t *)(base + a.lay.vc);
     w.vs = (int64_t *)(base + a.lay.vs);
-    log = a.log ? a.log + (size_t)cell * a.log_cap : nullptr;
+    w.ctid = (int32_t *)(base + a.lay.ctid);
+    log = (a.log && cell >= 0) ? a.log + (size_t)cell * a.log_cap : nullptr;
     gc = nullptr;
     gip = gcp = gii = gco = nullptr;
     vis = nullptr;
     ring = nullptr;
+    wcnt = &sh.cand_next;
     if (kRO && a.walkers > 0) {
       size_t off[6];
       cg_offsets(tr.T, tr.cg_nnz, off);
@@ -546,9 +558,9 @@ struct CellT {
       while (true) {
         if (sp == 0) {
           if (it >= 0) w.pacc[it] = acc;
-          it = atomicAdd(&sh.cand_next, 1);
+          it = atomicAdd(wcnt, 1);
           if (it >= nitems) break;
-          const int t = O()[cand[it >> 1]];
+          const int t = w.ctid[it >> 1];
           stage = it & 1;
           acc = 0;
           for (int q = 0; q < VW; q += 4) *reinterpret_cast<uint4 *>(mk + q) = make_uint4(0, 0, 0, 0);
@@ -583,10 +595,10 @@ struct CellT {
     const int nitems = 2 * ncand;
     while (true) {
       int it = 0;
-      if (lane == 0) it = atomicAdd(&sh.cand_next, 1);
+      if (lane == 0) it = atomicAdd(wcnt, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= nitems) break;
-      const int t = O()[cand[it >> 1]];
+      const int t = w.ctid[it >> 1];
       const int stage = it & 1;
       const uint16_t *lst = stage == 0 ? gii : gco;
       const uint16_t *ptr = stage == 0 ? gip : gcp;
@@ -791,10 +803,10 @@ struct CellT {
           if (gl == 0) w.pacc[it] = acc;
         }
         int nit = 0;
-        if (gl == 0) nit = atomicAdd(&sh.cand_next, 1);
+        if (gl == 0) nit = atomicAdd(wcnt, 1);
         it = __shfl_sync(gmask, nit, 0, kGL);
         if (it >= nitems) break;
-        t = O()[cand[it >> 1]];
+        t = w.ctid[it >> 1];
         stage = it & 1;
         lst = stage == 0 ? gii : gco;
         ptr = stage == 0 ? gip : gcp;
@@ -830,11 +842,29 @@ struct CellT {
     }
   }
 
+  // the fast walk of this event's items (both CTAs of a cluster run it)
+  __device__ void walk_items(const int32_t *cand, int ncand) {
+    if (a.warp_bfs == 2) closures_group(cand, ncand);
+    else if (a.warp_bfs) closures_warp(cand, ncand);
+    else closures_fast(cand, ncand);
+  }
+
   __device__ void projected_costs(const int32_t *cand, int ncand, int pol = 0) {
+    // the candidates' tensors, in global memory where a cluster helper can read them
+    for (int ci = threadIdx.x; ci < ncand; ci += kThreads) w.ctid[ci] = O()[cand[ci]];
+    __syncthreads();
     if (kRO && a.walkers > 0) {
-      if (a.warp_bfs == 2) closures_group(cand, ncand);
-      else if (a.warp_bfs) closures_warp(cand, ncand);
-      else closures_fast(cand, ncand);
+      if (a.helper) {  // the cluster's second CTA takes items from the same counter
+        if (threadIdx.x == 0) {
+          sh.helper_cmd = 1;
+          sh.ncand = ncand;
+        }
+        cooperative_groups::this_cluster().sync();  // A: the helper may start
+        walk_items(cand, ncand);
+        cooperative_groups::this_cluster().sync();  // B: every item's sums are in w.pacc
+      } else {
+        walk_items(cand, ncand);
+      }
       finish_costs(cand, ncand, pol);
       return;
     }
@@ -852,7 +882,7 @@ struct CellT {
         if (it >= 0) w.pacc[it] = acc;
         it = atomicAdd(&sh.cand_next, 1);
         if (it >= nitems) break;
-        const int t = O()[cand[it >> 1]];
+        const int t = w.ctid[it >> 1];
         stage = it & 1;
         acc = 0;
         ep = (uint8_t)++epoch;
@@ -1455,6 +1485,33 @@ struct CellT {
   }
   __device__ __forceinline__ int st_lock(int j) const { return j < sh.l_lock1 ? sh.llock[j - sh.l_lock0] : tr.lock_idx[j]; }
 
+  // The second CTA of a cluster: at every pressure event of the leader (rank 0) it copies
+  // the leader's tensor flags through distributed shared memory and walks work items from
+  // the leader's counter with its own walkers, bitmaps and graph copy; both CTAs' sums land
+  // in the cell's w.pacc.  Ends when the leader posts the exit command.
+  __device__ void cluster_helper() {
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    Shared *lead = cl.map_shared_rank(&sh, 0);
+    wcnt = &lead->cand_next;
+    while (true) {
+      cl.sync();  // A
+      const int cmd = lead->helper_cmd;
+      if (cmd != 1) {
+        cl.sync();  // the leader keeps its shared memory until this read is done
+        break;
+      }
+      const int ncand = lead->ncand;
+      {  // the leader's residency / liveness flags (16-byte copies)
+        const uint4 *src = reinterpret_cast<const uint4 *>(lead->tfl);
+        uint4 *dst = reinterpret_cast<uint4 *>(sh.tfl);
+        for (int i = threadIdx.x; i < a.tfl_bytes / 16; i += kThreads) dst[i] = src[i];
+      }
+      __syncthreads();
+      walk_items(nullptr, ncand);
+      cl.sync();  // B
+    }
+  }
+
   // ---------------------------------------------------------------- the op loop
   __device__ void run(uint64_t budget) {
     const int T = tr.T, M = tr.M;
@@ -1611,7 +1668,7 @@ WsLayout make_layout(int T) {
   L.taddr = take((size_t)T * 8);
   L.epochs = take((size_t)kThreads * 4);
   L.marks = take((size_t)kThreads * ((T + 15) & ~15));  // one byte per tensor and thread
-  L.stack = take((size_t)kThreads * T * 4);
+  L.stack = take((size_t)kMaxCluster * kThreads * T * 4);  // one set of stacks per CTA of a cluster
   L.isz = take((size_t)(kCap + 1) * 8);
   L.ih = take((size_t)(kCap + 1) * 8);
   L.ist = take((size_t)(kCap + 1));
@@ -1625,6 +1682,7 @@ WsLayout make_layout(int T) {
   L.rst = take((size_t)4 * kStackCap * 4);
   L.vc = take((size_t)(kCap + 2) * 8);
   L.vs = take((size_t)(kCap + 2) * 8);
+  L.ctid = take((size_t)(kCap + 2) * 4);
   L.bytes = o;
   return L;
 }

@@ -191,3 +191,20 @@ def test_r37_block_capacity_nomem():
     assert int(res[0]["max_blocks"]) <= 4096
     want, _ = O.replay(tr, budget, 0)
     assert int(want["status"]) == O.OK
+
+
+@pytest.mark.parametrize("helpers", [0, 1, 3])
+def test_cluster_helpers(helpers, monkeypatch):
+    """Thread-block clusters of 1 + helpers CTAs per cell: the helper
+    CTAs walk projected-cost closures from the leader's work counter at every pressure
+    event; every counter, the digest and the event log stay bit-exact with O2."""
+    monkeypatch.setenv("COOP_REPLAY_HELPER", str(helpers))
+    for name, frac in (("bilstm", 0.3), ("gpt3_2.7b", 0.5), ("resnet50", 0.4)):
+        tr = dnn.dnn(name)
+        flags = coop.F_PARTITION | coop.F_INPLACE
+        peak = O.peak_live(tr, flags)
+        check(tr, [int(peak * frac), int(peak * (frac + 0.1))], flags, log_cap=30000, ctx=f"helpers {helpers} {name}")
+    for pol in (coop.F_POLICY_DTR, coop.F_POLICY_DTE):
+        tr = dnn.unet()
+        peak = O.peak_live(tr, 0)
+        check(tr, [int(peak * 0.6)], pol, ctx=f"helpers {helpers} pol {pol}")
