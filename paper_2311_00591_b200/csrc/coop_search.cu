@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 
 #include "coop.h"
 #include "coop_internal.h"
@@ -40,8 +41,6 @@ constexpr bool kPhaseHooks = false;
 #endif
 constexpr int kCandCap = 512;  // fits two 512-thread CTAs (one stage each) per SM at N = 4096
 constexpr int kMaxWarps = 16;
-constexpr uint64_t kSizeMask = (1ull << 62) - 1ull;
-constexpr uint64_t kSizeLimit = 1ull << 48;
 constexpr uint64_t kRClamp = 1ull << 62;  // any R > sum of sizes (< 2^61) is infeasible
 constexpr int kInfIdx = 0x7fffffff;
 
@@ -52,7 +51,12 @@ struct Scratch {
   double wP[kMaxWarps];  // chunk-pruning upper bounds
   int32_t wF[kMaxWarps];
   int32_t wZ[kMaxWarps];
-  uint64_t part[2][kMaxWarps][3];
+  union {
+    uint64_t part[2][kMaxWarps][3];  // verification partial sums (phase B)
+    struct {
+      int32_t zW[kMaxWarps], zM[kMaxWarps], zW2[kMaxWarps];  // zero-pass reductions (phase 1)
+    };
+  };
   int32_t partn[2][kMaxWarps];
   uint64_t bcost[kMaxWarps];
   int32_t bfirst[kMaxWarps];
@@ -60,7 +64,7 @@ struct Scratch {
   int32_t bnev[kMaxWarps];
   int32_t ncand;
   int32_t nsurv;      // surviving chunks in the list (phase B1)
-  int32_t xend, xnev;  // end / evictions of the best exactly-costed window
+  uint16_t evc[kMaxWarps * 32];  // per chunk: EVICTABLE mask (exact re-summation, n_evict)
   uint32_t cand[kCandCap];
   unsigned long long mbar[2];
   int32_t nplist;                      // pending mode: pools of the chunk to finish
@@ -170,12 +174,24 @@ __device__ __forceinline__ void write_result(coop_window *o, int32_t first, int3
   *o = w;
 }
 
-template <typename T, typename Op>
-__device__ __forceinline__ T warp_allreduce(T v, Op op) {
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, d));
-  return v;
+
+// Warp reductions on the REDUX unit (one instruction per 32-bit step).  Doubles are reduced
+// through their total-order keys (monotone in the value for every non-NaN binary64).
+__device__ __forceinline__ int wmin_i32(int x) { return __reduce_min_sync(0xffffffffu, x); }
+__device__ __forceinline__ uint64_t wmin_u64(uint64_t x) {
+  const uint32_t xh = (uint32_t)(x >> 32);
+  const uint32_t hi = __reduce_min_sync(0xffffffffu, xh);
+  const uint32_t lo = __reduce_min_sync(0xffffffffu, xh == hi ? (uint32_t)x : 0xffffffffu);
+  return ((uint64_t)hi << 32) | lo;
 }
+__device__ __forceinline__ uint64_t dkey(double d) {
+  const uint64_t b = (uint64_t)__double_as_longlong(d);
+  return (int64_t)b < 0 ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dunkey(uint64_t k) {
+  return __longlong_as_double((long long)((int64_t)k < 0 ? (k & 0x7fffffffffffffffull) : ~k));
+}
+__device__ __forceinline__ double wmin_f64(double x) { return dunkey(wmin_u64(dkey(x))); }
 
 __device__ __forceinline__ U192 warp_sum192(U192 acc, int &nev) {
 #pragma unroll
@@ -194,54 +210,74 @@ __device__ __forceinline__ bool better(uint64_t cb, int i, uint64_t bb, int bi) 
   return cb < bb || (cb == bb && i < bi);
 }
 
-// Per-pool view after phase A (all in shared memory):
+// Per-pool view in shared memory after phase 1 (region = one TMA-staged array):
 //   region 0: S[k]   exclusive span prefix, k in [0, n]; S[n] = total span, S[n+1] = ~0
-//   region 1: H^[k]  fp64 prefix of h, k in [0, n]
-//   region 2: v[k]   h as binary64; FREE items stored as -0.0, PINNED items as NaN
+//   region 1: c[k]   as staged (the exact re-summation divides it again)
+//   region 2: H^[k]  fp64 prefix of the approximate h^ (chunk-local until phase 2)
 //   list[c]          (uint4, scratch) surviving chunks of the pruning pass (phase B1)
+//   evc[t]           EVICTABLE mask of chunk t
 struct PoolView {
-  smem_t *sr, *hr, *vr;
+  smem_t *sr, *cr, *hr;
   uint4 *list;
+  const uint16_t *evc;
+  const double *sg;  // this pool's staleness s in global memory (exact re-summation only)
   int32_t n;
-  uint64_t R, S_total;
+  uint64_t R;
   double gerr;
 
   __device__ __forceinline__ uint64_t S_at(int x) const { return sm<uint64_t>(sr, swz((uint32_t)x)); }
   __device__ __forceinline__ double H_at(int x) const { return sm<double>(hr, swz((uint32_t)x)); }
-  __device__ __forceinline__ double v_at(int x) const { return sm<double>(vr, swz((uint32_t)x)); }
-
+  __device__ __forceinline__ double c_at(int x) const { return sm<double>(cr, swz((uint32_t)x)); }
 };
+
+// 1/s for s in [1, 2^960): the MUFU approximation and two Newton steps (relative error a few
+// ulps; the filter's bound allows 2^-44 per h^)
+__device__ __forceinline__ double rcp_nr(double s) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+  double e = __fma_rn(-s, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-s, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
+// Exact cost of the window [i, e) (R3): h = c/s (IEEE RN, R1) of its EVICTABLE items --
+// FREE items add 0, a window never holds a PINNED one -- summed in 192-bit fixed point over
+// the items i + off, i + off + step, ...; counts the EVICTABLE items (n_evict).
+template <int K>
+__device__ __forceinline__ void window_sum(const PoolView &v, int i, int e, int off, int step,
+                                           U192 &acc, int &nev) {
+  for (int k = i + off; k < e; k += step) {
+    if ((v.evc[k / K] >> (k % K)) & 1u) {
+      acc = u192_add(acc, u192_from_double(__ddiv_rn(v.c_at(k), v.sg[k])));
+      ++nev;
+    }
+  }
+}
 
 // Per-thread running state of the filter.
 struct LaneBest {
-  double U, L, L2;   // inexact windows: min upper bound, min / second-min lower bound
-  int li, le;        // the inexact start with the minimal lower bound and its end
-  uint64_t xb;       // exactly known windows (zero-cost, or <= 2 items): min cost bits
-  int xi, xe;        //   ... its start (lowest among equal cost) and end
+  double U, L, L2;  // min upper bound, min / second-min lower bound
+  int li, le;       // the start with the minimal lower bound and its end
 };
 
 // A surviving chunk (phase B1): x = k0 | elo << 16 (elo <= e(i) for every start of the
-// chunk), y = PINNED mask | nonzero-h mask << 16 of its K items, z / w = first PINNED /
-// nonzero-h index to the right of the chunk.
-__device__ __forceinline__ uint4 chunk_rec(int k0, int elo, uint32_t barmask, uint32_t nzmask,
-                                           int nb_right, int nz_right) {
-  return make_uint4((uint32_t)k0 | ((uint32_t)elo << 16), barmask | (nzmask << 16),
-                    (uint32_t)nb_right, (uint32_t)nz_right);
+// chunk), y = PINNED mask of its K items, z = first PINNED index to the right of the chunk.
+__device__ __forceinline__ uint4 chunk_rec(int k0, int elo, uint32_t barmask, int nb_right) {
+  return make_uint4((uint32_t)k0 | ((uint32_t)elo << 16), barmask, (uint32_t)nb_right, 0u);
 }
 
 // The filter for start i = k0 + q of a surviving chunk, run by any thread: window end by a
-// galloping search from elo, PINNED and zero-cost checks from the chunk masks, exact cost
-// for zero windows and windows of <= 2 items, else the fp64 prefix difference with its
-// bound.  MODE 0 folds the start into LaneBest (lexicographic (cost bits, start) for exact
-// windows, so the order in which a thread visits starts does not matter); MODE 1 appends
-// it to the candidate list when it is inexact, its lower bound is <= thresh and i lies in
-// [w_lo, w_hi).
+// galloping search from elo, PINNED check from the chunk mask, and the fp64 prefix difference
+// C^ = H^[e] - H^[i] with its bound |C^ - C| <= gerr (H^[e] + H^[i]).  MODE 0 folds the start
+// into LaneBest; MODE 1 appends it to the candidate list when its lower bound is <= thresh
+// and i lies in [w_lo, w_hi).
 template <int MODE>
 __device__ __forceinline__ void eval_start(const PoolView &v, const uint4 rec, int q, double thresh,
                                            int w_lo, int w_hi, Scratch &sc, LaneBest &b) {
   const int n = v.n;
   const int k0 = (int)(rec.x & 0xffffu), elo = (int)(rec.x >> 16);
-  const uint32_t barmask = rec.y & 0xffffu, nzmask = rec.y >> 16;
+  const uint32_t barmask = rec.y;
   const int i = k0 + q;
   if (i >= n || ((barmask >> q) & 1u)) return;
   const uint64_t target = v.S_at(i) + v.R;  // < 2^63
@@ -264,104 +300,134 @@ __device__ __forceinline__ void eval_start(const PoolView &v, const uint4 rec, i
     e = hi;
   }
   if (e > n) return;  // no window covers R from i (nor from any later start)
-  const uint32_t mb = barmask >> q, mz = nzmask >> q;
+  const uint32_t mb = barmask >> q;
   const int nb = mb ? i + __ffs(mb) - 1 : (int)rec.z;
   if (nb < e) return;  // a PINNED item inside [i, e-1]
-  const int nz = mz ? i + __ffs(mz) - 1 : (int)rec.w;
-  const int len = e - i;
-  const bool zero = nz >= e;
-  const bool exact = zero || len <= 2;
-  const double h0 = fabs(v.v_at(i));
-  const double h1 = len >= 2 ? fabs(v.v_at(i + 1)) : 0.0;
   const double He = v.H_at(e), Hi = v.H_at(i);
-  const double Cx = zero ? 0.0 : __dadd_rn(h0, h1);
-  const double C = exact ? Cx : He - Hi;
-  const double err = exact ? 0.0 : v.gerr * (He + Hi);
+  const double C = He - Hi;
+  const double err = v.gerr * (He + Hi);
   const double Lb = C - err;
   if (MODE == 0) {
-    if (exact) {
-      const uint64_t cb = (uint64_t)__double_as_longlong(C);
-      if (better(cb, i, b.xb, b.xi)) {
-        b.xb = cb;
-        b.xi = i;
-        b.xe = e;
-      }
+    b.U = fmin(b.U, C + err);
+    if (Lb < b.L) {
+      b.L2 = b.L;
+      b.L = Lb;
+      b.li = i;
+      b.le = e;
     } else {
-      b.U = fmin(b.U, C + err);
-      if (Lb < b.L) {
-        b.L2 = b.L;
-        b.L = Lb;
-        b.li = i;
-        b.le = e;
-      } else {
-        b.L2 = fmin(b.L2, Lb);
-      }
+      b.L2 = fmin(b.L2, Lb);
     }
-  } else if (!exact && Lb <= thresh && i >= w_lo && i < w_hi) {
+  } else if (Lb <= thresh && i >= w_lo && i < w_hi) {
     const int slot = atomicAdd(&sc.ncand, 1);
     if (slot < kCandCap) sc.cand[slot] = ((uint32_t)i << 16) | (uint32_t)(e - i);  // n <= 8192
   }
 }
 
-// Phase A of one thread: decode its K items (pairs via 16-byte conflict-free loads of the
-// swizzled stage), validate (R7; integer tests on the binary64 encodings, same semantics as
-// the oracle's comparisons), h = c/s (R1), local exclusive prefixes of span and h, and the
-// h slot written back in place (FREE -> -0.0, PINNED -> NaN).  FULL: no item past n.
+// Phase 1 of one thread (every pool): decode its K items (pairs via 16-byte conflict-free
+// loads of the swizzled stage), local exclusive prefixes of span (u64) and of the
+// approximate h^ = c * rcp(s) (fp64; stored over s, which is not read again from shared
+// memory), a 2-bit state code per item, and the R7 checks WITHOUT a division: for c > 0
+// normal and s >= 1, c/s lies in (2^(d-1), 2^(d+1)) with d the exponent difference of c and
+// s, and hi(c) - hi(s) lies in ((d-1) 2^20, (d+1) 2^20), so hi(c) - hi(s) in
+// [-62 2^20, 58 2^20) gives d in [-62, 58] and RN(c/s) inside [2^-64, 2^60) (s is held to
+// [1, 2^960), so a negative or non-finite c falls outside the band too).  An EVICTABLE item
+// outside that clear range (c = +-0 is clear when s is) sets `oor`, and settle_chunk() then
+// re-decides the chunk with the oracle's own comparisons and the exact division.
+// FULL: no item past n.
+//   st2: bits 2j..2j+1 = state of item j (padding: FREE); nz: EVICTABLE with c != 0;
+//   badbits: size bits 48..61 of some item; minsz: 0 iff some live item has size 0.
 template <int K, bool FULL>
-__device__ __forceinline__ void phase_a(const PoolView &v, int k0, int n, bool &bad,
-                                        uint32_t &barmask, uint32_t &nzmask, uint64_t (&spre)[K],
-                                        double (&hpre)[K], uint64_t &sacc, double &hacc) {
+__device__ __forceinline__ void phase1(const PoolView &v, int k0, int n, uint32_t &st2,
+                                       uint32_t &nz, uint32_t &badbits, uint32_t &minsz,
+                                       bool &oor, uint64_t (&spre)[K], uint64_t &sacc,
+                                       double &hacc) {
 #pragma unroll
   for (int q = 0; q < K; q += 2) {
     const int k = k0 + q;
     const uint32_t o = swz((uint32_t)k);
     ulonglong2 vs = make_ulonglong2(0, 0);
-    double2 vc = make_double2(0.0, 0.0), vt = make_double2(1.0, 1.0);
+    uint4 vc = make_uint4(0, 0, 0, 0), vt = make_uint4(0, 0x3ff00000u, 0, 0x3ff00000u);
     if (FULL || k < n) {
       vs = sm<ulonglong2>(v.sr, o);
-      vc = sm<double2>(v.hr, o);
-      vt = sm<double2>(v.vr, o);
+      vc = sm<uint4>(v.cr, o);
+      vt = sm<uint4>(v.hr, o);
     }
-    double hs[2];
+    double hl[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
+      const int j = q + r;
       const bool live = FULL || (k + r < n);
       const uint64_t sv = live ? (r ? vs.y : vs.x) : 0ull;  // padding: FREE, size 0
-      const uint32_t svh = (uint32_t)(sv >> 32);
-      const uint32_t state = svh >> 30;
-      const bool ev = (state == COOP_EVICTABLE);
-      const uint64_t size = sv & kSizeMask;
-      const double cr = r ? vc.y : vc.x, sr_ = r ? vt.y : vt.x;
-      const double c = ev ? cr : 1.0, st = ev ? sr_ : 1.0;  // 1/1: no slow division path
-      const double hq = __ddiv_rn(c, st);                    // h(t) = c(t)/s(t), PAPER.md:150 (R1)
-      // validation (R7) on the high words: the bounds are powers of two, so these are the
-      // exact value ranges of the oracle's comparisons
-      const uint32_t ch = (uint32_t)((uint64_t)__double_as_longlong(c) >> 32);
-      const uint32_t cl = (uint32_t)__double_as_longlong(c);
-      const uint32_t sh_ = (uint32_t)((uint64_t)__double_as_longlong(st) >> 32);
-      const uint32_t hh = (uint32_t)((uint64_t)__double_as_longlong(hq) >> 32) & 0x7fffffffu;
-      const uint32_t hl = (uint32_t)__double_as_longlong(hq);
-      const bool hzero = (hh | hl) == 0u;
-      const bool c_ok = (ch < 0x7ff00000u) | ((ch == 0x80000000u) & (cl == 0u));  // finite, >= 0 (or -0)
-      const bool s_ok = (sh_ - 0x3ff00000u) < 0x40000000u;                       // finite, >= 1
-      const bool h_ok = hzero | ((hh - 0x3bf00000u) < 0x07c00000u);               // 0 or [2^-64, 2^60)
-      const bool size_bad = ((svh & 0x3fff0000u) != 0u) | (size == 0ull);       // size in [1, 2^48)
-      if (live) bad |= size_bad | (state == 3u) | (ev & !(c_ok & s_ok & h_ok));
-      const double h = ev ? hq : 0.0;
-      const bool nzh = ev & !hzero;
-      nzmask |= (uint32_t)nzh << (q + r);
-      barmask |= (uint32_t)(live & (state == COOP_PINNED)) << (q + r);
-      spre[q + r] = sacc;
-      hpre[q + r] = hacc;
-      sacc += live ? size : 0ull;
-      hacc = __dadd_rn(hacc, h);
-      // slot: EVICTABLE |h| (sign cleared), FREE -0.0 (h = 0, "not an eviction",
-      // PAPER.md:147), PINNED NaN (never summed)
-      const uint32_t oh = ev ? hh : (state == COOP_PINNED ? 0x7ff80000u : 0x80000000u);
-      const uint32_t ol = ev ? hl : 0u;
-      hs[r] = __hiloint2double((int)oh, (int)ol);
+      const uint32_t slo = (uint32_t)sv, svh = (uint32_t)(sv >> 32);
+      st2 |= (svh >> (30 - 2 * j)) & (3u << (2 * j));
+      badbits |= svh & 0x3fff0000u;
+      const uint32_t shi = svh & 0x3fffffffu;
+      minsz = min(minsz, live ? (slo | shi) : 1u);
+      spre[j] = sacc;
+      sacc += ((uint64_t)shi << 32) | slo;
+      const uint32_t cl = r ? vc.z : vc.x, ch = r ? vc.w : vc.y;
+      const uint32_t tl = r ? vt.z : vt.x, sh = r ? vt.w : vt.y;
+      double hh = 0.0;
+      if ((svh >> 30) == COOP_EVICTABLE) {
+        const bool czero = ((ch << 1) | cl) == 0u;
+        // clear range of s: [1, 2^960); then a negative, infinite or NaN c gives
+        // hi(c) - hi(s) >= 64 2^20, outside the clear band of the exponent test
+        oor |= (sh - 0x3ff00000u) >= 0x3c000000u;
+        if (!czero) {
+          nz |= 1u << j;
+          oor |= (ch - sh + (62u << 20)) >= (120u << 20);
+        }
+        hh = __hiloint2double((int)ch, (int)cl) * rcp_nr(__hiloint2double((int)sh, (int)tl));
+      }
+      hl[r] = hacc;
+      hacc = __dadd_rn(hacc, hh);
     }
-    if (FULL || k < n) sm<double2>(v.vr, o) = make_double2(hs[0], hs[1]);
+    if (FULL || k < n) sm<double2>(v.hr, o) = make_double2(hl[0], hl[1]);
+  }
+}
+
+// The exact R7 tests (the oracle's comparisons; h = c/s) for a chunk with an
+// EVICTABLE item phase 1 could not clear from the encodings: sets nz exactly and rebuilds the
+// chunk's local h^ prefixes with exact h (s from global memory: the stage holds the prefixes).
+template <int K>
+__device__ __noinline__ void settle_chunk(const PoolView &v, int k0, uint32_t evm, uint32_t &nz,
+                                          bool &bad, double &hacc) {
+  double acc = 0.0;
+  for (int q = 0; q < K && k0 + q < v.n; ++q) {
+    const uint32_t o = swz((uint32_t)(k0 + q));
+    double h = 0.0;
+    if ((evm >> q) & 1u) {
+      const double c = sm<double>(v.cr, o), s = v.sg[k0 + q];
+      if (!isfinite(c) || !isfinite(s) || c < 0.0 || s < 1.0) {
+        bad = true;
+      } else {
+        h = __ddiv_rn(c, s);
+        if (h == 0.0) nz &= ~(1u << q);
+        else if (h < 0x1p-64 || h >= 0x1p60) bad = true;
+      }
+    }
+    sm<double>(v.hr, o) = acc;
+    acc = __dadd_rn(acc, h);
+  }
+  hacc = acc;
+}
+
+// bits 2j of x -> bit j (K <= 16)
+__device__ __forceinline__ uint32_t even_bits(uint32_t x) {
+  x &= 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0f0f0f0fu;
+  x = (x | (x >> 4)) & 0x00ff00ffu;
+  return (x | (x >> 8)) & 0x0000ffffu;
+}
+
+// First item at or after chunk t's item q (q may be K) that is not an h = 0 item, using the
+// published per-chunk zero masks (rare paths only); n if none.
+__device__ int zero_run_stop(const uint16_t *zmk, int t, int q, int K, int n) {
+  for (;; ++t, q = 0) {
+    if (t * K >= n) return n;
+    const uint32_t m = ~((uint32_t)zmk[t] >> q) & ((1u << (K - q)) - 1u);  // K - q >= 1 here
+    if (q < K && m) return min(t * K + q + __ffs(m) - 1, n);
   }
 }
 
@@ -373,411 +439,376 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
   const int T = blockDim.x, W = T >> 5;
   const int n = a.n;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  constexpr uint32_t kFull = K == 32 ? ~0u : ((1u << K) - 1u);
   PoolView v;
   v.sr = stage;
-  v.hr = stage + a.region_bytes;
-  v.vr = stage + 2u * a.region_bytes;
+  v.cr = stage + a.region_bytes;
+  v.hr = stage + 2u * a.region_bytes;
   v.list = Ebuf;
+  v.evc = sc.evc;
+  v.sg = a.stale + p * a.stride;
   v.n = n;
   v.R = Rraw < kRClamp ? Rraw : kRClamp;
   v.gerr = a.gerr;
   const int k0 = tid * K;
+  uint16_t *zmk16 = reinterpret_cast<uint16_t *>(Ebuf);  // per chunk: h = 0 item mask
 
   if (a.dbg == 1) {
     if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK);
     return;
   }
+  // ---------------- phase 1: decode, validate (R7), span / h^ prefixes, masks --------------
+  bool bad = (Rraw == 0), oor = false;
+  uint32_t st2 = 0, nzmask = 0, badbits = 0, minsz = 1;
+  uint64_t spre[K];
+  uint64_t sacc = 0;
+  double hacc = 0.0;
+  if (k0 + K <= n)  // warp-uniform except in the last warp
+    phase1<K, true>(v, k0, n, st2, nzmask, badbits, minsz, oor, spre, sacc, hacc);
+  else
+    phase1<K, false>(v, k0, n, st2, nzmask, badbits, minsz, oor, spre, sacc, hacc);
+  const uint32_t evmask = even_bits(st2 & ~(st2 >> 1));  // state 01
+  const uint32_t barmask = even_bits((st2 >> 1) & ~st2);  // state 10
+  bad |= (badbits != 0u) | (minsz == 0u) | ((st2 & (st2 >> 1) & 0x55555555u) != 0u);  // state 3
+  if (oor) settle_chunk<K>(v, k0, evmask, nzmask, bad, hacc);
+  const int cnt = n - k0;
+  const uint32_t valid = cnt >= K ? kFull : (cnt > 0 ? (1u << cnt) - 1u : 0u);
+  const uint32_t zm = valid & ~barmask & ~nzmask;  // h = 0 items (FREE, or EVICTABLE with h = 0)
+  sc.evc[tid] = (uint16_t)evmask;
+  zmk16[tid] = (uint16_t)zm;
+
+  // ---------------- warp scans: S (u64), H^ (fp64), next PINNED (suffix min) -------------
+  uint64_t sinc = sacc;
+  double hinc = hacc;
+  int32_t fb = barmask ? k0 + __ffs(barmask) - 1 : kInfIdx;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t so = __shfl_up_sync(0xffffffffu, sinc, d);
+    const double ho = __shfl_up_sync(0xffffffffu, hinc, d);
+    const int32_t bo = __shfl_down_sync(0xffffffffu, fb, d);
+    if (lane >= d) {
+      sinc += so;
+      hinc = __dadd_rn(ho, hinc);
+    }
+    if (lane + d < 32) fb = min(fb, bo);
+  }
+  uint64_t sexc = __shfl_up_sync(0xffffffffu, sinc, 1);
+  double hexc = __shfl_up_sync(0xffffffffu, hinc, 1);
+  int32_t bexc = __shfl_down_sync(0xffffffffu, fb, 1);
+  if (lane == 0) {
+    sexc = 0;
+    hexc = 0.0;
+    sc.wF[warp] = fb;
+  }
+  if (lane == 31) {
+    bexc = kInfIdx;
+    sc.wS[warp] = sinc;
+    sc.wH[warp] = hinc;
+  }
+  const int bad_any = __syncthreads_or(bad);
+  uint64_t S_car, S_total;
   {
-    // ---------------- phase A: decode, validate, h = c/s, local prefixes -------------
-    bool bad = (Rraw == 0);
-    uint32_t barmask = 0, nzmask = 0;
-    uint64_t spre[K];
-    double hpre[K];
-    uint64_t sacc = 0;
-    double hacc = 0.0;
-    if (k0 + K <= n)  // warp-uniform except in the last warp
-      phase_a<K, true>(v, k0, n, bad, barmask, nzmask, spre, hpre, sacc, hacc);
-    else
-      phase_a<K, false>(v, k0, n, bad, barmask, nzmask, spre, hpre, sacc, hacc);
-
-    // ---------------- block scan: S (u64), H^ (fp64), next PINNED / next nonzero-h ------
-    uint64_t sinc = sacc;
-    double hinc = hacc;
-    int32_t fb = barmask ? k0 + __ffs(barmask) - 1 : kInfIdx;
-    int32_t fz = nzmask ? k0 + __ffs(nzmask) - 1 : kInfIdx;
+    uint64_t ws = lane < W ? sc.wS[lane] : 0ull;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t so = __shfl_up_sync(0xffffffffu, sinc, d);
-      const double ho = __shfl_up_sync(0xffffffffu, hinc, d);
-      const int32_t bo = __shfl_down_sync(0xffffffffu, fb, d);
-      const int32_t zo = __shfl_down_sync(0xffffffffu, fz, d);
-      if (lane >= d) {
-        sinc += so;
-        hinc = __dadd_rn(ho, hinc);
-      }
-      if (lane + d < 32) {
-        fb = min(fb, bo);
-        fz = min(fz, zo);
-      }
+    for (int d = 1; d < kMaxWarps; d <<= 1) {
+      const uint64_t so = __shfl_up_sync(0xffffffffu, ws, d);
+      if (lane >= d) ws += so;
     }
-    uint64_t sexc = __shfl_up_sync(0xffffffffu, sinc, 1);
-    double hexc = __shfl_up_sync(0xffffffffu, hinc, 1);
-    int32_t bexc = __shfl_down_sync(0xffffffffu, fb, 1);
-    int32_t zexc = __shfl_down_sync(0xffffffffu, fz, 1);
-    if (lane == 0) {
-      sexc = 0;
-      hexc = 0.0;
-    }
-    if (lane == 31) {
-      bexc = kInfIdx;
-      zexc = kInfIdx;
-      sc.wS[warp] = sinc;
-      sc.wH[warp] = hinc;
-    }
-    if (lane == 0) {
-      sc.wF[warp] = fb;
-      sc.wZ[warp] = fz;
-    }
-    const int bad_any = __syncthreads_or(bad);
-    uint64_t S_car, S_total;
-    double H_car;
-    int32_t nb_right, nz_right;
-    {
-      // cross-warp: lane l < W holds warp l's totals; shuffle scan over the (<= 16) warps
-      uint64_t ws = lane < W ? sc.wS[lane] : 0ull;
-      double wh = lane < W ? sc.wH[lane] : 0.0;
-      int32_t wb = lane < W ? sc.wF[lane] : kInfIdx;
-      int32_t wz = lane < W ? sc.wZ[lane] : kInfIdx;
+    const uint64_t sprev = __shfl_sync(0xffffffffu, ws, warp ? warp - 1 : 0);
+    S_car = (warp ? sprev : 0ull) + sexc;
+    S_total = __shfl_sync(0xffffffffu, ws, W - 1);
+  }
+  const uint64_t Sk0 = S_car + spre[0];
+  if (bad_any || a.dbg == 2) {
+    if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, bad_any ? COOP_ERR_INVALID_ARG : COOP_OK);
+    return;
+  }
+  // S over the size words (the sizes live on in spre, the states in the masks)
 #pragma unroll
-      for (int d = 1; d < kMaxWarps; d <<= 1) {
-        const uint64_t so = __shfl_up_sync(0xffffffffu, ws, d);
-        const double ho = __shfl_up_sync(0xffffffffu, wh, d);
-        const int32_t bo = __shfl_down_sync(0xffffffffu, wb, d);
-        const int32_t zo = __shfl_down_sync(0xffffffffu, wz, d);
-        if (lane >= d) {
-          ws += so;
-          wh = __dadd_rn(ho, wh);
-        }
-        if (lane + d < 32) {
-          wb = min(wb, bo);
-          wz = min(wz, zo);
-        }
-      }
-      const uint64_t sprev = __shfl_sync(0xffffffffu, ws, warp ? warp - 1 : 0);
-      const double hprev = __shfl_sync(0xffffffffu, wh, warp ? warp - 1 : 0);
-      const int32_t bnext = __shfl_sync(0xffffffffu, wb, min(warp + 1, 31));
-      const int32_t znext = __shfl_sync(0xffffffffu, wz, min(warp + 1, 31));
-      S_car = (warp ? sprev : 0ull) + sexc;
-      H_car = __dadd_rn(warp ? hprev : 0.0, hexc);
-      nb_right = min(bexc, warp + 1 < W ? bnext : kInfIdx);
-      nz_right = min(zexc, warp + 1 < W ? znext : kInfIdx);
-      S_total = __shfl_sync(0xffffffffu, ws, W - 1);
-    }
-    v.S_total = S_total;
-    if (!bad_any) {
-#pragma unroll
-      for (int q = 0; q < K; q += 2) {
-        const int k = k0 + q;
-        if (k < n) {
-          const uint32_t o = swz((uint32_t)k);
-          sm<ulonglong2>(v.sr, o) = make_ulonglong2(S_car + spre[q], S_car + spre[q + 1]);
-          sm<double2>(v.hr, o) = make_double2(__dadd_rn(H_car, hpre[q]), __dadd_rn(H_car, hpre[q + 1]));
-        }
-      }
-      if (k0 <= n - 1 && n - 1 < k0 + K) {  // sentinels at slots n, n + 1
-        sm<uint64_t>(v.sr, swz((uint32_t)n)) = S_total;
-        sm<uint64_t>(v.sr, swz((uint32_t)n + 1u)) = ~0ull;
-        sm<double>(v.hr, swz((uint32_t)n)) = __dadd_rn(H_car, hacc);
-      }
-    }
-    __syncthreads();
-
-    if (bad_any || a.dbg == 2) {
-      if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_ERR_INVALID_ARG);
-    } else {
-      if (kPhaseHooks && a.dbg == 3) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
-      // ---------------- phase B0: zero-cost windows -------------------------------------
-      // A run of consecutive h = 0 items (FREE, or EVICTABLE with c = 0) is a zero-cost
-      // window iff its span covers R; the lowest such run head is the answer (exact cost
-      // 0 is the global minimum, R4).  Each thread checks the run heads of its chunk.
-      int zi = kInfIdx, ze = -1, znev = 0;
-      {
-        const int cnt = n - k0;
-        const uint32_t valid = cnt >= K ? (K == 32 ? ~0u : ((1u << K) - 1u)) : (cnt > 0 ? (1u << cnt) - 1u : 0u);
-        const uint32_t zm = valid & ~barmask & ~nzmask;
-        const uint32_t heads = zm & ~(zm << 1);
-        // items that alone cover R (sizes from the prefix registers; the chunk's last
-        // item is left to the span test below)
-        uint32_t cov = 0;
-#pragma unroll
-        for (int q = 0; q + 1 < K; ++q) cov |= (uint32_t)(spre[q + 1] - spre[q] >= v.R) << q;
-        const uint32_t one = heads & cov;  // zero windows [q, q]
-        const uint32_t lower = one ? (1u << (__ffs(one) - 1)) - 1u : ~0u;
-        // heads below the first of them whose run may be longer than one item
-        uint32_t multi = heads & ~one & lower & ((zm >> 1) | (1u << (K - 1)));
-        int zstop = n;
-        while (multi) {
-          const int q = __ffs(multi) - 1;
-          multi &= multi - 1u;
-          const uint32_t mb = barmask >> q, mz = nzmask >> q;
-          const int nb = mb ? k0 + q + __ffs(mb) - 1 : nb_right;
-          const int nz = mz ? k0 + q + __ffs(mz) - 1 : nz_right;
-          const int stop = min(min(nb, nz), n);
-          if (v.S_at(stop) - v.S_at(k0 + q) >= v.R) {
-            zi = k0 + q;
-            zstop = stop;
-            break;
-          }
-        }
-        if (zi == kInfIdx && one) {
-          zi = k0 + __ffs(one) - 1;
-          zstop = zi + 1;
-        }
-        if (zi != kInfIdx) {
-          const uint64_t target = v.S_at(zi) + v.R;
-          int lo = zi + 1, hi = zstop;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (v.S_at(mid) >= target) hi = mid;
-            else lo = mid + 1;
-          }
-          ze = lo;
-          for (int k = zi; k < ze; ++k) znev += (__double_as_longlong(v.v_at(k)) >= 0);
-        }
-      }
-      const int zw = warp_allreduce(zi, [](int x, int y) { return min(x, y); });
-      if (lane == 0) sc.wZ[warp] = zw;
-      __syncthreads();
-      const int zmin = warp_allreduce(lane < W ? sc.wZ[lane] : kInfIdx, [](int x, int y) { return min(x, y); });
-      if (kPhaseHooks && a.dbg == 4) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
-      if (zmin != kInfIdx) {
-        if (zi == zmin) write_result(a.out + p, zi, ze - 1, v.S_at(ze) - v.S_at(zi), 0.0, znev, COOP_OK);
-      } else {
-      // ---------------- phase B1: chunk pruning -------------------------------------------
-      // Thread t's starts i in [k0, kl] have ends e(i) >= e(k0) (monotone) and prefixes
-      // H[i] <= H[kl], so every window cost there is >= H[e(k0)] - H[kl].  e(k0) by one
-      // binary search per thread; the first start's window (when PINNED-free) gives an
-      // upper bound; chunks whose lower bound exceeds the CTA's best upper bound by more
-      // than the filter's margin cannot hold the winner (nor tie it after rounding) and
-      // skip the per-start work.  Bounds: |C^ - C| <= gerr (H^[e] + H^[i]) for any pair.
-      const int kl = min(k0 + K, n) - 1;
-      int e0 = n + 1;
-      double LBt = kInf, Ut = kInf;
-      if (k0 < n && !(barmask & 1u)) {
-        const uint64_t target = S_car + spre[0] + v.R;  // S[k0] + R  (< 2^63)
-        int lo = k0 + 1, hi = n + 1;                    // S[n + 1] = ~0 >= target
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (v.S_at(mid) >= target) hi = mid;
-          else lo = mid + 1;
-        }
-        e0 = lo;
-      } else if (k0 < n) {
-        e0 = -1;  // first start PINNED: no sample; ends of the others found below
-      }
-      if (k0 < n && e0 <= n) {
-        const int nb = barmask ? k0 + __ffs(barmask) - 1 : nb_right;
-        double hl = hpre[0];  // hpre[kl - k0] with constant indices (stays in registers)
-#pragma unroll
-        for (int q = 1; q < K; ++q)
-          if (k0 + q <= kl) hl = hpre[q];
-        const double Hl = __dadd_rn(H_car, hl);
-        if (e0 >= 0) {
-          const double He = v.H_at(e0), Hk = __dadd_rn(H_car, hpre[0]);
-          if (nb >= e0) Ut = (He - Hk) + v.gerr * (He + Hk);
-          LBt = (He - Hl) - v.gerr * (He + Hl);
-        } else {
-          LBt = -kInf;  // no bound without e(k0): keep the chunk
-        }
-      }
-      {
-        const double uw = warp_allreduce(Ut, [](double x, double y) { return fmin(x, y); });
-        if (lane == 0) sc.wP[warp] = uw;
-        if (tid == 0) sc.nsurv = 0;
-      }
-      __syncthreads();
-      const double Upre = warp_allreduce(lane < W ? sc.wP[lane] : kInf,
-                                         [](double x, double y) { return fmin(x, y); });
-      const bool survive = (k0 < n) && (e0 <= n) && !(LBt > Upre * (1.0 + 0x1p-45));
-      {  // compact the surviving chunks (one shared atomic per warp)
-        const uint32_t bal = __ballot_sync(0xffffffffu, survive);
-        int wbase = 0;
-        if (lane == 0 && bal) wbase = atomicAdd(&sc.nsurv, __popc(bal));
-        wbase = __shfl_sync(0xffffffffu, wbase, 0);
-        if (survive)
-          v.list[wbase + __popc(bal & ((1u << lane) - 1u))] =
-              chunk_rec(k0, e0 >= 0 ? e0 : k0 + 1, barmask, nzmask, nb_right, nz_right);
-      }
-      __syncthreads();
-      if (kPhaseHooks && a.dbg == 5) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
-      // every start of the surviving chunks, spread evenly over the CTA's threads
-      const int nslots = sc.nsurv * K;
-      LaneBest bl;
-      bl.U = kInf; bl.L = kInf; bl.L2 = kInf; bl.li = -1; bl.le = -1;
-      bl.xb = ~0ull; bl.xi = kInfIdx; bl.xe = -1;
-      for (int sl = tid; sl < nslots; sl += T)
-        eval_start<0>(v, v.list[sl / K], sl % K, 0.0, 0, 0, sc, bl);
-      const double Uw = warp_allreduce(bl.U, [](double x, double y) { return fmin(x, y); });
-      const uint64_t xw = warp_allreduce(bl.xb, [](uint64_t x, uint64_t y) { return x < y ? x : y; });
-      if (lane == 0) {
-        sc.wU[warp] = Uw;
-        sc.bcost[warp] = xw;
-      }
-      if (tid == 0) sc.ncand = 0;
-      __syncthreads();
-      const double Umin = warp_allreduce(lane < W ? sc.wU[lane] : kInf,
-                                         [](double x, double y) { return fmin(x, y); });
-      const uint64_t xbest = warp_allreduce(lane < W ? sc.bcost[lane] : ~0ull,
-                                            [](uint64_t x, uint64_t y) { return x < y ? x : y; });
-      const double thresh = fmin(Umin, __longlong_as_double((long long)xbest)) * (1.0 + 0x1p-45);
-      if (kPhaseHooks && a.dbg == 6) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
-      // a lane with exactly one start under the threshold appends it; two or more re-walk
-      const bool multi = (bl.L2 <= thresh);
-      if (bl.L <= thresh && !multi) {
-        const int slot = atomicAdd(&sc.ncand, 1);
-        if (slot < kCandCap) sc.cand[slot] = ((uint32_t)bl.li << 16) | (uint32_t)(bl.le - bl.li);
-      }
-      const int xiw = warp_allreduce(bl.xb == xbest ? bl.xi : kInfIdx, [](int x, int y) { return min(x, y); });
-      const int mw = __any_sync(0xffffffffu, multi) ? 1 : 0;
-      if (lane == 0) {
-        sc.bfirst[warp] = xiw;
-        sc.bnev[warp] = mw;
-      }
-      __syncthreads();
-      const int xfirst = warp_allreduce(lane < W ? sc.bfirst[lane] : kInfIdx, [](int x, int y) { return min(x, y); });
-      const int any_multi = warp_allreduce(lane < W ? sc.bnev[lane] : 0, [](int x, int y) { return x | y; });
-      const int nc0 = sc.ncand;
-      const bool x_owner = (xbest != ~0ull) && bl.xi == xfirst && bl.xb == xbest;
-      if (Umin == kInf && xbest == ~0ull) {
-        if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_INFEASIBLE);
-      } else if (nc0 == 0 && !any_multi) {
-        // no window of inexactly known cost can reach the exact best: the owner writes
-        if (x_owner) {
-          int nev = 0;
-          for (int k = bl.xi; k < bl.xe; ++k) nev += (__double_as_longlong(v.v_at(k)) >= 0);
-          write_result(a.out + p, bl.xi, bl.xe - 1, v.S_at(bl.xe) - v.S_at(bl.xi),
-                       __longlong_as_double((long long)xbest), nev, COOP_OK);
-        }
-      } else {
-        // ------------- candidates: exact 192-bit re-summation, RN, (cost, first) min ----
-        if (x_owner) {
-          int nev = 0;
-          for (int k = bl.xi; k < bl.xe; ++k) nev += (__double_as_longlong(v.v_at(k)) >= 0);
-          sc.xend = bl.xe;
-          sc.xnev = nev;
-        }
-        __syncthreads();
-        uint64_t best = xbest;  // meaningful in thread 0
-        int bfirst = xfirst, bend = xbest != ~0ull ? sc.xend : -1, bnev = xbest != ~0ull ? sc.xnev : 0;
-        const bool wmulti = __any_sync(0xffffffffu, bl.L <= thresh);  // this warp holds candidates
-        // rounds: the prebuilt list (no multi), or re-walks restricted to windows of
-        // kCandCap consecutive starts (cannot overflow the list)
-        const int rounds = any_multi ? (n + kCandCap - 1) / kCandCap : 1;
-        for (int rd = 0; rd < rounds; ++rd) {
-          if (any_multi) {
-            __syncthreads();
-            if (tid == 0) sc.ncand = 0;
-            __syncthreads();
-            const int w_lo = rd * kCandCap, w_hi = w_lo + kCandCap;
-            if (wmulti) {
-              LaneBest dummy = bl;
-              for (int sl = tid; sl < nslots; sl += T)
-                eval_start<1>(v, v.list[sl / K], sl % K, thresh, w_lo, w_hi, sc, dummy);
-            }
-            __syncthreads();
-          }
-          const int nc = min(sc.ncand, kCandCap);
-          if (nc <= W) {
-            // few candidates: the whole CTA sums each window (short latency chain)
-            for (int c = 0; c < nc; ++c) {
-              const uint32_t cd = sc.cand[c];
-              const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
-              U192 acc = u192_zero();
-              int nev = 0;
-              if (i + warp * 32 < e) {  // warp-uniform: warps without items skip
-                for (int k = i + tid; k < e; k += T) {
-                  const double hv = v.v_at(k);
-                  nev += (__double_as_longlong(hv) >= 0);
-                  acc = u192_add(acc, u192_from_double(hv));
-                }
-                acc = warp_sum192(acc, nev);
-              }
-              const int par = c & 1;
-              if (lane == 0) {
-                sc.part[par][warp][0] = acc.w0;
-                sc.part[par][warp][1] = acc.w1;
-                sc.part[par][warp][2] = acc.w2;
-                sc.partn[par][warp] = nev;
-              }
-              __syncthreads();
-              if (warp == 0) {
-                U192 t = u192_zero();
-                int tn = 0;
-                if (lane < W) {
-                  t.w0 = sc.part[par][lane][0];
-                  t.w1 = sc.part[par][lane][1];
-                  t.w2 = sc.part[par][lane][2];
-                  tn = sc.partn[par][lane];
-                }
-                t = warp_sum192(t, tn);
-                const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(t));
-                if (lane == 0 && better(cb, i, best, bfirst)) {
-                  best = cb;
-                  bfirst = i;
-                  bend = e;
-                  bnev = tn;
-                }
-              }
-            }
-          } else {
-            // many candidates: one warp per candidate window
-            uint64_t wbest = ~0ull;
-            int32_t wfirst = kInfIdx, wend = -1, wnev = 0;
-            for (int c = warp; c < nc; c += W) {
-              const uint32_t cd = sc.cand[c];
-              const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
-              U192 acc = u192_zero();
-              int nev = 0;
-              for (int k = i + lane; k < e; k += 32) {
-                const double hv = v.v_at(k);
-                nev += (__double_as_longlong(hv) >= 0);
-                acc = u192_add(acc, u192_from_double(hv));
-              }
-              acc = warp_sum192(acc, nev);
-              const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(acc));
-              if (better(cb, i, wbest, wfirst)) {
-                wbest = cb;
-                wfirst = i;
-                wend = e;
-                wnev = nev;
-              }
-            }
-            if (lane == 0) {
-              sc.bcost[warp] = wbest;
-              sc.bfirst[warp] = wfirst;
-              sc.bend[warp] = wend;
-              sc.bnev[warp] = wnev;
-            }
-            __syncthreads();
-            if (tid == 0) {
-              for (int w = 0; w < W; ++w) {
-                if (sc.bend[w] >= 0 && better(sc.bcost[w], sc.bfirst[w], best, bfirst)) {
-                  best = sc.bcost[w];
-                  bfirst = sc.bfirst[w];
-                  bend = sc.bend[w];
-                  bnev = sc.bnev[w];
-                }
-              }
-            }
-          }
-        }
-        if (tid == 0)
-          write_result(a.out + p, bfirst, bend - 1, v.S_at(bend) - v.S_at(bfirst),
-                       __longlong_as_double((long long)best), bnev, COOP_OK);
-      }
+  for (int q = 0; q < K; q += 2) {
+    const int k = k0 + q;
+    if (k < n) sm<ulonglong2>(v.sr, swz((uint32_t)k)) = make_ulonglong2(S_car + spre[q], S_car + spre[q + 1]);
+  }
+  if (k0 <= n - 1 && n - 1 < k0 + K) {  // sentinels at slots n, n + 1
+    sm<uint64_t>(v.sr, swz((uint32_t)n)) = S_total;
+    sm<uint64_t>(v.sr, swz((uint32_t)n + 1u)) = ~0ull;
+  }
+  // ---------------- zero pass: zero-cost windows ----------------------------------------
+  // A run of consecutive h = 0 items is a zero-cost window iff its span covers R; the lowest
+  // such run head is the answer (exact cost 0 is the global minimum, R4).  From registers:
+  // the heads whose own item covers R; heads of runs that go on past the head (never on the
+  // config-4 law) are settled below from S.
+  const bool cont = (k0 + K < n) && (zmk16[tid + 1] & 1u);  // item k0 + K is h = 0
+  const uint32_t heads = zm & ~(zm << 1);
+  uint32_t one = 0;
+  {
+    uint32_t hm = heads;
+    while (hm) {  // ~1 head per chunk; stop at the first whose own item covers R
+      const int q = __ffs(hm) - 1;
+      hm &= hm - 1u;
+      // S of this thread's own items was just stored by this thread (program order)
+      const uint64_t nxt = q == K - 1 ? S_car + sacc : v.S_at(k0 + q + 1);
+      if (nxt - v.S_at(k0 + q) >= v.R) {
+        one = 1u << q;
+        break;
       }
     }
   }
+  const uint32_t below = one ? one - 1u : kFull;
+  const uint32_t multi = heads & below & ~one & ((zm >> 1) | (cont ? (1u << (K - 1)) : 0u));
+  const int zi1 = one ? k0 + __ffs(one) - 1 : kInfIdx;
+  const int zmh = multi ? k0 + __ffs(multi) - 1 : kInfIdx;
+  {
+    const int a1 = wmin_i32(zi1);
+    const int a2 = wmin_i32(zmh);
+    if (lane == 0) {
+      sc.zW[warp] = a1;
+      sc.zM[warp] = a2;
+    }
+  }
+  __syncthreads();
+  int zmin = wmin_i32(lane < W ? sc.zW[lane] : kInfIdx);
+  const int mmin = wmin_i32(lane < W ? sc.zM[lane] : kInfIdx);
+  if (mmin < zmin) {  // CTA-uniform, rare: runs of several h = 0 items below the best single one
+    int zi2 = kInfIdx;
+    uint32_t mm = multi;
+    while (mm) {
+      const int q = __ffs(mm) - 1;
+      mm &= mm - 1u;
+      if (k0 + q >= zmin) break;
+      const int stop = zero_run_stop(zmk16, tid, q, K, n);
+      if (v.S_at(stop) - v.S_at(k0 + q) >= v.R) {
+        zi2 = k0 + q;
+        break;
+      }
+    }
+    const int a2 = wmin_i32(zi2);
+    if (lane == 0) sc.zW2[warp] = a2;
+    __syncthreads();
+    zmin = min(zmin, wmin_i32(lane < W ? sc.zW2[lane] : kInfIdx));
+  }
+  if (kPhaseHooks && a.dbg == 4) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
+  if (zmin != kInfIdx) {
+    if (zmin >= k0 && zmin < k0 + K) {  // the owner of the winning head writes the window
+      const uint64_t target = v.S_at(zmin) + v.R;
+      int lo = zmin + 1, hi = zero_run_stop(zmk16, tid, zmin - k0, K, n);
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (v.S_at(mid) >= target) hi = mid;
+        else lo = mid + 1;
+      }
+      int znev = 0;
+      for (int k = zmin; k < lo; ++k) znev += (sc.evc[k / K] >> (k % K)) & 1;
+      write_result(a.out + p, zmin, lo - 1, v.S_at(lo) - v.S_at(zmin), 0.0, znev, COOP_OK);
+    }
+    return;
+  }
+  // ---------------- phase 2: carries of H^ and of the next-PINNED index -------------------
+  int32_t nb_right;
+  {
+    double wh = lane < W ? sc.wH[lane] : 0.0;
+    int32_t wb = lane < W ? sc.wF[lane] : kInfIdx;
+#pragma unroll
+    for (int d = 1; d < kMaxWarps; d <<= 1) {
+      const double ho = __shfl_up_sync(0xffffffffu, wh, d);
+      const int32_t bo = __shfl_down_sync(0xffffffffu, wb, d);
+      if (lane >= d) wh = __dadd_rn(ho, wh);
+      if (lane + d < 32) wb = min(wb, bo);
+    }
+    const double hprev = __shfl_sync(0xffffffffu, wh, warp ? warp - 1 : 0);
+    const int32_t bnext = __shfl_sync(0xffffffffu, wb, min(warp + 1, 31));
+    const double H_car = __dadd_rn(warp ? hprev : 0.0, hexc);
+    nb_right = min(bexc, warp + 1 < W ? bnext : kInfIdx);
+#pragma unroll
+    for (int q = 0; q < K; q += 2) {
+      const int k = k0 + q;
+      if (k < n) {
+        const uint32_t o = swz((uint32_t)k);
+        const double2 hl = sm<double2>(v.hr, o);
+        sm<double2>(v.hr, o) = make_double2(__dadd_rn(H_car, hl.x), __dadd_rn(H_car, hl.y));
+      }
+    }
+    if (k0 <= n - 1 && n - 1 < k0 + K) sm<double>(v.hr, swz((uint32_t)n)) = __dadd_rn(H_car, hacc);
+  }
+  __syncthreads();
+  if (kPhaseHooks && a.dbg == 3) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
+  // ---------------- phase B1: chunk pruning -------------------------------------------
+  // Thread t's starts i in [k0, kl] have ends e(i) >= e(k0) (monotone) and prefixes
+  // H[i] <= H[kl], so every window cost there is >= H[e(k0)] - H[kl].  e(k0) by one binary
+  // search per thread; the first start's window (when PINNED-free) gives an upper bound;
+  // chunks whose lower bound exceeds the CTA's best upper bound by more than the margin
+  // cannot hold the winner (nor tie it after rounding) and skip the per-start work.
+  const int kl = min(k0 + K, n) - 1;
+  int e0 = n + 1;
+  double LBt = kInf, Ut = kInf;
+  if (k0 < n && !(barmask & 1u)) {
+    const uint64_t target = Sk0 + v.R;  // S[k0] + R  (< 2^63)
+    int lo = k0 + 1, hi = n + 1;        // S[n + 1] = ~0 >= target
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (v.S_at(mid) >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    e0 = lo;
+  } else if (k0 < n) {
+    e0 = -1;  // first start PINNED: no sample; ends of the others found below
+  }
+  if (k0 < n && e0 <= n) {
+    const int nb = barmask ? k0 + __ffs(barmask) - 1 : nb_right;
+    const double Hl = v.H_at(kl);
+    if (e0 >= 0) {
+      const double He = v.H_at(e0), Hk = v.H_at(k0);
+      if (nb >= e0) Ut = (He - Hk) + v.gerr * (He + Hk);
+      LBt = (He - Hl) - v.gerr * (He + Hl);
+    } else {
+      LBt = -kInf;  // no bound without e(k0): keep the chunk
+    }
+  }
+  {
+    const double uw = wmin_f64(Ut);
+    if (lane == 0) sc.wP[warp] = uw;
+    if (tid == 0) sc.nsurv = 0;
+  }
+  __syncthreads();
+  const double Upre = wmin_f64(lane < W ? sc.wP[lane] : kInf);
+  const bool survive = (k0 < n) && (e0 <= n) && !(LBt > Upre * (1.0 + 0x1p-45));
+  {  // compact the surviving chunks (one shared atomic per warp)
+    const uint32_t bal = __ballot_sync(0xffffffffu, survive);
+    int wbase = 0;
+    if (lane == 0 && bal) wbase = atomicAdd(&sc.nsurv, __popc(bal));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (survive)
+      v.list[wbase + __popc(bal & ((1u << lane) - 1u))] = chunk_rec(k0, e0 >= 0 ? e0 : k0 + 1, barmask, nb_right);
+  }
+  __syncthreads();
+  if (kPhaseHooks && a.dbg == 5) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
+  // ---------------- phase B2: filter every start of the surviving chunks ---------------
+  // (spread evenly over the CTA's threads, not left to the owner threads)
+  const int nslots = sc.nsurv * K;
+  LaneBest bl;
+  bl.U = kInf; bl.L = kInf; bl.L2 = kInf; bl.li = -1; bl.le = -1;
+  for (int sl = tid; sl < nslots; sl += T)
+    eval_start<0>(v, v.list[sl / K], sl % K, 0.0, 0, 0, sc, bl);
+  {
+    const double Uw = wmin_f64(bl.U);
+    if (lane == 0) sc.wU[warp] = Uw;
+    if (tid == 0) sc.ncand = 0;
+  }
+  __syncthreads();
+  const double Umin = wmin_f64(lane < W ? sc.wU[lane] : kInf);
+  if (kPhaseHooks && a.dbg == 6) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
+  if (Umin == kInf) {  // no PINNED-free window covers R
+    if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, COOP_INFEASIBLE);
+    return;
+  }
+  const double thresh = Umin * (1.0 + 0x1p-45);
+  // a lane with exactly one start under the threshold appends it; two or more re-walk
+  const bool multi_l = (bl.L2 <= thresh);
+  if (bl.L <= thresh && !multi_l) {
+    const int slot = atomicAdd(&sc.ncand, 1);
+    if (slot < kCandCap) sc.cand[slot] = ((uint32_t)bl.li << 16) | (uint32_t)(bl.le - bl.li);
+  }
+  const int any_multi = __syncthreads_or(multi_l);
+  // ------------- candidates: exact 192-bit re-summation, RN, (cost, first) min ----
+  uint64_t best = ~0ull;  // meaningful in thread 0
+  int bfirst = kInfIdx, bend = -1, bnev = 0;
+  const bool wmulti = __any_sync(0xffffffffu, bl.L <= thresh);  // this warp holds candidates
+  // rounds: the prebuilt list (no multi), or re-walks restricted to windows of kCandCap
+  // consecutive starts (cannot overflow the list)
+  const int rounds = any_multi ? (n + kCandCap - 1) / kCandCap : 1;
+  for (int rd = 0; rd < rounds; ++rd) {
+    if (any_multi) {
+      __syncthreads();
+      if (tid == 0) sc.ncand = 0;
+      __syncthreads();
+      const int w_lo = rd * kCandCap, w_hi = w_lo + kCandCap;
+      if (wmulti) {
+        LaneBest dummy = bl;
+        for (int sl = tid; sl < nslots; sl += T)
+          eval_start<1>(v, v.list[sl / K], sl % K, thresh, w_lo, w_hi, sc, dummy);
+      }
+      __syncthreads();
+    }
+    const int nc = min(sc.ncand, kCandCap);
+    if (nc <= W) {
+      // few candidates: the whole CTA sums each window (short latency chain)
+      for (int c = 0; c < nc; ++c) {
+        const uint32_t cd = sc.cand[c];
+        const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
+        U192 acc = u192_zero();
+        int nev = 0;
+        if (i + warp * 32 < e) {  // warp-uniform: warps without items skip
+          window_sum<K>(v, i, e, tid, T, acc, nev);
+          acc = warp_sum192(acc, nev);
+        }
+        const int par = c & 1;
+        if (lane == 0) {
+          sc.part[par][warp][0] = acc.w0;
+          sc.part[par][warp][1] = acc.w1;
+          sc.part[par][warp][2] = acc.w2;
+          sc.partn[par][warp] = nev;
+        }
+        __syncthreads();
+        if (warp == 0) {
+          U192 t = u192_zero();
+          int tn = 0;
+          if (lane < W) {
+            t.w0 = sc.part[par][lane][0];
+            t.w1 = sc.part[par][lane][1];
+            t.w2 = sc.part[par][lane][2];
+            tn = sc.partn[par][lane];
+          }
+          t = warp_sum192(t, tn);
+          const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(t));
+          if (lane == 0 && better(cb, i, best, bfirst)) {
+            best = cb;
+            bfirst = i;
+            bend = e;
+            bnev = tn;
+          }
+        }
+      }
+    } else {
+      // many candidates: one warp per candidate window
+      uint64_t wbest = ~0ull;
+      int32_t wfirst = kInfIdx, wend = -1, wnev = 0;
+      for (int c = warp; c < nc; c += W) {
+        const uint32_t cd = sc.cand[c];
+        const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
+        U192 acc = u192_zero();
+        int nev = 0;
+        window_sum<K>(v, i, e, lane, 32, acc, nev);
+        acc = warp_sum192(acc, nev);
+        const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(acc));
+        if (better(cb, i, wbest, wfirst)) {
+          wbest = cb;
+          wfirst = i;
+          wend = e;
+          wnev = nev;
+        }
+      }
+      if (lane == 0) {
+        sc.bcost[warp] = wbest;
+        sc.bfirst[warp] = wfirst;
+        sc.bend[warp] = wend;
+        sc.bnev[warp] = wnev;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 0; w < W; ++w) {
+          if (sc.bend[w] >= 0 && better(sc.bcost[w], sc.bfirst[w], best, bfirst)) {
+            best = sc.bcost[w];
+            bfirst = sc.bfirst[w];
+            bend = sc.bend[w];
+            bnev = sc.bnev[w];
+          }
+        }
+      }
+    }
+  }
+  if (tid == 0)
+    write_result(a.out + p, bfirst, bend - 1, v.S_at(bend) - v.S_at(bfirst),
+                 __longlong_as_double((long long)best), bnev, COOP_OK);
 }
 
 template <int K, int MAXT, int MINB>
@@ -906,7 +937,7 @@ int launch_k(const Args &a0, cudaStream_t st) {
   const int threads = ((a.n + K - 1) / K + 31) / 32 * 32;
   const int W = threads / 32;
   (void)W;  // summation depth of any H^ entry <= K + 5 (warp) + 4 (cross-warp) + 2 < K + 32
-  a.gerr = 2.0 * (double)(K + 32) * 0x1p-53 + 0x1p-50;
+  a.gerr = 2.0 * (double)(K + 32) * 0x1p-53 + 0x1p-50 + 0x1p-43;  // + 2 x 2^-44 for h^ (rcp_nr)
 
   int dev = 0;
   cudaGetDevice(&dev);
@@ -975,10 +1006,10 @@ int launch_window_search_cta(const coop_tables_soa *t, const uint64_t *requests,
   a.n = t->n_blocks;
   a.pending = pending ? 1 : 0;
   if (a.n_pools == 0) return COOP_OK;
-  const char *two = getenv("COOP_SEARCH_TWO_CTA");  // profiling hook: 2 CTAs/SM, 1 stage
-  if (two && two[0] == '1' && a.n <= 4096) return launch_k<16, 256, 2>(a, st);
-  if (a.n <= 2048) return launch_k<8, 256, 2>(a, st);  // 2 CTAs per SM
-  if (a.n <= 4096) return launch_k<8, 512, 2>(a, st);  // 2 CTAs per SM, 1 stage each
+  const char *cfg = getenv("COOP_SEARCH_CFG");  // profiling hook: "8x512" = K 8, 512 threads
+  if (cfg && strcmp(cfg, "8x512") == 0 && a.n <= 4096) return launch_k<8, 512, 2>(a, st);
+  if (a.n <= 2048) return launch_k<8, 256, 2>(a, st);   // 2 CTAs per SM
+  if (a.n <= 4096) return launch_k<16, 256, 2>(a, st);  // 2 CTAs per SM, 1 stage each
   return launch_k<16, 512, 1>(a, st);
 }
 

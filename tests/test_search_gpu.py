@@ -249,3 +249,55 @@ def test_stream_kernel_parity(n, monkeypatch):
         P = 256
         ss, c, s, r = G.bench_pools_host(G.MODE_BENCH, 3, 5000, P, n)
         assert_same(gpu_search(ss, c, s, r, P, n, n), O.search_many(ss, c, s, r, P, n, n), "stream bench law")
+
+
+def _edge_values():
+    """(c, s) pairs on and around every R7 boundary: c = +-0, subnormal c, h underflowing
+    to 0 (valid zero item), h = 2^-64 exactly and one ulp below, h just below / at 2^60,
+    huge s, non-finite or negative c, s < 1, plus random pairs straddling both h bounds."""
+    nb = np.nextafter
+    v = [(0.0, 1.0), (-0.0, 1.0), (-0.0, 0.5), (0.0, np.nan), (0.0, np.inf),
+         (5e-324, 1.0), (5e-324, 3.0), (1e-300, 1e300), (2.0 ** -64, 1.0),
+         (nb(2.0 ** -64, 0.0), 1.0), (2.0 ** -63, 2.0), (nb(2.0 ** -63, 0.0), 2.0),
+         (1.5 * 2.0 ** -64, 1.5), (2.0 ** 60, 1.0), (nb(2.0 ** 60, 0.0), 1.0), (2.0 ** 61, 2.0),
+         (1.0, 2.0 ** 1000), (2.0 ** 1000, 2.0 ** 1022), (2.0 ** 1023, 1.5), (np.inf, 1.0),
+         (np.nan, 1.0), (-1.0, 1.0), (1.0, 0.999), (1.0, -1.0), (1.0, 5e-324),
+         (2.0 ** -1022, 1.0), (3.0, 3.0)]
+    rng = np.random.default_rng(17)
+    for _ in range(24):
+        v.append((float(2.0 ** rng.uniform(-70, -58)), float(rng.uniform(1, 4))))
+        v.append((float(2.0 ** rng.uniform(55, 63)), float(rng.uniform(1, 8))))
+    return v
+
+
+@pytest.mark.parametrize("n", [64, 4096])
+def test_r7_domain_edges(n):
+    """Validation (R7) and zero-ness of h decided without a division where the exponents
+    allow and exactly elsewhere: bit-identical to O1 on every edge value, at several item
+    positions (chunk starts / ends), as a lone large item (zero window iff h == 0), and with
+    garbage c / s on FREE and PINNED items (ignored)."""
+    rng = np.random.default_rng(n)
+    pools, reqs = [], []
+    for ci, (cv, sv) in enumerate(_edge_values()):
+        for pos in (0, 7, 8, 15, n // 2 + 3, n - 1):
+            ss, c, s = G.random_pool(rng, n, p_free=0.0, p_pinned=0.02, max_size=64)
+            sizes = ss & np.uint64((1 << 62) - 1)
+            sizes[pos] = 1 << 20
+            states = np.where((ss >> np.uint64(62)) == 2, 2, 1)
+            states[pos] = 1
+            ss = G.pack(sizes, states)
+            c[pos], s[pos] = cv, sv
+            # garbage on non-evictable items must be ignored
+            j = (pos + 5) % n
+            ss[j] = G.pack([3], [ci % 2 * 2])[0]
+            c[j], s[j] = (np.nan, -1.0) if ci % 3 else (-5.0, 0.25)
+            pools.append((ss, c, s))
+            reqs.append((1 << 20) if ci % 2 else int(rng.integers(1, 200)))
+    SS, C, S = G.stack_pools(pools, n)
+    req = np.array(reqs, np.uint64)
+    g = gpu_search(SS, C, S, req, len(pools), n, n)
+    o = O.search_many(SS, C, S, req, len(pools), n, n)
+    assert_same(g, o, f"R7 edges n={n}")
+    st = o["status"]
+    assert (st == O.INVALID_ARG).sum() > 20 and (st == O.OK).sum() > 20
+    assert ((st == O.OK) & (o["cost"] == 0.0) & (o["span"] >= (1 << 20))).sum() > 5  # underflow zeros
