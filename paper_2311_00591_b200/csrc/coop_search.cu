@@ -58,6 +58,7 @@ struct Scratch {
     };
   };
   int32_t partn[2][kMaxWarps];
+  uint64_t pspan[2][kMaxWarps];
   uint64_t bcost[kMaxWarps];
   int32_t bfirst[kMaxWarps];
   int32_t bend[kMaxWarps];
@@ -67,6 +68,7 @@ struct Scratch {
   uint16_t evc[kMaxWarps * 32];  // per chunk: EVICTABLE mask (exact re-summation, n_evict)
   uint32_t cand[kCandCap];
   unsigned long long mbar[2];
+  int64_t dpool;  // pool whose candidates wait for the deferred exact re-summation (-1: none)
   int32_t nplist;                      // pending mode: pools of the chunk to finish
   int16_t plist[kMaxWarps * 32];
 };
@@ -128,6 +130,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// CTA barriers (named barrier 1, T threads).
+__device__ __forceinline__ void cbar(int T) { asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory"); }
+__device__ __forceinline__ int cbar_or(int pred, int T) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %1, 0;\n\t"
+      "bar.red.or.pred p, 1, %2, p;\n\tselp.s32 %0, 1, 0, p;\n\t}"
+      : "=r"(r)
+      : "r"(pred), "r"(T)
+      : "memory");
+  return r;
+}
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
                                             int c2, uint32_t bar) {
   asm volatile(
@@ -151,9 +168,9 @@ __device__ __forceinline__ void issue_stage(const Args &a, const CUtensorMap *m_
 }
 
 // Fallback staging for layouts the TMA map cannot describe (plain coalesced loads).
-__device__ __forceinline__ void stage_plain(const Args &a, smem_t *stage, int64_t p) {
+__device__ __forceinline__ void stage_plain(const Args &a, smem_t *stage, int64_t p, int T) {
   const int64_t base = p * a.stride;
-  for (int k = threadIdx.x; k < a.n; k += blockDim.x) {
+  for (int k = threadIdx.x; k < a.n; k += T) {
     const uint32_t o = swz((uint32_t)k);
     sm<uint64_t>(stage, o) = a.ss[base + k];
     sm<double>(stage, a.region_bytes + o) = a.cost[base + k];
@@ -241,18 +258,128 @@ __device__ __forceinline__ double rcp_nr(double s) {
   return __fma_rn(r, e, r);
 }
 
-// Exact cost of the window [i, e) (R3): h = c/s (IEEE RN, R1) of its EVICTABLE items --
-// FREE items add 0, a window never holds a PINNED one -- summed in 192-bit fixed point over
-// the items i + off, i + off + step, ...; counts the EVICTABLE items (n_evict).
-template <int K>
-__device__ __forceinline__ void window_sum(const PoolView &v, int i, int e, int off, int step,
-                                           U192 &acc, int &nev) {
+// Exact cost of the window [i, e) of pool p (R3): h = c/s (IEEE RN, R1) of its EVICTABLE
+// items -- FREE items add 0, a window never holds a PINNED one -- summed in 192-bit fixed
+// point over the items i + off, i + off + step, ...; also the span and the EVICTABLE count
+// (n_evict).  Read from global memory: the stage may already hold the next pool.
+__device__ __forceinline__ void window_sum(const Args &a, int64_t p, int i, int e, int off,
+                                           int step, U192 &acc, uint64_t &span, int &nev) {
+  const uint64_t *ss = a.ss + p * a.stride;
+  const double *cg = a.cost + p * a.stride, *sg = a.stale + p * a.stride;
   for (int k = i + off; k < e; k += step) {
-    if ((v.evc[k / K] >> (k % K)) & 1u) {
-      acc = u192_add(acc, u192_from_double(__ddiv_rn(v.c_at(k), v.sg[k])));
+    const uint64_t w = __ldg(ss + k);
+    const double c = __ldg(cg + k), s = __ldg(sg + k);
+    span += w & ((1ull << 62) - 1ull);
+    if ((w >> 62) == COOP_EVICTABLE) {
+      acc = u192_add(acc, u192_from_double(__ddiv_rn(c, s)));
       ++nev;
     }
   }
+}
+
+__device__ __forceinline__ void warp_sum_all(U192 &acc, uint64_t &span, int &nev) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    acc = u192_add(acc, U192{__shfl_xor_sync(0xffffffffu, acc.w0, d), __shfl_xor_sync(0xffffffffu, acc.w1, d),
+                             __shfl_xor_sync(0xffffffffu, acc.w2, d)});
+    span += __shfl_xor_sync(0xffffffffu, span, d);
+    nev += __shfl_xor_sync(0xffffffffu, nev, d);
+  }
+}
+
+// The exact re-summation of the candidate windows sc.cand[0, nc) of pool p by the whole CTA
+// and the pool's result: the lexicographic (rounded exact cost bits, first) minimum.
+template <int K>
+__device__ __forceinline__ void verify_pool(const Args &a, Scratch &sc, int64_t p, int nc, int T) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
+  uint64_t best = ~0ull, bspan = 0;  // meaningful in thread 0
+  int bfirst = kInfIdx, bend = -1, bnev = 0;
+  if (nc <= W) {
+    // few candidates: the whole CTA sums each window (short latency chain)
+    for (int c = 0; c < nc; ++c) {
+      const uint32_t cd = sc.cand[c];
+      const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
+      U192 acc = u192_zero();
+      uint64_t span = 0;
+      int nev = 0;
+      if (i + warp * 32 < e) {  // warp-uniform: warps without items skip
+        window_sum(a, p, i, e, tid, T, acc, span, nev);
+        warp_sum_all(acc, span, nev);
+      }
+      const int par = c & 1;
+      if (lane == 0) {
+        sc.part[par][warp][0] = acc.w0;
+        sc.part[par][warp][1] = acc.w1;
+        sc.part[par][warp][2] = acc.w2;
+        sc.partn[par][warp] = nev;
+        sc.pspan[par][warp] = span;
+      }
+      cbar(T);
+      if (warp == 0) {
+        U192 t = u192_zero();
+        uint64_t tsp = 0;
+        int tn = 0;
+        if (lane < W) {
+          t.w0 = sc.part[par][lane][0];
+          t.w1 = sc.part[par][lane][1];
+          t.w2 = sc.part[par][lane][2];
+          tn = sc.partn[par][lane];
+          tsp = sc.pspan[par][lane];
+        }
+        warp_sum_all(t, tsp, tn);
+        const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(t));
+        if (lane == 0 && better(cb, i, best, bfirst)) {
+          best = cb;
+          bfirst = i;
+          bend = e;
+          bnev = tn;
+          bspan = tsp;
+        }
+      }
+    }
+  } else {
+    // many candidates: one warp per candidate window
+    uint64_t wbest = ~0ull, wspan = 0;
+    int32_t wfirst = kInfIdx, wend = -1, wnev = 0;
+    for (int c = warp; c < nc; c += W) {
+      const uint32_t cd = sc.cand[c];
+      const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
+      U192 acc = u192_zero();
+      uint64_t span = 0;
+      int nev = 0;
+      window_sum(a, p, i, e, lane, 32, acc, span, nev);
+      warp_sum_all(acc, span, nev);
+      const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(acc));
+      if (better(cb, i, wbest, wfirst)) {
+        wbest = cb;
+        wfirst = i;
+        wend = e;
+        wnev = nev;
+        wspan = span;
+      }
+    }
+    if (lane == 0) {
+      sc.bcost[warp] = wbest;
+      sc.bfirst[warp] = wfirst;
+      sc.bend[warp] = wend;
+      sc.bnev[warp] = wnev;
+      sc.pspan[0][warp] = wspan;
+    }
+    cbar(T);
+    if (tid == 0) {
+      for (int w = 0; w < W; ++w) {
+        if (sc.bend[w] >= 0 && better(sc.bcost[w], sc.bfirst[w], best, bfirst)) {
+          best = sc.bcost[w];
+          bfirst = sc.bfirst[w];
+          bend = sc.bend[w];
+          bnev = sc.bnev[w];
+          bspan = sc.pspan[0][w];
+        }
+      }
+    }
+  }
+  if (tid == 0) write_result(a.out + p, bfirst, bend - 1, bspan, __longlong_as_double((long long)best), bnev, COOP_OK);
+  cbar(T);  // sc.cand / sc.part free again
 }
 
 // Per-thread running state of the filter.
@@ -505,7 +632,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     sc.wS[warp] = sinc;
     sc.wH[warp] = hinc;
   }
-  const int bad_any = __syncthreads_or(bad);
+  const int bad_any = cbar_or(bad, T);
   uint64_t S_car, S_total;
   {
     uint64_t ws = lane < W ? sc.wS[lane] : 0ull;
@@ -566,7 +693,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
       sc.zM[warp] = a2;
     }
   }
-  __syncthreads();
+  cbar(T);
   int zmin = wmin_i32(lane < W ? sc.zW[lane] : kInfIdx);
   const int mmin = wmin_i32(lane < W ? sc.zM[lane] : kInfIdx);
   if (mmin < zmin) {  // CTA-uniform, rare: runs of several h = 0 items below the best single one
@@ -584,7 +711,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     }
     const int a2 = wmin_i32(zi2);
     if (lane == 0) sc.zW2[warp] = a2;
-    __syncthreads();
+    cbar(T);
     zmin = min(zmin, wmin_i32(lane < W ? sc.zW2[lane] : kInfIdx));
   }
   if (kPhaseHooks && a.dbg == 4) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
@@ -630,7 +757,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     }
     if (k0 <= n - 1 && n - 1 < k0 + K) sm<double>(v.hr, swz((uint32_t)n)) = __dadd_rn(H_car, hacc);
   }
-  __syncthreads();
+  cbar(T);
   if (kPhaseHooks && a.dbg == 3) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
   // ---------------- phase B1: chunk pruning -------------------------------------------
   // Thread t's starts i in [k0, kl] have ends e(i) >= e(k0) (monotone) and prefixes
@@ -669,7 +796,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     if (lane == 0) sc.wP[warp] = uw;
     if (tid == 0) sc.nsurv = 0;
   }
-  __syncthreads();
+  cbar(T);
   const double Upre = wmin_f64(lane < W ? sc.wP[lane] : kInf);
   const bool survive = (k0 < n) && (e0 <= n) && !(LBt > Upre * (1.0 + 0x1p-45));
   {  // compact the surviving chunks (one shared atomic per warp)
@@ -680,7 +807,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     if (survive)
       v.list[wbase + __popc(bal & ((1u << lane) - 1u))] = chunk_rec(k0, e0 >= 0 ? e0 : k0 + 1, barmask, nb_right);
   }
-  __syncthreads();
+  cbar(T);
   if (kPhaseHooks && a.dbg == 5) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
   // ---------------- phase B2: filter every start of the surviving chunks ---------------
   // (spread evenly over the CTA's threads, not left to the owner threads)
@@ -694,7 +821,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     if (lane == 0) sc.wU[warp] = Uw;
     if (tid == 0) sc.ncand = 0;
   }
-  __syncthreads();
+  cbar(T);
   const double Umin = wmin_f64(lane < W ? sc.wU[lane] : kInf);
   if (kPhaseHooks && a.dbg == 6) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
   if (Umin == kInf) {  // no PINNED-free window covers R
@@ -708,107 +835,44 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     const int slot = atomicAdd(&sc.ncand, 1);
     if (slot < kCandCap) sc.cand[slot] = ((uint32_t)bl.li << 16) | (uint32_t)(bl.le - bl.li);
   }
-  const int any_multi = __syncthreads_or(multi_l);
-  // ------------- candidates: exact 192-bit re-summation, RN, (cost, first) min ----
-  uint64_t best = ~0ull;  // meaningful in thread 0
-  int bfirst = kInfIdx, bend = -1, bnev = 0;
+  const int any_multi = cbar_or(multi_l, T);
+  if (!any_multi) {
+    // the usual case: the candidates' exact re-summation reads global memory only, so it is
+    // deferred until this CTA has released the stage and started the next pool's load
+    if (tid == 0) sc.dpool = p;
+    return;
+  }
+  // rare: some thread holds two or more candidates -- re-walk, restricted to windows of
+  // kCandCap consecutive starts (cannot overflow the list), and verify round by round
   const bool wmulti = __any_sync(0xffffffffu, bl.L <= thresh);  // this warp holds candidates
-  // rounds: the prebuilt list (no multi), or re-walks restricted to windows of kCandCap
-  // consecutive starts (cannot overflow the list)
-  const int rounds = any_multi ? (n + kCandCap - 1) / kCandCap : 1;
-  for (int rd = 0; rd < rounds; ++rd) {
-    if (any_multi) {
-      __syncthreads();
-      if (tid == 0) sc.ncand = 0;
-      __syncthreads();
-      const int w_lo = rd * kCandCap, w_hi = w_lo + kCandCap;
-      if (wmulti) {
-        LaneBest dummy = bl;
-        for (int sl = tid; sl < nslots; sl += T)
-          eval_start<1>(v, v.list[sl / K], sl % K, thresh, w_lo, w_hi, sc, dummy);
-      }
-      __syncthreads();
+  uint64_t best = ~0ull, bspan = 0;  // meaningful in thread 0
+  int bfirst = kInfIdx, blast = -1, bnev = 0;
+  for (int w_lo = 0; w_lo < n; w_lo += kCandCap) {
+    cbar(T);
+    if (tid == 0) sc.ncand = 0;
+    cbar(T);
+    if (wmulti) {
+      LaneBest dummy = bl;
+      for (int sl = tid; sl < nslots; sl += T)
+        eval_start<1>(v, v.list[sl / K], sl % K, thresh, w_lo, w_lo + kCandCap, sc, dummy);
     }
+    cbar(T);
     const int nc = min(sc.ncand, kCandCap);
-    if (nc <= W) {
-      // few candidates: the whole CTA sums each window (short latency chain)
-      for (int c = 0; c < nc; ++c) {
-        const uint32_t cd = sc.cand[c];
-        const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
-        U192 acc = u192_zero();
-        int nev = 0;
-        if (i + warp * 32 < e) {  // warp-uniform: warps without items skip
-          window_sum<K>(v, i, e, tid, T, acc, nev);
-          acc = warp_sum192(acc, nev);
-        }
-        const int par = c & 1;
-        if (lane == 0) {
-          sc.part[par][warp][0] = acc.w0;
-          sc.part[par][warp][1] = acc.w1;
-          sc.part[par][warp][2] = acc.w2;
-          sc.partn[par][warp] = nev;
-        }
-        __syncthreads();
-        if (warp == 0) {
-          U192 t = u192_zero();
-          int tn = 0;
-          if (lane < W) {
-            t.w0 = sc.part[par][lane][0];
-            t.w1 = sc.part[par][lane][1];
-            t.w2 = sc.part[par][lane][2];
-            tn = sc.partn[par][lane];
-          }
-          t = warp_sum192(t, tn);
-          const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(t));
-          if (lane == 0 && better(cb, i, best, bfirst)) {
-            best = cb;
-            bfirst = i;
-            bend = e;
-            bnev = tn;
-          }
-        }
-      }
-    } else {
-      // many candidates: one warp per candidate window
-      uint64_t wbest = ~0ull;
-      int32_t wfirst = kInfIdx, wend = -1, wnev = 0;
-      for (int c = warp; c < nc; c += W) {
-        const uint32_t cd = sc.cand[c];
-        const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
-        U192 acc = u192_zero();
-        int nev = 0;
-        window_sum<K>(v, i, e, lane, 32, acc, nev);
-        acc = warp_sum192(acc, nev);
-        const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(acc));
-        if (better(cb, i, wbest, wfirst)) {
-          wbest = cb;
-          wfirst = i;
-          wend = e;
-          wnev = nev;
-        }
-      }
-      if (lane == 0) {
-        sc.bcost[warp] = wbest;
-        sc.bfirst[warp] = wfirst;
-        sc.bend[warp] = wend;
-        sc.bnev[warp] = wnev;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        for (int w = 0; w < W; ++w) {
-          if (sc.bend[w] >= 0 && better(sc.bcost[w], sc.bfirst[w], best, bfirst)) {
-            best = sc.bcost[w];
-            bfirst = sc.bfirst[w];
-            bend = sc.bend[w];
-            bnev = sc.bnev[w];
-          }
-        }
+    if (nc == 0) continue;
+    verify_pool<K>(a, sc, p, nc, T);  // writes this round's best into out[p]
+    if (tid == 0) {
+      const coop_window r = a.out[p];
+      const uint64_t cb = (uint64_t)__double_as_longlong(r.cost);
+      if (better(cb, r.first, best, bfirst)) {
+        best = cb;
+        bfirst = r.first;
+        blast = r.last;
+        bspan = r.span;
+        bnev = r.n_evict;
       }
     }
   }
-  if (tid == 0)
-    write_result(a.out + p, bfirst, bend - 1, v.S_at(bend) - v.S_at(bfirst),
-                 __longlong_as_double((long long)best), bnev, COOP_OK);
+  if (tid == 0) write_result(a.out + p, bfirst, blast, bspan, __longlong_as_double((long long)best), bnev, COOP_OK);
 }
 
 template <int K, int MAXT, int MINB>
@@ -823,16 +887,15 @@ __global__ void __launch_bounds__(MAXT, MINB)
   uint4 *Ebuf = reinterpret_cast<uint4 *>(base_ptr + (size_t)a.stages * a.stage_bytes +
                                                  (sizeof(Scratch) + 15) / 16 * 16);
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int T = blockDim.x, W = T >> 5;
-  const int n = a.n;
-  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const int tid = threadIdx.x;
+  const int T = blockDim.x;
 
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) mbar_init(smem_u32(&sc.mbar[s]), 1);
+    sc.dpool = -1;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  cbar(T);
   if (a.use_tma && tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
       const int64_t p = (int64_t)blockIdx.x + (int64_t)s * gridDim.x;
@@ -846,45 +909,57 @@ __global__ void __launch_bounds__(MAXT, MINB)
     // second pass after the streaming kernel: only the pools it marked COOP_PENDING_;
     // chunks of T pools are scanned with one status read per thread, plain staging
     for (int64_t c0 = (int64_t)blockIdx.x * T; c0 < a.n_pools; c0 += (int64_t)gridDim.x * T) {
-      __syncthreads();
+      cbar(T);
       if (tid == 0) sc.nplist = 0;
-      __syncthreads();
+      cbar(T);
       const int64_t q = c0 + tid;
       if (q < a.n_pools && a.out[q].status == COOP_PENDING_) sc.plist[atomicAdd(&sc.nplist, 1)] = tid;
-      __syncthreads();
+      cbar(T);
       const int np = sc.nplist;
       for (int u = 0; u < np; ++u) {
         const int64_t p = c0 + sc.plist[u];
         smem_t *stage = base_ptr;
-        stage_plain(a, stage, p);
-        __syncthreads();
+        stage_plain(a, stage, p, T);
+        cbar(T);
         search_pool<K>(a, sc, Ebuf, stage, p, a.req[p]);
-        __syncthreads();
+        cbar(T);
+        const int64_t dp = sc.dpool;
+        if (dp >= 0) {
+          verify_pool<K>(a, sc, dp, sc.ncand, T);
+          if (tid == 0) sc.dpool = -1;
+        }
       }
     }
     return;
   }
-  int it = 0, s = 0;
+  int s = 0;
   uint32_t phase = 0;
-  for (int64_t p = blockIdx.x; p < a.n_pools; p += gridDim.x, ++it) {
+  for (int64_t p = blockIdx.x; p < a.n_pools; p += gridDim.x) {
     smem_t *stage = base_ptr + (size_t)s * a.stage_bytes;
     const uint64_t Rraw = a.req[p];
     if (a.use_tma) {
       mbar_wait(smem_u32(&sc.mbar[s]), phase);
     } else {
-      stage_plain(a, stage, p);
-      __syncthreads();
+      stage_plain(a, stage, p, T);
+      cbar(T);
     }
     search_pool<K>(a, sc, Ebuf, stage, p, Rraw);
-    // every thread orders its generic-proxy writes into the stage (S / H^ / h write-back)
+    // every thread orders its generic-proxy writes into the stage (S / H^ write-back)
     // before the async-proxy (TMA) refill that the barrier releases
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();  // stage s fully consumed
+    cbar(T);  // stage s fully consumed
     if (a.use_tma && tid == 0) {
       const int64_t pn = p + (int64_t)a.stages * gridDim.x;
       if (pn < a.n_pools)
         issue_stage(a, &m_ss, &m_c, &m_s, base + (uint32_t)s * a.stage_bytes,
                     smem_u32(&sc.mbar[s]), pn);
+    }
+    // the deferred exact re-summation of this pool's candidates (global memory), while the
+    // stage refills
+    const int64_t dp = sc.dpool;
+    if (dp >= 0) {
+      verify_pool<K>(a, sc, dp, sc.ncand, T);
+      if (tid == 0) sc.dpool = -1;
     }
     if (++s == a.stages) {  // next stage of the ring; parity flips on wrap-around
       s = 0;
