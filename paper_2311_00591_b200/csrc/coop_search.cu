@@ -41,8 +41,10 @@ constexpr bool kPhaseHooks = false;
 #endif
 constexpr int kCandCap = 512;  // fits two 512-thread CTAs (one stage each) per SM at N = 4096
 constexpr int kMaxWarps = 16;
+constexpr int kDefMax = 16;  // candidates a deferred re-summation takes
 constexpr uint64_t kRClamp = 1ull << 62;  // any R > sum of sizes (< 2^61) is infeasible
 constexpr int kInfIdx = 0x7fffffff;
+constexpr uint64_t kSizeMask = (1ull << 62) - 1ull;
 
 struct Scratch {
   uint64_t wS[kMaxWarps];
@@ -51,12 +53,8 @@ struct Scratch {
   double wP[kMaxWarps];  // chunk-pruning upper bounds
   int32_t wF[kMaxWarps];
   int32_t wZ[kMaxWarps];
-  union {
-    uint64_t part[2][kMaxWarps][3];  // verification partial sums (phase B)
-    struct {
-      int32_t zW[kMaxWarps], zM[kMaxWarps], zW2[kMaxWarps];  // zero-pass reductions (phase 1)
-    };
-  };
+  uint64_t part[2][kMaxWarps][3];                         // verification partial sums
+  int32_t zW[kMaxWarps], zM[kMaxWarps], zW2[kMaxWarps];  // zero-pass reductions
   int32_t partn[2][kMaxWarps];
   uint64_t pspan[2][kMaxWarps];
   uint64_t bcost[kMaxWarps];
@@ -68,7 +66,11 @@ struct Scratch {
   uint16_t evc[kMaxWarps * 32];  // per chunk: EVICTABLE mask (exact re-summation, n_evict)
   uint32_t cand[kCandCap];
   unsigned long long mbar[2];
-  int64_t dpool;  // pool whose candidates wait for the deferred exact re-summation (-1: none)
+  // deferred exact re-summations (two slots: the newest and an older one): pool (-1: none),
+  // candidate count and windows; dnext = the slot the next deferral uses
+  int64_t dpool[2];
+  int32_t dnc[2], dnext;
+  uint32_t dcand[2][kDefMax];
   int32_t nplist;                      // pending mode: pools of the chunk to finish
   int16_t plist[kMaxWarps * 32];
 };
@@ -260,19 +262,30 @@ __device__ __forceinline__ double rcp_nr(double s) {
 
 // Exact cost of the window [i, e) of pool p (R3): h = c/s (IEEE RN, R1) of its EVICTABLE
 // items -- FREE items add 0, a window never holds a PINNED one -- summed in 192-bit fixed
-// point over the items i + off, i + off + step, ...; also the span and the EVICTABLE count
-// (n_evict).  Read from global memory: the stage may already hold the next pool.
-__device__ __forceinline__ void window_sum(const Args &a, int64_t p, int i, int e, int off,
-                                           int step, U192 &acc, uint64_t &span, int &nev) {
+// point over the items i + off, i + off + step, ...; also the EVICTABLE count (n_evict) and
+// the span.  SMEM = false: everything from global memory (deferred re-summations: the stage
+// holds another pool by then; the lines were prefetched into L1); SMEM = true: exact h from
+// region 1 (converted in place by exact_h_in_place) and the states from the chunk masks.
+template <bool SMEM, int K>
+__device__ __forceinline__ void window_sum(const Args &a, const PoolView *v, int64_t p, int i,
+                                           int e, int off, int step, U192 &acc, uint64_t &span,
+                                           int &nev) {
   const uint64_t *ss = a.ss + p * a.stride;
   const double *cg = a.cost + p * a.stride, *sg = a.stale + p * a.stride;
   for (int k = i + off; k < e; k += step) {
-    const uint64_t w = __ldg(ss + k);
-    const double c = __ldg(cg + k), s = __ldg(sg + k);
-    span += w & ((1ull << 62) - 1ull);
-    if ((w >> 62) == COOP_EVICTABLE) {
-      acc = u192_add(acc, u192_from_double(__ddiv_rn(c, s)));
-      ++nev;
+    if (SMEM) {
+      if ((v->evc[k / K] >> (k % K)) & 1u) {
+        acc = u192_add(acc, u192_from_double(v->c_at(k)));
+        ++nev;
+      }
+    } else {
+      const uint64_t w = __ldg(ss + k);
+      const double c = __ldg(cg + k), s = __ldg(sg + k);
+      span += w & kSizeMask;
+      if ((w >> 62) == COOP_EVICTABLE) {
+        acc = u192_add(acc, u192_from_double(__ddiv_rn(c, s)));
+        ++nev;
+      }
     }
   }
 }
@@ -289,21 +302,22 @@ __device__ __forceinline__ void warp_sum_all(U192 &acc, uint64_t &span, int &nev
 
 // The exact re-summation of the candidate windows sc.cand[0, nc) of pool p by the whole CTA
 // and the pool's result: the lexicographic (rounded exact cost bits, first) minimum.
-template <int K>
-__device__ __forceinline__ void verify_pool(const Args &a, Scratch &sc, int64_t p, int nc, int T) {
+template <bool SMEM, int K>
+__device__ __forceinline__ void verify_pool(const Args &a, const PoolView *v, Scratch &sc, int64_t p,
+                                            const uint32_t *cand, int nc, int T) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
   uint64_t best = ~0ull, bspan = 0;  // meaningful in thread 0
   int bfirst = kInfIdx, bend = -1, bnev = 0;
   if (nc <= W) {
     // few candidates: the whole CTA sums each window (short latency chain)
     for (int c = 0; c < nc; ++c) {
-      const uint32_t cd = sc.cand[c];
+      const uint32_t cd = cand[c];
       const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
       U192 acc = u192_zero();
       uint64_t span = 0;
       int nev = 0;
       if (i + warp * 32 < e) {  // warp-uniform: warps without items skip
-        window_sum(a, p, i, e, tid, T, acc, span, nev);
+        window_sum<SMEM, K>(a, v, p, i, e, tid, T, acc, span, nev);
         warp_sum_all(acc, span, nev);
       }
       const int par = c & 1;
@@ -342,12 +356,12 @@ __device__ __forceinline__ void verify_pool(const Args &a, Scratch &sc, int64_t 
     uint64_t wbest = ~0ull, wspan = 0;
     int32_t wfirst = kInfIdx, wend = -1, wnev = 0;
     for (int c = warp; c < nc; c += W) {
-      const uint32_t cd = sc.cand[c];
+      const uint32_t cd = cand[c];
       const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
       U192 acc = u192_zero();
       uint64_t span = 0;
       int nev = 0;
-      window_sum(a, p, i, e, lane, 32, acc, span, nev);
+      window_sum<SMEM, K>(a, v, p, i, e, lane, 32, acc, span, nev);
       warp_sum_all(acc, span, nev);
       const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(acc));
       if (better(cb, i, wbest, wfirst)) {
@@ -378,8 +392,11 @@ __device__ __forceinline__ void verify_pool(const Args &a, Scratch &sc, int64_t 
       }
     }
   }
-  if (tid == 0) write_result(a.out + p, bfirst, bend - 1, bspan, __longlong_as_double((long long)best), bnev, COOP_OK);
-  cbar(T);  // sc.cand / sc.part free again
+  if (tid == 0) {
+    if (SMEM) bspan = v->S_at(bend) - v->S_at(bfirst);
+    write_result(a.out + p, bfirst, bend - 1, bspan, __longlong_as_double((long long)best), bnev, COOP_OK);
+  }
+  cbar(T);  // the candidate list / sc.part free again
 }
 
 // Per-thread running state of the filter.
@@ -650,21 +667,11 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, bad_any ? COOP_ERR_INVALID_ARG : COOP_OK);
     return;
   }
-  // S over the size words (the sizes live on in spre, the states in the masks)
-#pragma unroll
-  for (int q = 0; q < K; q += 2) {
-    const int k = k0 + q;
-    if (k < n) sm<ulonglong2>(v.sr, swz((uint32_t)k)) = make_ulonglong2(S_car + spre[q], S_car + spre[q + 1]);
-  }
-  if (k0 <= n - 1 && n - 1 < k0 + K) {  // sentinels at slots n, n + 1
-    sm<uint64_t>(v.sr, swz((uint32_t)n)) = S_total;
-    sm<uint64_t>(v.sr, swz((uint32_t)n + 1u)) = ~0ull;
-  }
   // ---------------- zero pass: zero-cost windows ----------------------------------------
   // A run of consecutive h = 0 items is a zero-cost window iff its span covers R; the lowest
-  // such run head is the answer (exact cost 0 is the global minimum, R4).  From registers:
-  // the heads whose own item covers R; heads of runs that go on past the head (never on the
-  // config-4 law) are settled below from S.
+  // such run head is the answer (exact cost 0 is the global minimum, R4).  The heads whose
+  // own item covers R first (sizes from the raw words still in region 0); heads of runs that
+  // go on past the head (never on the config-4 law) are settled below.
   const bool cont = (k0 + K < n) && (zmk16[tid + 1] & 1u);  // item k0 + K is h = 0
   const uint32_t heads = zm & ~(zm << 1);
   uint32_t one = 0;
@@ -673,9 +680,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     while (hm) {  // ~1 head per chunk; stop at the first whose own item covers R
       const int q = __ffs(hm) - 1;
       hm &= hm - 1u;
-      // S of this thread's own items was just stored by this thread (program order)
-      const uint64_t nxt = q == K - 1 ? S_car + sacc : v.S_at(k0 + q + 1);
-      if (nxt - v.S_at(k0 + q) >= v.R) {
+      if ((v.S_at(k0 + q) & kSizeMask) >= v.R) {  // raw size word (S is written in phase 2)
         one = 1u << q;
         break;
       }
@@ -704,7 +709,9 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
       mm &= mm - 1u;
       if (k0 + q >= zmin) break;
       const int stop = zero_run_stop(zmk16, tid, q, K, n);
-      if (v.S_at(stop) - v.S_at(k0 + q) >= v.R) {
+      uint64_t span = 0;
+      for (int k = k0 + q; k < stop && span < v.R; ++k) span += v.S_at(k) & kSizeMask;
+      if (span >= v.R) {
         zi2 = k0 + q;
         break;
       }
@@ -717,16 +724,14 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
   if (kPhaseHooks && a.dbg == 4) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
   if (zmin != kInfIdx) {
     if (zmin >= k0 && zmin < k0 + K) {  // the owner of the winning head writes the window
-      const uint64_t target = v.S_at(zmin) + v.R;
-      int lo = zmin + 1, hi = zero_run_stop(zmk16, tid, zmin - k0, K, n);
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (v.S_at(mid) >= target) hi = mid;
-        else lo = mid + 1;
-      }
-      int znev = 0;
-      for (int k = zmin; k < lo; ++k) znev += (sc.evc[k / K] >> (k % K)) & 1;
-      write_result(a.out + p, zmin, lo - 1, v.S_at(lo) - v.S_at(zmin), 0.0, znev, COOP_OK);
+      uint64_t span = 0;
+      int k = zmin, znev = 0;
+      do {  // the shortest covering window from zmin (inside its run of h = 0 items)
+        span += v.S_at(k) & kSizeMask;
+        znev += (sc.evc[k / K] >> (k % K)) & 1;
+        ++k;
+      } while (span < v.R);
+      write_result(a.out + p, zmin, k - 1, span, 0.0, znev, COOP_OK);
     }
     return;
   }
@@ -746,16 +751,22 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     const int32_t bnext = __shfl_sync(0xffffffffu, wb, min(warp + 1, 31));
     const double H_car = __dadd_rn(warp ? hprev : 0.0, hexc);
     nb_right = min(bexc, warp + 1 < W ? bnext : kInfIdx);
+    // S over the raw size words, H^ carries added in place
 #pragma unroll
     for (int q = 0; q < K; q += 2) {
       const int k = k0 + q;
       if (k < n) {
         const uint32_t o = swz((uint32_t)k);
+        sm<ulonglong2>(v.sr, o) = make_ulonglong2(S_car + spre[q], S_car + spre[q + 1]);
         const double2 hl = sm<double2>(v.hr, o);
         sm<double2>(v.hr, o) = make_double2(__dadd_rn(H_car, hl.x), __dadd_rn(H_car, hl.y));
       }
     }
-    if (k0 <= n - 1 && n - 1 < k0 + K) sm<double>(v.hr, swz((uint32_t)n)) = __dadd_rn(H_car, hacc);
+    if (k0 <= n - 1 && n - 1 < k0 + K) {  // sentinels: S[n], S[n+1] = ~0, H^[n]
+      sm<uint64_t>(v.sr, swz((uint32_t)n)) = S_total;
+      sm<uint64_t>(v.sr, swz((uint32_t)n + 1u)) = ~0ull;
+      sm<double>(v.hr, swz((uint32_t)n)) = __dadd_rn(H_car, hacc);
+    }
   }
   cbar(T);
   if (kPhaseHooks && a.dbg == 3) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
@@ -836,14 +847,50 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     if (slot < kCandCap) sc.cand[slot] = ((uint32_t)bl.li << 16) | (uint32_t)(bl.le - bl.li);
   }
   const int any_multi = cbar_or(multi_l, T);
-  if (!any_multi) {
-    // the usual case: the candidates' exact re-summation reads global memory only, so it is
-    // deferred until this CTA has released the stage and started the next pool's load
-    if (tid == 0) sc.dpool = p;
+  if (!any_multi && sc.ncand <= kDefMax) {
+    // the usual case: the candidates' exact re-summation reads global memory only; it is
+    // deferred until the end of the next pool (while a TMA load is in flight), and their
+    // lines are prefetched into L1 now -- one 128-byte line per thread: (candidate, array, line)
+    const int nc = sc.ncand, slot = sc.dnext;
+    int f = tid;
+    for (int c = 0; c < nc && f >= 0; ++c) {
+      const uint32_t cd = sc.cand[c];
+      const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
+      const int lines = (e - 1 - i) / 16 + 2;  // items i, i+16, ..., and e-1
+      if (f < 3 * lines) {
+        const int arr = f / lines, j = f % lines;
+        const int k = min(i + 16 * j, e - 1);
+        const void *ptr = arr == 0 ? (const void *)(a.ss + p * a.stride + k)
+                        : arr == 1 ? (const void *)(a.cost + p * a.stride + k)
+                                   : (const void *)(a.stale + p * a.stride + k);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
+      }
+      f -= 3 * lines;
+    }
+    if (tid < nc) sc.dcand[slot][tid] = sc.cand[tid];
+    if (tid == 0) {
+      sc.dpool[slot] = p;
+      sc.dnc[slot] = nc;
+      sc.dnext = slot ^ 1;
+    }
     return;
   }
-  // rare: some thread holds two or more candidates -- re-walk, restricted to windows of
-  // kCandCap consecutive starts (cannot overflow the list), and verify round by round
+  // rare (ties, many candidates): exact h over region 1 first, then -- if some thread holds
+  // two or more candidates -- re-walks restricted to windows of kCandCap consecutive starts
+  // (cannot overflow the list), verified round by round from shared memory
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const int k = k0 + q;
+    if (k < n && ((evmask >> q) & 1u)) {
+      const uint32_t o = swz((uint32_t)k);
+      sm<double>(v.cr, o) = __ddiv_rn(sm<double>(v.cr, o), v.sg[k]);
+    }
+  }
+  cbar(T);
+  if (!any_multi) {
+    verify_pool<true, K>(a, &v, sc, p, sc.cand, sc.ncand, T);
+    return;
+  }
   const bool wmulti = __any_sync(0xffffffffu, bl.L <= thresh);  // this warp holds candidates
   uint64_t best = ~0ull, bspan = 0;  // meaningful in thread 0
   int bfirst = kInfIdx, blast = -1, bnev = 0;
@@ -859,7 +906,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     cbar(T);
     const int nc = min(sc.ncand, kCandCap);
     if (nc == 0) continue;
-    verify_pool<K>(a, sc, p, nc, T);  // writes this round's best into out[p]
+    verify_pool<true, K>(a, &v, sc, p, sc.cand, nc, T);  // writes this round's best into out[p]
     if (tid == 0) {
       const coop_window r = a.out[p];
       const uint64_t cb = (uint64_t)__double_as_longlong(r.cost);
@@ -892,13 +939,19 @@ __global__ void __launch_bounds__(MAXT, MINB)
 
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) mbar_init(smem_u32(&sc.mbar[s]), 1);
-    sc.dpool = -1;
+    sc.dpool[0] = sc.dpool[1] = -1;
+    sc.dnext = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cbar(T);
+  // pool of this CTA's round k: the rounds sweep [kG, (k+1)G) in a rotated order, so every
+  // CTA sees every residue of the pool index modulo G (a periodic mix of short and long
+  // requests -- the config-4 law alternates them -- is spread evenly over the CTAs and SMs)
+  const int64_t G = gridDim.x;
+  auto pool_of = [&](int64_t k) { return k * G + (int64_t)(((int64_t)blockIdx.x + k) % G); };
   if (a.use_tma && tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
-      const int64_t p = (int64_t)blockIdx.x + (int64_t)s * gridDim.x;
+      const int64_t p = pool_of(s);
       if (p < a.n_pools)
         issue_stage(a, &m_ss, &m_c, &m_s, base + (uint32_t)s * a.stage_bytes,
                     smem_u32(&sc.mbar[s]), p);
@@ -923,48 +976,56 @@ __global__ void __launch_bounds__(MAXT, MINB)
         cbar(T);
         search_pool<K>(a, sc, Ebuf, stage, p, a.req[p]);
         cbar(T);
-        const int64_t dp = sc.dpool;
-        if (dp >= 0) {
-          verify_pool<K>(a, sc, dp, sc.ncand, T);
-          if (tid == 0) sc.dpool = -1;
+        const int slot = sc.dnext;  // keep a slot free for the next deferral
+        if (sc.dpool[slot] >= 0) {
+          verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dnc[slot], T);
+          if (tid == 0) sc.dpool[slot] = -1;
         }
       }
     }
-    return;
+  } else {
+    int s = 0;
+    uint32_t phase = 0;
+    for (int64_t k = 0;; ++k) {
+      const int64_t p = pool_of(k);
+      if (p >= a.n_pools) break;  // only the last round is partial
+      smem_t *stage = base_ptr + (size_t)s * a.stage_bytes;
+      const uint64_t Rraw = a.req[p];
+      if (a.use_tma) {
+        mbar_wait(smem_u32(&sc.mbar[s]), phase);
+      } else {
+        stage_plain(a, stage, p, T);
+        cbar(T);
+      }
+      search_pool<K>(a, sc, Ebuf, stage, p, Rraw);
+      // every thread orders its generic-proxy writes into the stage (S / H^ write-back)
+      // before the async-proxy (TMA) refill that the barrier releases
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      cbar(T);  // stage s fully consumed
+      if (a.use_tma && tid == 0) {
+        const int64_t pn = pool_of(k + a.stages);
+        if (pn < a.n_pools)
+          issue_stage(a, &m_ss, &m_c, &m_s, base + (uint32_t)s * a.stage_bytes,
+                      smem_u32(&sc.mbar[s]), pn);
+      }
+      // an older pool's deferred re-summation (its lines prefetched a pool ago) while the
+      // stage refills
+      {
+        const int slot = sc.dnext;
+        if (sc.dpool[slot] >= 0) {
+          verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dnc[slot], T);
+          if (tid == 0) sc.dpool[slot] = -1;
+        }
+      }
+      if (++s == a.stages) {  // next stage of the ring; parity flips on wrap-around
+        s = 0;
+        phase ^= 1u;
+      }
+    }
   }
-  int s = 0;
-  uint32_t phase = 0;
-  for (int64_t p = blockIdx.x; p < a.n_pools; p += gridDim.x) {
-    smem_t *stage = base_ptr + (size_t)s * a.stage_bytes;
-    const uint64_t Rraw = a.req[p];
-    if (a.use_tma) {
-      mbar_wait(smem_u32(&sc.mbar[s]), phase);
-    } else {
-      stage_plain(a, stage, p, T);
-      cbar(T);
-    }
-    search_pool<K>(a, sc, Ebuf, stage, p, Rraw);
-    // every thread orders its generic-proxy writes into the stage (S / H^ write-back)
-    // before the async-proxy (TMA) refill that the barrier releases
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    cbar(T);  // stage s fully consumed
-    if (a.use_tma && tid == 0) {
-      const int64_t pn = p + (int64_t)a.stages * gridDim.x;
-      if (pn < a.n_pools)
-        issue_stage(a, &m_ss, &m_c, &m_s, base + (uint32_t)s * a.stage_bytes,
-                    smem_u32(&sc.mbar[s]), pn);
-    }
-    // the deferred exact re-summation of this pool's candidates (global memory), while the
-    // stage refills
-    const int64_t dp = sc.dpool;
-    if (dp >= 0) {
-      verify_pool<K>(a, sc, dp, sc.ncand, T);
-      if (tid == 0) sc.dpool = -1;
-    }
-    if (++s == a.stages) {  // next stage of the ring; parity flips on wrap-around
-      s = 0;
-      phase ^= 1u;
-    }
+  for (int slot = 0; slot < 2; ++slot) {  // the last deferred re-summations
+    cbar(T);
+    if (sc.dpool[slot] >= 0) verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dnc[slot], T);
   }
 }
 
@@ -1083,6 +1144,8 @@ int launch_window_search_cta(const coop_tables_soa *t, const uint64_t *requests,
   if (a.n_pools == 0) return COOP_OK;
   const char *cfg = getenv("COOP_SEARCH_CFG");  // profiling hook: "8x512" = K 8, 512 threads
   if (cfg && strcmp(cfg, "8x512") == 0 && a.n <= 4096) return launch_k<8, 512, 2>(a, st);
+  if (cfg && strcmp(cfg, "8x512x1") == 0 && a.n <= 4096) return launch_k<8, 512, 1>(a, st);
+  if (cfg && strcmp(cfg, "16x256x1") == 0 && a.n <= 4096) return launch_k<16, 256, 1>(a, st);
   if (a.n <= 2048) return launch_k<8, 256, 2>(a, st);   // 2 CTAs per SM
   if (a.n <= 4096) return launch_k<16, 256, 2>(a, st);  // 2 CTAs per SM, 1 stage each
   return launch_k<16, 512, 1>(a, st);
