@@ -849,7 +849,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
   const int any_multi = cbar_or(multi_l, T);
   if (!any_multi && sc.ncand <= kDefMax) {
     // the usual case: the candidates' exact re-summation reads global memory only; it is
-    // deferred until the end of the next pool (while a TMA load is in flight), and their
+    // deferred until this CTA has released the stage and issued the next TMA load, and their
     // lines are prefetched into L1 now -- one 128-byte line per thread: (candidate, array, line)
     const int nc = sc.ncand, slot = sc.dnext;
     int f = tid;
@@ -1008,10 +1008,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
           issue_stage(a, &m_ss, &m_c, &m_s, base + (uint32_t)s * a.stage_bytes,
                       smem_u32(&sc.mbar[s]), pn);
       }
-      // an older pool's deferred re-summation (its lines prefetched a pool ago) while the
-      // stage refills
+      // this pool's deferred exact re-summation (global memory; its lines were prefetched into
+      // L1 when the candidates were found) while the stage refills
       {
-        const int slot = sc.dnext;
+        const int slot = sc.dnext ^ 1;
         if (sc.dpool[slot] >= 0) {
           verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dnc[slot], T);
           if (tid == 0) sc.dpool[slot] = -1;
