@@ -473,28 +473,27 @@ __device__ __forceinline__ void eval_start(const PoolView &v, const uint4 rec, i
 // memory), a 2-bit state code per item, and the R7 checks WITHOUT a division: for c > 0
 // normal and s >= 1, c/s lies in (2^(d-1), 2^(d+1)) with d the exponent difference of c and
 // s, and hi(c) - hi(s) lies in ((d-1) 2^20, (d+1) 2^20), so hi(c) - hi(s) in
-// [-62 2^20, 58 2^20) gives d in [-62, 58] and RN(c/s) inside [2^-64, 2^60) (s is held to
-// [1, 2^960), so a negative or non-finite c falls outside the band too).  An EVICTABLE item
-// outside that clear range (c = +-0 is clear when s is) sets `oor`, and settle_chunk() then
-// re-decides the chunk with the oracle's own comparisons and the exact division.
+// [-62 2^20, 58 2^20) gives d in [-62, 58] and RN(c/s) inside [2^-64, 2^60), nonzero (s is
+// held to [1, 2^960), so c = +-0 or a negative or non-finite c falls outside the band too).
+// An EVICTABLE item outside that clear range sets `oor`, and settle_chunk() then re-decides
+// the chunk with the oracle's own comparisons and the exact division (h = 0 items included).
 // FULL: no item past n.
-//   st2: bits 2j..2j+1 = state of item j (padding: FREE); nz: EVICTABLE with c != 0;
-//   badbits: size bits 48..61 of some item; minsz: 0 iff some live item has size 0.
+//   st2: bits 2j..2j+1 = state of item j (padding: FREE); badbits: size bits 48..61 of
+//   some item; zsize: some live item has size 0.
 template <int K, bool FULL>
 __device__ __forceinline__ void phase1(const PoolView &v, int k0, int n, uint32_t &st2,
-                                       uint32_t &nz, uint32_t &badbits, uint32_t &minsz,
-                                       bool &oor, uint64_t (&spre)[K], uint64_t &sacc,
-                                       double &hacc) {
+                                       uint32_t &badbits, bool &zsize, bool &oor,
+                                       uint64_t (&spre)[K], uint64_t &sacc, double &hacc) {
 #pragma unroll
   for (int q = 0; q < K; q += 2) {
     const int k = k0 + q;
     const uint32_t o = swz((uint32_t)k);
     ulonglong2 vs = make_ulonglong2(0, 0);
-    uint4 vc = make_uint4(0, 0, 0, 0), vt = make_uint4(0, 0x3ff00000u, 0, 0x3ff00000u);
+    double2 vc = make_double2(0.0, 0.0), vt = make_double2(1.0, 1.0);
     if (FULL || k < n) {
       vs = sm<ulonglong2>(v.sr, o);
-      vc = sm<uint4>(v.cr, o);
-      vt = sm<uint4>(v.hr, o);
+      vc = sm<double2>(v.cr, o);
+      vt = sm<double2>(v.hr, o);
     }
     double hl[2];
 #pragma unroll
@@ -506,25 +505,19 @@ __device__ __forceinline__ void phase1(const PoolView &v, int k0, int n, uint32_
       st2 |= (svh >> (30 - 2 * j)) & (3u << (2 * j));
       badbits |= svh & 0x3fff0000u;
       const uint32_t shi = svh & 0x3fffffffu;
-      minsz = min(minsz, live ? (slo | shi) : 1u);
+      zsize |= live && (slo | shi) == 0u;
       spre[j] = sacc;
       sacc += ((uint64_t)shi << 32) | slo;
-      const uint32_t cl = r ? vc.z : vc.x, ch = r ? vc.w : vc.y;
-      const uint32_t tl = r ? vt.z : vt.x, sh = r ? vt.w : vt.y;
-      double hh = 0.0;
-      if ((svh >> 30) == COOP_EVICTABLE) {
-        const bool czero = ((ch << 1) | cl) == 0u;
-        // clear range of s: [1, 2^960); then a negative, infinite or NaN c gives
-        // hi(c) - hi(s) >= 64 2^20, outside the clear band of the exponent test
-        oor |= (sh - 0x3ff00000u) >= 0x3c000000u;
-        if (!czero) {
-          nz |= 1u << j;
-          oor |= (ch - sh + (62u << 20)) >= (120u << 20);
-        }
-        hh = __hiloint2double((int)ch, (int)cl) * rcp_nr(__hiloint2double((int)sh, (int)tl));
-      }
+      // branch-free: h^ is formed for every item and kept for EVICTABLE ones only
+      const double c = r ? vc.y : vc.x, s = r ? vt.y : vt.x;
+      const uint32_t ch = (uint32_t)__double2hiint(c), sh = (uint32_t)__double2hiint(s);
+      const bool ev = (svh >> 30) == COOP_EVICTABLE;
+      // clear range: s in [1, 2^960) and hi(c) - hi(s) in [-62 2^20, 58 2^20); c = +-0,
+      // negative, infinite or NaN (and every s outside the range) lands outside it too
+      oor |= ev & (((sh - 0x3ff00000u) >= 0x3c000000u) | ((ch - sh + (62u << 20)) >= (120u << 20)));
+      const double hq = c * rcp_nr(s);
       hl[r] = hacc;
-      hacc = __dadd_rn(hacc, hh);
+      hacc = __dadd_rn(hacc, ev ? hq : 0.0);
     }
     if (FULL || k < n) sm<double2>(v.hr, o) = make_double2(hl[0], hl[1]);
   }
@@ -602,18 +595,19 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     return;
   }
   // ---------------- phase 1: decode, validate (R7), span / h^ prefixes, masks --------------
-  bool bad = (Rraw == 0), oor = false;
-  uint32_t st2 = 0, nzmask = 0, badbits = 0, minsz = 1;
+  bool bad = (Rraw == 0), oor = false, zsize = false;
+  uint32_t st2 = 0, badbits = 0;
   uint64_t spre[K];
   uint64_t sacc = 0;
   double hacc = 0.0;
   if (k0 + K <= n)  // warp-uniform except in the last warp
-    phase1<K, true>(v, k0, n, st2, nzmask, badbits, minsz, oor, spre, sacc, hacc);
+    phase1<K, true>(v, k0, n, st2, badbits, zsize, oor, spre, sacc, hacc);
   else
-    phase1<K, false>(v, k0, n, st2, nzmask, badbits, minsz, oor, spre, sacc, hacc);
+    phase1<K, false>(v, k0, n, st2, badbits, zsize, oor, spre, sacc, hacc);
   const uint32_t evmask = even_bits(st2 & ~(st2 >> 1));  // state 01
   const uint32_t barmask = even_bits((st2 >> 1) & ~st2);  // state 10
-  bad |= (badbits != 0u) | (minsz == 0u) | ((st2 & (st2 >> 1) & 0x55555555u) != 0u);  // state 3
+  uint32_t nzmask = evmask;  // EVICTABLE items in the clear range have h != 0
+  bad |= (badbits != 0u) | zsize | ((st2 & (st2 >> 1) & 0x55555555u) != 0u);  // state 3
   if (oor) settle_chunk<K>(v, k0, evmask, nzmask, bad, hacc);
   const int cnt = n - k0;
   const uint32_t valid = cnt >= K ? kFull : (cnt > 0 ? (1u << cnt) - 1u : 0u);
