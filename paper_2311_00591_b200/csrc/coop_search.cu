@@ -843,24 +843,9 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
   const int any_multi = cbar_or(multi_l, T);
   if (!any_multi && sc.ncand <= kDefMax) {
     // the usual case: the candidates' exact re-summation reads global memory only; it is
-    // deferred until this CTA has released the stage and issued the next TMA load, and their
-    // lines are prefetched into L1 now -- one 128-byte line per thread: (candidate, array, line)
+    // deferred until this CTA has released the stage and issued the next TMA load (an L1 /
+    // L2 prefetch of the windows' lines measured slower)
     const int nc = sc.ncand, slot = sc.dnext;
-    int f = tid;
-    for (int c = 0; c < nc && f >= 0; ++c) {
-      const uint32_t cd = sc.cand[c];
-      const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
-      const int lines = (e - 1 - i) / 16 + 2;  // items i, i+16, ..., and e-1
-      if (f < 3 * lines) {
-        const int arr = f / lines, j = f % lines;
-        const int k = min(i + 16 * j, e - 1);
-        const void *ptr = arr == 0 ? (const void *)(a.ss + p * a.stride + k)
-                        : arr == 1 ? (const void *)(a.cost + p * a.stride + k)
-                                   : (const void *)(a.stale + p * a.stride + k);
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
-      }
-      f -= 3 * lines;
-    }
     if (tid < nc) sc.dcand[slot][tid] = sc.cand[tid];
     if (tid == 0) {
       sc.dpool[slot] = p;
