@@ -21,6 +21,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kCap = 4096;       // blocks per pool held by the kernel (COOP_ERR_NOMEM beyond)
 constexpr int kStackCap = 1030;  // rematerialization frames (max_depth <= 1024)
+constexpr int kRsm = 64;         // of which held in shared memory
 constexpr int kFree = -1;
 constexpr int kOpChunk = 32;   // replay: trace ops whose records are staged in shared memory at once
 constexpr int kListCap = 384;  // their input / death / lock lists staged with them (else read from L2)
@@ -187,6 +188,8 @@ struct Shared {
   // the last evicted window (read by the online calls): items, span, cost bits, victims
   int32_t win_first, win_last, nvict;
   uint64_t win_span, win_cost;
+  // the bottom kRsm frames of the rematerialization stack (deeper frames: the workspace)
+  int32_t rsm[4][kRsm];
   // replay op loop: the records and lists of the current chunk of kOpChunk ops
   OpRec ops[kOpChunk];
   int32_t op_base;                    // first op of the staged chunk
@@ -1349,20 +1352,25 @@ struct CellT {
   // ---------------------------------------------------------------- rematerialization
   // M(t): explicit stack (R21-R23); a dead tensor recomputed here stays resident until
   // the end of the current trace op (R22).
+  // stack frame field (0 tensor, 1 stage, 2 next input to check, 3 depth): shared memory for
+  // the bottom kRsm frames, the workspace beyond
+  __device__ __forceinline__ int32_t &rs(int field, int f) {
+    return f < kRsm ? sh.rsm[field][f] : w.rst[field * kStackCap + f];
+  }
   __device__ void materialize(int t0) {
     if (threadIdx.x == 0) {
       sh.sp = 1;
-      w.rst[0 * kStackCap + 0] = t0;
-      w.rst[1 * kStackCap + 0] = 0;
-      w.rst[2 * kStackCap + 0] = 0;
-      w.rst[3 * kStackCap + 0] = 0;
+      rs(0, 0) = t0;
+      rs(1, 0) = 0;
+      rs(2, 0) = 0;
+      rs(3, 0) = 0;
     }
     __syncthreads();
     while (sh.sp > 0 && ok()) {
       const int f = sh.sp - 1;
-      const int t = w.rst[0 * kStackCap + f], depth = w.rst[3 * kStackCap + f];
-      const int op = tr.producer[t];
-      if (w.rst[1 * kStackCap + f] == 0) {
+      const int t = rs(0, f), depth = rs(3, f), stage = rs(1, f);
+      const int op = ldg_if<kRO>(&tr.producer[t]);
+      if (stage == 0) {
         __syncthreads();
         if (threadIdx.x == 0) {
           if (depth > a.max_depth) {
@@ -1373,7 +1381,7 @@ struct CellT {
             sh.res.fail_op = sh.cur_op;
           } else {
             if (depth > sh.res.max_depth) sh.res.max_depth = depth;
-            w.rst[1 * kStackCap + f] = 1;
+            rs(1, f) = 1;
           }
         }
         __syncthreads();
@@ -1382,26 +1390,39 @@ struct CellT {
         __syncthreads();
         continue;
       }
-      if (w.rst[1 * kStackCap + f] == 1) {
-        int j = w.rst[2 * kStackCap + f];
-        const int n = nin(op);
-        while (j < n && (sh.tfl[in_at(op, j)] & TF_RES)) ++j;
+      if (stage == 1) {
+        // the first input at or after the frame's cursor that is not resident: warp 0 checks
+        // 32 inputs at a time (inputs before the cursor were made resident and are pinned)
         __syncthreads();
-        if (threadIdx.x == 0) {
-          if (j < n) {
-            w.rst[2 * kStackCap + f] = j + 1;
-            if (sh.sp >= kStackCap) {
-              sh.status = COOP_ERR_THRASHED;
-              sh.res.fail_op = sh.cur_op;
-            } else {
-              const int g = sh.sp++;
-              w.rst[0 * kStackCap + g] = in_at(op, j);
-              w.rst[1 * kStackCap + g] = 0;
-              w.rst[2 * kStackCap + g] = 0;
-              w.rst[3 * kStackCap + g] = depth + 1;
+        if (threadIdx.x < 32) {
+          const int n = nin(op), ib = ldg_if<kRO>(&tr.in_ptr[op]);
+          int j = rs(2, f);
+          while (j < n) {
+            const int jj = j + (int)threadIdx.x;
+            const bool miss = jj < n && !(sh.tfl[ldg_if<kRO>(&tr.in_idx[ib + jj])] & TF_RES);
+            const uint32_t bal = __ballot_sync(0xffffffffu, miss);
+            if (bal) {
+              j += __ffs(bal) - 1;
+              break;
             }
-          } else {
-            w.rst[1 * kStackCap + f] = 2;
+            j += 32;
+          }
+          if (threadIdx.x == 0) {
+            if (j < n) {
+              rs(2, f) = j + 1;
+              if (sh.sp >= kStackCap) {
+                sh.status = COOP_ERR_THRASHED;
+                sh.res.fail_op = sh.cur_op;
+              } else {
+                const int g = sh.sp++;
+                rs(0, g) = ldg_if<kRO>(&tr.in_idx[ib + j]);
+                rs(1, g) = 0;
+                rs(2, g) = 0;
+                rs(3, g) = depth + 1;
+              }
+            } else {
+              rs(1, f) = 2;
+            }
           }
         }
         __syncthreads();
