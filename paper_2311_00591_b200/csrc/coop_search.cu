@@ -526,27 +526,35 @@ __device__ __forceinline__ void phase1(const PoolView &v, int k0, int n, uint32_
 // The exact R7 tests (the oracle's comparisons; h = c/s) for a chunk with an
 // EVICTABLE item phase 1 could not clear from the encodings: sets nz exactly and rebuilds the
 // chunk's local h^ prefixes with exact h (s from global memory: the stage holds the prefixes).
+struct Settled {
+  uint32_t nz, bad;
+  double hacc;
+};
+// (by value: a reference argument to a non-inlined call would keep the caller's PoolView and
+// flags in local memory on every pool)
 template <int K>
-__device__ __noinline__ void settle_chunk(const PoolView &v, int k0, uint32_t evm, uint32_t &nz,
-                                          bool &bad, double &hacc) {
+__device__ __noinline__ Settled settle_chunk(smem_t *cr, smem_t *hr, const double *sg, int n, int k0,
+                                             uint32_t evm, uint32_t nz) {
+  Settled r{nz, 0u, 0.0};
   double acc = 0.0;
-  for (int q = 0; q < K && k0 + q < v.n; ++q) {
+  for (int q = 0; q < K && k0 + q < n; ++q) {
     const uint32_t o = swz((uint32_t)(k0 + q));
     double h = 0.0;
     if ((evm >> q) & 1u) {
-      const double c = sm<double>(v.cr, o), s = v.sg[k0 + q];
+      const double c = sm<double>(cr, o), s = sg[k0 + q];
       if (!isfinite(c) || !isfinite(s) || c < 0.0 || s < 1.0) {
-        bad = true;
+        r.bad = 1u;
       } else {
         h = __ddiv_rn(c, s);
-        if (h == 0.0) nz &= ~(1u << q);
-        else if (h < 0x1p-64 || h >= 0x1p60) bad = true;
+        if (h == 0.0) r.nz &= ~(1u << q);
+        else if (h < 0x1p-64 || h >= 0x1p60) r.bad = 1u;
       }
     }
-    sm<double>(v.hr, o) = acc;
+    sm<double>(hr, o) = acc;
     acc = __dadd_rn(acc, h);
   }
-  hacc = acc;
+  r.hacc = acc;
+  return r;
 }
 
 // bits 2j of x -> bit j (K <= 16)
@@ -608,7 +616,12 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
   const uint32_t barmask = even_bits((st2 >> 1) & ~st2);  // state 10
   uint32_t nzmask = evmask;  // EVICTABLE items in the clear range have h != 0
   bad |= (badbits != 0u) | zsize | ((st2 & (st2 >> 1) & 0x55555555u) != 0u);  // state 3
-  if (oor) settle_chunk<K>(v, k0, evmask, nzmask, bad, hacc);
+  if (oor) {
+    const Settled st = settle_chunk<K>(v.cr, v.hr, v.sg, n, k0, evmask, nzmask);
+    nzmask = st.nz;
+    bad |= st.bad != 0u;
+    hacc = st.hacc;
+  }
   const int cnt = n - k0;
   const uint32_t valid = cnt >= K ? kFull : (cnt > 0 ? (1u << cnt) - 1u : 0u);
   const uint32_t zm = valid & ~barmask & ~nzmask;  // h = 0 items (FREE, or EVICTABLE with h = 0)
@@ -644,19 +657,6 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     sc.wH[warp] = hinc;
   }
   const int bad_any = cbar_or(bad, T);
-  uint64_t S_car, S_total;
-  {
-    uint64_t ws = lane < W ? sc.wS[lane] : 0ull;
-#pragma unroll
-    for (int d = 1; d < kMaxWarps; d <<= 1) {
-      const uint64_t so = __shfl_up_sync(0xffffffffu, ws, d);
-      if (lane >= d) ws += so;
-    }
-    const uint64_t sprev = __shfl_sync(0xffffffffu, ws, warp ? warp - 1 : 0);
-    S_car = (warp ? sprev : 0ull) + sexc;
-    S_total = __shfl_sync(0xffffffffu, ws, W - 1);
-  }
-  const uint64_t Sk0 = S_car + spre[0];
   if (bad_any || a.dbg == 2) {
     if (tid == 0) write_result(a.out + p, -1, -1, 0, kInf, 0, bad_any ? COOP_ERR_INVALID_ARG : COOP_OK);
     return;
@@ -729,20 +729,29 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     }
     return;
   }
-  // ---------------- phase 2: carries of H^ and of the next-PINNED index -------------------
+  // ---------------- phase 2: carries of S, H^ and of the next-PINNED index ---------------
   int32_t nb_right;
+  uint64_t S_car, S_total;
   {
+    uint64_t ws = lane < W ? sc.wS[lane] : 0ull;
     double wh = lane < W ? sc.wH[lane] : 0.0;
     int32_t wb = lane < W ? sc.wF[lane] : kInfIdx;
 #pragma unroll
     for (int d = 1; d < kMaxWarps; d <<= 1) {
+      const uint64_t so = __shfl_up_sync(0xffffffffu, ws, d);
       const double ho = __shfl_up_sync(0xffffffffu, wh, d);
       const int32_t bo = __shfl_down_sync(0xffffffffu, wb, d);
-      if (lane >= d) wh = __dadd_rn(ho, wh);
+      if (lane >= d) {
+        ws += so;
+        wh = __dadd_rn(ho, wh);
+      }
       if (lane + d < 32) wb = min(wb, bo);
     }
+    const uint64_t sprev = __shfl_sync(0xffffffffu, ws, warp ? warp - 1 : 0);
     const double hprev = __shfl_sync(0xffffffffu, wh, warp ? warp - 1 : 0);
     const int32_t bnext = __shfl_sync(0xffffffffu, wb, min(warp + 1, 31));
+    S_car = (warp ? sprev : 0ull) + sexc;
+    S_total = __shfl_sync(0xffffffffu, ws, W - 1);
     const double H_car = __dadd_rn(warp ? hprev : 0.0, hexc);
     nb_right = min(bexc, warp + 1 < W ? bnext : kInfIdx);
     // S over the raw size words, H^ carries added in place
@@ -764,6 +773,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
   }
   cbar(T);
   if (kPhaseHooks && a.dbg == 3) { if (tid == 0) write_result(a.out + p, -1, -1, 0, 0.0, 0, COOP_OK); return; }
+  const uint64_t Sk0 = S_car + spre[0];
   // ---------------- phase B1: chunk pruning -------------------------------------------
   // Thread t's starts i in [k0, kl] have ends e(i) >= e(k0) (monotone) and prefixes
   // H[i] <= H[kl], so every window cost there is >= H[e(k0)] - H[kl].  e(k0) by one binary
