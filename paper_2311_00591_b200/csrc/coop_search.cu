@@ -937,7 +937,12 @@ __global__ void __launch_bounds__(MAXT, MINB)
   // CTA sees every residue of the pool index modulo G (a periodic mix of short and long
   // requests -- the config-4 law alternates them -- is spread evenly over the CTAs and SMs)
   const int64_t G = gridDim.x;
-  auto pool_of = [&](int64_t k) { return k * G + (int64_t)(((int64_t)blockIdx.x + k) % G); };
+  // (k < G rounds ahead at most: the residue is blockIdx.x + k reduced once or twice)
+  auto pool_of = [&](int64_t k) {
+    int64_t r = (int64_t)blockIdx.x + (k % G);
+    if (r >= G) r -= G;
+    return k * G + r;
+  };
   if (a.use_tma && tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
       const int64_t p = pool_of(s);
@@ -975,11 +980,17 @@ __global__ void __launch_bounds__(MAXT, MINB)
   } else {
     int s = 0;
     uint32_t phase = 0;
-    for (int64_t k = 0;; ++k) {
-      const int64_t p = pool_of(k);
+    // residue of round k, advanced incrementally (no 64-bit division per pool); the next
+    // pool's request is loaded a pool ahead
+    int64_t rk = blockIdx.x, kG = 0;
+    uint64_t Rnext = rk < a.n_pools ? a.req[rk] : 0ull;
+    for (int64_t k = 0;; ++k, kG += G) {
+      const int64_t p = kG + rk;
       if (p >= a.n_pools) break;  // only the last round is partial
       smem_t *stage = base_ptr + (size_t)s * a.stage_bytes;
-      const uint64_t Rraw = a.req[p];
+      const uint64_t Rraw = Rnext;
+      if (++rk == G) rk = 0;
+      if (kG + G + rk < a.n_pools) Rnext = a.req[kG + G + rk];
       if (a.use_tma) {
         mbar_wait(smem_u32(&sc.mbar[s]), phase);
       } else {
