@@ -14,6 +14,15 @@ if which in ("all", "search"):
         out = torch.empty(P * 4, dtype=torch.int64, device=dev)
         coop.window_search_batched(*d, out, P, n, n)
         torch.cuda.synchronize()
+    # ties everywhere (every start a candidate): the re-walk rounds of the rare path
+    n = 600
+    ss = G.pack([8] * n, [G.EVICTABLE] * n)
+    SS, C, S = G.stack_pools([(ss, np.full(n, 0.1), np.ones(n))] * 2)
+    d = [torch.from_numpy(SS.view(np.int64)).to(dev), torch.from_numpy(C).to(dev),
+         torch.from_numpy(S).to(dev), torch.from_numpy(np.array([80, 8 * 500], np.uint64).view(np.int64)).to(dev)]
+    out = torch.empty(2 * 4, dtype=torch.int64, device=dev)
+    coop.window_search_batched(*d, out, 2, n, n)
+    torch.cuda.synchronize()
     print("search ok")
 if which in ("all", "replay"):
     t = coop.Trace(TR.fig2_trace())
