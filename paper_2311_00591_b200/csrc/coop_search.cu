@@ -4,21 +4,22 @@
 // sliding window: the contiguous, PINNED-free run of items with
 // span >= R and the minimum correctly rounded exact sum of h = c/s (R1-R7).
 //
-// Design:
-//   * persistent CTAs (one per SM at N = 4096) loop over pools; a 2-stage ring of
-//     shared-memory buffers is filled by TMA (cp.async.bulk.tensor, SWIZZLE_128B) so the
-//     next pool streams in while the current one is searched; thread t owns K items;
-//   * phase A: h = c/s (IEEE RN), local prefixes of span (u64, exact) and h (fp64),
-//     warp-shuffle + cross-warp scans; the stage is overwritten in place with
-//     S[k] (span prefix), H^[k] (fp64 prefix of h) and h[k] (sign bit = FREE);
-//   * phase B: per start i the window end e(i) = min{e : S[e] - S[i] >= R} by a galloping
-//     two-pointer (cost ~2 log2 of the advance), PINNED and zero-cost checks from
-//     per-thread bit masks, and an fp64 filter C^(i) = H^[e] - H^[i] with a rigorous
-//     error bound (sums of nonnegative terms);
-//   * a window of h = 0 items is exactly optimal (lowest start wins); otherwise every
-//     start whose lower bound can reach the minimum is re-summed EXACTLY in 192-bit
-//     fixed point (fixed192.cuh) and rounded once; winner = lexicographic min of
-//     (rounded cost, first index)  -- bit-identical to the oracle.
+// Design ("Batched search"):
+//   * persistent CTAs (two 256-thread CTAs per SM at N = 4096) loop over pools in rotated
+//     rounds; one shared-memory stage per CTA is filled by TMA (cp.async.bulk.tensor,
+//     SWIZZLE_128B) while the other CTA of the SM computes; thread t owns K items;
+//   * phase 1 (every pool): state codes, R7 validation from the binary64 encodings (the exact
+//     division only for the rare items the exponents cannot clear), local prefixes of span
+//     (u64) and of an approximate h^ = c * rcp(s) (fp64), warp scans;
+//   * zero pass: a run of h = 0 items covering R is exactly optimal (lowest head wins);
+//     short-request pools end here;
+//   * phase 2 + B (the others): S and H^ completed in place; chunk pruning from one
+//     bisection per thread; the surviving starts' ends by galloping and an fp64 filter
+//     C^(i) = H^[e] - H^[i] with a rigorous error bound (sums of nonnegative terms);
+//   * every start whose lower bound can reach the minimum is re-summed EXACTLY (h = c/s by
+//     IEEE division, 192-bit fixed point, fixed192.cuh) and rounded once -- from global
+//     memory, after the stage has been released; winner = lexicographic min of (rounded
+//     cost, first index) -- bit-identical to the oracle.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -71,6 +72,7 @@ struct Scratch {
   int64_t dpool[2];
   int32_t dnc[2], dnext;
   uint32_t dcand[2][kDefMax];
+  uint64_t dspan[2][kDefMax];
   int32_t nplist;                      // pending mode: pools of the chunk to finish
   int16_t plist[kMaxWarps * 32];
 };
@@ -91,9 +93,9 @@ struct Args {
   int32_t stages;
   int32_t use_tma;
   int32_t pending;  // finish only the pools the streaming kernel marked COOP_PENDING_
-  int32_t dbg;  // profiling hook (COOP_SEARCH_DBG): stop each pool after 1 = load, 2 = phase A +
-                // scan + write-back; with -DCOOP_SEARCH_PHASE_HOOKS also 3 = write-back,
-                // 4 = zero pass, 5 = pruning + compaction, 6 = filter + reductions
+  int32_t dbg;  // profiling hook (COOP_SEARCH_DBG): stop each pool after 1 = load, 2 = phase 1;
+                // with -DCOOP_SEARCH_PHASE_HOOKS also 4 = zero pass, 3 = phase 2, 5 = pruning +
+                // compaction, 6 = filter + reductions
   double gerr;  // filter error coefficient: |C^ - C| <= gerr * (H^[e] + H^[i])
 };
 
@@ -266,26 +268,17 @@ __device__ __forceinline__ double rcp_nr(double s) {
 // the span.  SMEM = false: everything from global memory (deferred re-summations: the stage
 // holds another pool by then; the lines were prefetched into L1); SMEM = true: exact h from
 // region 1 (converted in place by exact_h_in_place) and the states from the chunk masks.
-template <bool SMEM, int K>
-__device__ __forceinline__ void window_sum(const Args &a, const PoolView *v, int64_t p, int i,
-                                           int e, int off, int step, U192 &acc, uint64_t &span,
-                                           int &nev) {
+template <bool SMEM, bool GSPAN, int K>
+__device__ __forceinline__ void window_sum(const Args &a, const PoolView *v, const uint16_t *evc, int64_t p,
+                                           int i, int e, int off, int step, U192 &acc,
+                                           uint64_t &span, int &nev) {
   const uint64_t *ss = a.ss + p * a.stride;
   const double *cg = a.cost + p * a.stride, *sg = a.stale + p * a.stride;
   for (int k = i + off; k < e; k += step) {
-    if (SMEM) {
-      if ((v->evc[k / K] >> (k % K)) & 1u) {
-        acc = u192_add(acc, u192_from_double(v->c_at(k)));
-        ++nev;
-      }
-    } else {
-      const uint64_t w = __ldg(ss + k);
-      const double c = __ldg(cg + k), s = __ldg(sg + k);
-      span += w & kSizeMask;
-      if ((w >> 62) == COOP_EVICTABLE) {
-        acc = u192_add(acc, u192_from_double(__ddiv_rn(c, s)));
-        ++nev;
-      }
+    if (GSPAN) span += __ldg(ss + k) & kSizeMask;
+    if ((evc[k / K] >> (k % K)) & 1u) {  // EVICTABLE (the chunk masks of this pool)
+      acc = u192_add(acc, u192_from_double(SMEM ? v->c_at(k) : __ddiv_rn(__ldg(cg + k), __ldg(sg + k))));
+      ++nev;
     }
   }
 }
@@ -302,9 +295,11 @@ __device__ __forceinline__ void warp_sum_all(U192 &acc, uint64_t &span, int &nev
 
 // The exact re-summation of the candidate windows sc.cand[0, nc) of pool p by the whole CTA
 // and the pool's result: the lexicographic (rounded exact cost bits, first) minimum.
+// spans: the candidates' spans when known (taken from S before the stage was released), else
+// summed from the global size words
 template <bool SMEM, int K>
 __device__ __forceinline__ void verify_pool(const Args &a, const PoolView *v, Scratch &sc, int64_t p,
-                                            const uint32_t *cand, int nc, int T) {
+                                            const uint32_t *cand, const uint64_t *spans, int nc, int T) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
   uint64_t best = ~0ull, bspan = 0;  // meaningful in thread 0
   int bfirst = kInfIdx, bend = -1, bnev = 0;
@@ -317,7 +312,8 @@ __device__ __forceinline__ void verify_pool(const Args &a, const PoolView *v, Sc
       uint64_t span = 0;
       int nev = 0;
       if (i + warp * 32 < e) {  // warp-uniform: warps without items skip
-        window_sum<SMEM, K>(a, v, p, i, e, tid, T, acc, span, nev);
+        if (spans) window_sum<SMEM, false, K>(a, v, sc.evc, p, i, e, tid, T, acc, span, nev);
+        else window_sum<SMEM, true, K>(a, v, sc.evc, p, i, e, tid, T, acc, span, nev);
         warp_sum_all(acc, span, nev);
       }
       const int par = c & 1;
@@ -347,7 +343,7 @@ __device__ __forceinline__ void verify_pool(const Args &a, const PoolView *v, Sc
           bfirst = i;
           bend = e;
           bnev = tn;
-          bspan = tsp;
+          bspan = spans ? spans[c] : tsp;
         }
       }
     }
@@ -361,7 +357,8 @@ __device__ __forceinline__ void verify_pool(const Args &a, const PoolView *v, Sc
       U192 acc = u192_zero();
       uint64_t span = 0;
       int nev = 0;
-      window_sum<SMEM, K>(a, v, p, i, e, lane, 32, acc, span, nev);
+      if (spans) window_sum<SMEM, false, K>(a, v, sc.evc, p, i, e, lane, 32, acc, span, nev);
+      else window_sum<SMEM, true, K>(a, v, sc.evc, p, i, e, lane, 32, acc, span, nev);
       warp_sum_all(acc, span, nev);
       const uint64_t cb = (uint64_t)__double_as_longlong(u192_round_to_double(acc));
       if (better(cb, i, wbest, wfirst)) {
@@ -369,7 +366,7 @@ __device__ __forceinline__ void verify_pool(const Args &a, const PoolView *v, Sc
         wfirst = i;
         wend = e;
         wnev = nev;
-        wspan = span;
+        wspan = spans ? spans[c] : span;
       }
     }
     if (lane == 0) {
@@ -856,7 +853,12 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     // deferred until this CTA has released the stage and issued the next TMA load (an L1 /
     // L2 prefetch of the windows' lines measured slower)
     const int nc = sc.ncand, slot = sc.dnext;
-    if (tid < nc) sc.dcand[slot][tid] = sc.cand[tid];
+    if (tid < nc) {
+      const uint32_t cd = sc.cand[tid];
+      const int i = (int)(cd >> 16), e = i + (int)(cd & 0xffffu);
+      sc.dcand[slot][tid] = cd;
+      sc.dspan[slot][tid] = v.S_at(e) - v.S_at(i);
+    }
     if (tid == 0) {
       sc.dpool[slot] = p;
       sc.dnc[slot] = nc;
@@ -877,7 +879,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
   }
   cbar(T);
   if (!any_multi) {
-    verify_pool<true, K>(a, &v, sc, p, sc.cand, sc.ncand, T);
+    verify_pool<true, K>(a, &v, sc, p, sc.cand, nullptr, sc.ncand, T);
     return;
   }
   const bool wmulti = __any_sync(0xffffffffu, bl.L <= thresh);  // this warp holds candidates
@@ -895,7 +897,7 @@ __device__ __forceinline__ void search_pool(const Args &a, Scratch &sc, uint4 *E
     cbar(T);
     const int nc = min(sc.ncand, kCandCap);
     if (nc == 0) continue;
-    verify_pool<true, K>(a, &v, sc, p, sc.cand, nc, T);  // writes this round's best into out[p]
+    verify_pool<true, K>(a, &v, sc, p, sc.cand, nullptr, nc, T);  // writes this round's best into out[p]
     if (tid == 0) {
       const coop_window r = a.out[p];
       const uint64_t cb = (uint64_t)__double_as_longlong(r.cost);
@@ -972,7 +974,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
         cbar(T);
         const int slot = sc.dnext;  // keep a slot free for the next deferral
         if (sc.dpool[slot] >= 0) {
-          verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dnc[slot], T);
+          verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dspan[slot], sc.dnc[slot], T);
           if (tid == 0) sc.dpool[slot] = -1;
         }
       }
@@ -1013,7 +1015,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
       {
         const int slot = sc.dnext ^ 1;
         if (sc.dpool[slot] >= 0) {
-          verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dnc[slot], T);
+          verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dspan[slot], sc.dnc[slot], T);
           if (tid == 0) sc.dpool[slot] = -1;
         }
       }
@@ -1025,7 +1027,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
   }
   for (int slot = 0; slot < 2; ++slot) {  // the last deferred re-summations
     cbar(T);
-    if (sc.dpool[slot] >= 0) verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dnc[slot], T);
+    if (sc.dpool[slot] >= 0) verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dspan[slot], sc.dnc[slot], T);
   }
 }
 

@@ -121,7 +121,9 @@ COOP_HD bool u192_any_below(U192 a, int pos) {
 
 COOP_HD double scale2(double x, int e) {  // x * 2^e, exact for the ranges used here
 #ifdef __CUDA_ARCH__
-  return scalbn(x, e);
+  // 2^e built from its encoding (e in [-1022, 1023]: every use here is a normal power of two),
+  // one exact multiply instead of the library scalbn
+  return x * __hiloint2double((e + 1023) << 20, 0);
 #else
   return __builtin_scalbn(x, e);
 #endif
