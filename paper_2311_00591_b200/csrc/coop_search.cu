@@ -1005,7 +1005,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       cbar(T);  // stage s fully consumed
       if (a.use_tma && tid == 0) {
-        const int64_t pn = pool_of(k + a.stages);
+        // round k + stages: rk is already round k + 1's residue (stages is 1 or 2)
+        int64_t rn = rk + (a.stages - 1);
+        if (rn >= G) rn -= G;
+        const int64_t pn = kG + (int64_t)a.stages * G + rn;
         if (pn < a.n_pools)
           issue_stage(a, &m_ss, &m_c, &m_s, base + (uint32_t)s * a.stage_bytes,
                       smem_u32(&sc.mbar[s]), pn);
