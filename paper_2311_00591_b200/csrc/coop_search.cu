@@ -69,6 +69,7 @@ struct Scratch {
   unsigned long long mbar[2];
   // deferred exact re-summations (two slots: the newest and an older one): pool (-1: none),
   // candidate count and windows; dnext = the slot the next deferral uses
+  int32_t swap;  // 1: this CTA visits its rounds in pair-swapped order (k = j ^ 1)
   int64_t dpool[2];
   int32_t dnc[2], dnext;
   uint32_t dcand[2][kDefMax];
@@ -76,6 +77,10 @@ struct Scratch {
   int32_t nplist;                      // pending mode: pools of the chunk to finish
   int16_t plist[kMaxWarps * 32];
 };
+
+// per-SM launch counters: which of the two CTAs on an SM this one is (see the round order in
+// search_kernel; a wrong guess only costs balance, never correctness)
+__device__ unsigned int g_smcnt[1024];
 
 struct Args {
   const uint64_t *ss;
@@ -932,6 +937,11 @@ __global__ void __launch_bounds__(MAXT, MINB)
     for (int s = 0; s < a.stages; ++s) mbar_init(smem_u32(&sc.mbar[s]), 1);
     sc.dpool[0] = sc.dpool[1] = -1;
     sc.dnext = 0;
+    {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      sc.swap = (int)(atomicAdd(&g_smcnt[smid & 1023u], 1u) & 1u);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cbar(T);
@@ -945,7 +955,8 @@ __global__ void __launch_bounds__(MAXT, MINB)
     if (r >= G) r -= G;
     return k * G + r;
   };
-  if (a.use_tma && tid == 0) {
+  const bool paired = a.use_tma && a.stages == 1 && !a.pending;
+  if (a.use_tma && tid == 0 && !paired) {
     for (int s = 0; s < a.stages; ++s) {
       const int64_t p = pool_of(s);
       if (p < a.n_pools)
@@ -978,6 +989,52 @@ __global__ void __launch_bounds__(MAXT, MINB)
           if (tid == 0) sc.dpool[slot] = -1;
         }
       }
+    }
+  } else if (paired) {
+    // one stage per CTA, two CTAs per SM: the CTA visits its rounds k = j ^ swap, where the
+    // second CTA to arrive on an SM swaps each pair of rounds -- with the rotated residues
+    // (b + k) mod G the pool parity then differs between the two CTAs of an SM in every step
+    // (the config-4 law alternates short and long requests by parity), so one CTA's
+    // latency-bound phases of a long-request pool meet the other's throughput-bound phase 1
+    const int64_t J = (a.n_pools + G - 1) / G + 1;
+    const int64_t sw = sc.swap;
+    auto pof = [&](int64_t j) -> int64_t {
+      const int64_t k = j ^ sw;
+      const uint32_t r = ((uint32_t)blockIdx.x + (uint32_t)k) % (uint32_t)G;  // k < 2^31
+      return k * G + r;
+    };
+    int64_t j = 0;
+    while (j < J && pof(j) >= a.n_pools) ++j;
+    int64_t p = j < J ? pof(j) : -1;
+    if (tid == 0 && p >= 0) issue_stage(a, &m_ss, &m_c, &m_s, base, smem_u32(&sc.mbar[0]), p);
+    uint64_t Rnext = p >= 0 ? a.req[p] : 0ull;
+    uint32_t phase = 0;
+    while (p >= 0) {
+      int64_t jn = j + 1, pn = -1;
+      for (; jn < J; ++jn) {
+        const int64_t q = pof(jn);
+        if (q < a.n_pools) {
+          pn = q;
+          break;
+        }
+      }
+      const uint64_t Rraw = Rnext;
+      if (pn >= 0) Rnext = a.req[pn];
+      mbar_wait(smem_u32(&sc.mbar[0]), phase);
+      search_pool<K>(a, sc, Ebuf, base_ptr, p, Rraw);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      cbar(T);  // the stage fully consumed
+      if (tid == 0 && pn >= 0) issue_stage(a, &m_ss, &m_c, &m_s, base, smem_u32(&sc.mbar[0]), pn);
+      {
+        const int slot = sc.dnext ^ 1;
+        if (sc.dpool[slot] >= 0) {
+          verify_pool<false, K>(a, nullptr, sc, sc.dpool[slot], sc.dcand[slot], sc.dspan[slot], sc.dnc[slot], T);
+          if (tid == 0) sc.dpool[slot] = -1;
+        }
+      }
+      phase ^= 1u;
+      j = jn;
+      p = pn;
     }
   } else {
     int s = 0;
