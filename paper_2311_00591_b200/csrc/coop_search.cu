@@ -6,8 +6,10 @@
 //
 // Design ("Batched search"):
 //   * persistent CTAs (two 256-thread CTAs per SM at N = 4096) loop over pools in rotated
-//     rounds; one shared-memory stage per CTA is filled by TMA (cp.async.bulk.tensor,
-//     SWIZZLE_128B) while the other CTA of the SM computes; thread t owns K items;
+//     rounds (the second CTA of an SM in pair-swapped order, so the two alternate short- and
+//     long-request pools); one shared-memory stage per CTA is filled by TMA
+//     (cp.async.bulk.tensor, SWIZZLE_128B) while the other CTA of the SM computes; thread t
+//     owns K items;
 //   * phase 1 (every pool): state codes, R7 validation from the binary64 encodings (the exact
 //     division only for the rare items the exponents cannot clear), local prefixes of span
 //     (u64) and of an approximate h^ = c * rcp(s) (fp64), warp scans;
