@@ -519,15 +519,16 @@ static int replay_on_device(coop_trace_t t, const uint64_t *budgets, int32_t n_b
   int helper = 0;
   if (walkers > 0) {
     const char *henv = getenv("COOP_REPLAY_HELPER");
-    // helpers per cell, 0..3.  Default (measured on B200): none for traces below 4096
+    // helpers per cell, 0..7.  Default (measured on B200): none for traces below 4096
     // tensors (their closures are short: ResNet-50 loses more to the per-event cluster
     // barriers than it gains); for larger traces 1 when the cells fill a quarter to half of
     // the SMs (all of them then still run at once: config 3, 64 GPT-3 cells on 128 SMs), else
-    // 3 (a sweep's time is its slowest cell: the BiLSTM 256-cell sweep 50 -> 31 / 23 / 20 s
-    // with 1 / 2 / 3 helpers)
+    // 7 (a sweep's time is its slowest cell: the BiLSTM 256-cell sweep 50 -> 31 / 23 / 20 /
+    // 18.5 / 18.1 s with 1 / 2 / 3 / 5 / 7 helpers; a GPT-3 256-cell sweep alone pays for the
+    // extra waves, 446 -> 733 ms, hidden under BiLSTM in config 5)
     if (henv) helper = std::max(0, std::min(kMaxCluster - 1, atoi(henv)));
     else if (t->T >= 4096)
-      helper = ((int64_t)n_budgets * 4 > (int64_t)sms && (int64_t)n_budgets * 2 <= (int64_t)sms) ? 1 : 3;
+      helper = ((int64_t)n_budgets * 4 > (int64_t)sms && (int64_t)n_budgets * 2 <= (int64_t)sms) ? 1 : 7;
   }
   int max_clusters = 0;
   if (helper) {

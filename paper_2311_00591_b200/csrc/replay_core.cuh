@@ -25,7 +25,7 @@ constexpr int kRsm = 64;         // of which held in shared memory
 constexpr int kFree = -1;
 constexpr int kOpChunk = 32;   // replay: trace ops whose records are staged in shared memory at once
 constexpr int kListCap = 384;  // their input / death / lock lists staged with them (else read from L2)
-constexpr int kMaxCluster = 4;  // replay: CTAs per cell (the leader + up to 3 closure helpers)
+constexpr int kMaxCluster = 8;  // replay: CTAs per cell (the leader + up to 7 closure helpers)
 constexpr int kRing = 2048;    // replay warp BFS: per-warp queue ring (uint16 entries, shared memory)
 constexpr int kGL = 8;         // replay group BFS: lanes per group (4 groups per warp)
 constexpr int kGroups = kThreads / kGL;

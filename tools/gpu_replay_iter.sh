@@ -6,5 +6,5 @@ import json
 d=json.load(open('gpurun_out/bench_replay.json'))
 for k,v in d['replay'].items():
     if isinstance(v,dict) and 'ms_per_sweep' in v:
-        print(k, round(v['ms_per_sweep'],2), 'oracle', round(v.get('oracle_ms_per_sweep') or 0,2), 'x', round(v.get('gpu_vs_oracle') or 0,3), 'mism', v['parity']['mismatches'])
+        print(k, round(v['ms_per_sweep'],2), 'oracle', round(v.get('oracle_ms_per_sweep') or 0,2), 'x', round(v.get('gpu_vs_oracle') or 0,3), 'mism', (v.get('parity') or {}).get('mismatches'))
 PY
