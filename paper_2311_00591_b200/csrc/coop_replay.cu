@@ -31,6 +31,12 @@
 namespace coop {
 namespace {
 
+// a cluster's helper CTA (rank >= 1): its own CellT
+__device__ __forceinline__ void helper_entry(const KArgs &a, Shared &sh, int slot, int rank) {
+  CellT<true> c(a, sh, -1, slot, rank);
+  c.cluster_helper();
+}
+
 __global__ void __launch_bounds__(kThreads, 1) replay_kernel(const KArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   Shared &sh = *reinterpret_cast<Shared *>(smem);
@@ -46,33 +52,33 @@ __global__ void __launch_bounds__(kThreads, 1) replay_kernel(const KArgs a) {
     for (int i = threadIdx.x; i < nbm * a.vis_words; i += kThreads) v[i] = 0u;
     __syncthreads();
   }
-  if (!a.helper) {
-    for (int cell = blockIdx.x; cell < a.n_cells; cell += gridDim.x) {
-      CellT<true> c(a, sh, cell);
-      c.run(a.budgets[cell]);
-      if (threadIdx.x == 0) a.out[cell] = sh.res;
-      __syncthreads();
-    }
-    return;
-  }
-  // clusters of two CTAs: rank 0 replays the cells of the cluster, rank 1 helps with the
-  // projected-cost closures of every pressure event (CellT::cluster_helper)
-  cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+  // clusters (a.helper > 0): rank 0 replays the cells of the cluster, the other ranks help
+  // with the projected-cost closures of every pressure event (CellT::cluster_helper).  ONE
+  // call site of CellT::run, so that it is inlined and the cell's state stays in registers
+  // (two call sites made it a real call: the whole CellT on the stack, every member access
+  // a local load -- config 2 10.4 -> 13.4 ms)
   const int csize = a.helper + 1;
-  const int slot = (int)blockIdx.x / csize, nslots = (int)gridDim.x / csize;
-  if (cl.block_rank() == 0) {
-    for (int cell = slot; cell < a.n_cells; cell += nslots) {
-      CellT<true> c(a, sh, cell, slot);
-      c.run(a.budgets[cell]);
-      if (threadIdx.x == 0) a.out[cell] = sh.res;
-      __syncthreads();
+  int slot = (int)blockIdx.x, nslots = (int)gridDim.x;
+  if (a.helper) {
+    const int rank = (int)cooperative_groups::this_cluster().block_rank();
+    slot = (int)blockIdx.x / csize;
+    nslots = (int)gridDim.x / csize;
+    if (rank != 0) {
+      helper_entry(a, sh, slot, rank);
+      return;
     }
+  }
+  for (int cell = slot; cell < a.n_cells; cell += nslots) {
+    CellT<true> c(a, sh, cell, a.helper ? slot : -1);
+    c.run(a.budgets[cell]);
+    if (threadIdx.x == 0) a.out[cell] = sh.res;
+    __syncthreads();
+  }
+  if (a.helper) {
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
     if (threadIdx.x == 0) sh.helper_cmd = 2;  // exit
     cl.sync();  // A
-    cl.sync();  // the helper has read the command
-  } else {
-    CellT<true> c(a, sh, -1, slot, (int)cl.block_rank());
-    c.cluster_helper();
+    cl.sync();  // the helpers have read the command
   }
 }
 

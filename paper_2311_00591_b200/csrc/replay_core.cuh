@@ -1296,7 +1296,7 @@ struct CellT {
     allocate_with(op, t, tr.size[t], tr.src[op], goes_right(op), allow_inplace, kind);
   }
   // the same with the op's fields already at hand (the replay's staged op records)
-  __device__ void allocate_with(int op, int t, uint64_t need, int src, bool right, bool allow_inplace, int kind) {
+  __device__ __forceinline__ void allocate_with(int op, int t, uint64_t need, int src, bool right, bool allow_inplace, int kind) {
     if (allow_inplace && src >= 0 && (a.flags & COOP_F_INPLACE)) {  // addr <- input.addr
       const uint64_t ad = w.taddr[src];
       const int b = block_of_addr(ad);
